@@ -1,0 +1,61 @@
+"""Seeded synthetic inputs for the BASELINE.json configs.
+
+The reference publishes no dataset: every config is a synthetic decay matrix
+defined by formula, so these generators stand in for the inputs exactly.
+Recipe (the same arrays feed the CPU oracle and the GPU path):
+
+* u = numpy PCG64 ``default_rng(seed).uniform(-1.0, 1.0, size=(n, n))``
+* d = |i - j| as float64
+* exponential decay ``u * lam**d``; algebraic decay ``u / (d**lam + 1)``
+* symmetrisation ``0.5 * (A + A.T)``
+
+Seeds: 0 for A, 1 for an independent B (BASELINE.json pins seeds for
+config 1 only; SURVEY.md §8(d) states the same choice for the others).
+Host-side numpy only -- input preparation, not the hot path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def _distance(n):
+    idx = np.arange(n, dtype=np.float64)
+    return np.abs(idx[:, None] - idx[None, :])
+
+
+def uniform(n, seed):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n, n))
+
+
+def exponential_decay(n, lam, seed, symmetric=False):
+    """A_ij = u_ij * lam**|i-j| (BASELINE.json configs 1, 2, 5)."""
+    a = uniform(n, seed) * np.power(lam, _distance(n))
+    return 0.5 * (a + a.T) if symmetric else a
+
+
+def algebraic_decay(n, lam, seed, symmetric=True):
+    """A_ij = u_ij / (|i-j|**lam + 1) (BASELINE.json config 3)."""
+    a = uniform(n, seed) / (np.power(_distance(n), lam) + 1.0)
+    return 0.5 * (a + a.T) if symmetric else a
+
+
+# name -> (n, leaf, taus, builder returning (A, B))
+CONFIGS = {
+    "c1": dict(n=1024, leaf=32, taus=(1e-6,),
+               make=lambda: (exponential_decay(1024, 0.9, 0), exponential_decay(1024, 0.9, 1))),
+    "c2": dict(n=4096, leaf=64, taus=(1e-4, 1e-6, 1e-8, 1e-10),
+               make=lambda: (lambda a: (a, a))(exponential_decay(4096, 0.95, 0, symmetric=True))),
+    "c3_l2": dict(n=8192, leaf=64, taus=(1e-6, 1e-8),
+                  make=lambda: (algebraic_decay(8192, 2.0, 0), algebraic_decay(8192, 2.0, 1))),
+    "c3_l3": dict(n=8192, leaf=64, taus=(1e-6, 1e-8),
+                  make=lambda: (algebraic_decay(8192, 3.0, 0), algebraic_decay(8192, 3.0, 1))),
+    "c5": dict(n=65536, leaf=64, taus=(1e-8,),
+               make=lambda: (lambda a: (a, a))(exponential_decay(65536, 0.98, 0, symmetric=True))),
+}
+
+
+def make_config(name):
+    cfg = CONFIGS[name]
+    a, b = cfg["make"]()
+    return a, b, cfg["leaf"], cfg["taus"]
