@@ -1,0 +1,143 @@
+/*
+ * spamm_b200.h -- C ABI of the B200-native SpAMM hot path.
+ *
+ * Plain pointers, sizes and opaque handles only (no torch or CUDA types in
+ * the signatures).  Every entry point returns SPAMM_OK (0) or an error code
+ * and records a message retrievable with spamm_last_error() (thread-local).
+ * Calls are synchronous from the caller's point of view: results are ready
+ * on return.  Trees are immutable after construction and safe to share
+ * between concurrent readers; calls that touch the same device serialise on
+ * a per-device lock.
+ *
+ * Reference interfaces replaced (arxiv/paper_1011_3534, pkg/src/spamm):
+ *   spamm_tree_from_host      <- quadtree.from_dense          quadtree.py:218-251
+ *                                (+ QuadTreeMatrix.__init__    quadtree.py:116-151)
+ *   spamm_tree_to_host        <- QuadTreeMatrix.to_dense      quadtree.py:184-187, :264-266
+ *   spamm_tree_padded_to_host <- QuadTreeMatrix._padded       quadtree.py:145
+ *   spamm_tree_pyramid_to_host<- QuadTreeMatrix._norm_sq / _occupied  quadtree.py:131-138
+ *   spamm_tree_info_get       <- logical_dim/leaf_size/depth/padded_dim/dtype, norm()
+ *                                                              quadtree.py:95-162, :189-191
+ *   spamm_multiply            <- multiply.spamm               multiply.py:144-221
+ *                                (_leaf_stage :224-257, _merge_contributions :119-141)
+ *   spamm_stats               <- multiply.ProductStats        multiply.py:93-116
+ *   spamm_product_boxes       <- ProductStats.boxes / PrunedBox multiply.py:77-90, :214-218
+ *   spamm_tree_diff_norm      <- the dense norm in multiply_error  multiply.py:276
+ *   spamm_multiply_rows       <- (new) output block-row shard of spamm for multi-GPU
+ *                                partitioning; the reference is single-process.
+ */
+#ifndef SPAMM_B200_H
+#define SPAMM_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SPAMM_API __attribute__((visibility("default")))
+#else
+#define SPAMM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define SPAMM_OK 0
+#define SPAMM_ERR_VALUE 1     /* -> ValueError                       */
+#define SPAMM_ERR_DIMENSION 2 /* -> DimensionMismatchError(ValueError) */
+#define SPAMM_ERR_CUDA 3      /* -> RuntimeError (CUDA failure)       */
+#define SPAMM_ERR_NOMEM 4     /* -> MemoryError                       */
+#define SPAMM_ERR_INTERNAL 5  /* -> RuntimeError                      */
+
+/* element storage types (quadtree.py:18 _SUPPORTED_DTYPES) */
+#define SPAMM_DTYPE_F64 0
+#define SPAMM_DTYPE_F32 1
+
+/* spamm_multiply flags (SpammConfig, multiply.py:43-74) */
+#define SPAMM_COLLECT_BOXES 0x1u  /* record a PrunedBox per tau-pruned call  */
+#define SPAMM_COUNT_STATS 0x2u    /* maintain the ProductStats counters       */
+#define SPAMM_TIER_TAU_DECAY 0x4u /* prune tier t against tau / 8**t          */
+#define SPAMM_KEEP_TRIPLES 0x8u   /* keep the retained leaf (i,j,k) list      */
+
+typedef struct spamm_tree spamm_tree;
+typedef struct spamm_product spamm_product;
+
+typedef struct {
+  int64_t logical_dim; /* n                                   */
+  int64_t padded_dim;  /* N = leaf_size << depth              */
+  int64_t block_grid;  /* N / leaf_size                       */
+  int32_t leaf_size;
+  int32_t depth;
+  int32_t dtype;       /* SPAMM_DTYPE_*                        */
+  int32_t device;      /* CUDA ordinal holding the tree        */
+  double root_norm_sq; /* _norm_sq[0][0, 0]                    */
+} spamm_tree_info;
+
+typedef struct {
+  int64_t leaf_matmuls;
+  int64_t pruned_calls;
+  int64_t pruned_volume;
+  int64_t empty_skip_volume;
+  int32_t max_depth_reached;
+  int32_t reserved0;
+  double omitted_budget;
+  int64_t n_boxes;   /* number of PrunedBox records (if collected)   */
+  int64_t n_triples; /* retained leaf triples (== leaf_matmuls)      */
+  int64_t n_groups;  /* C blocks with at least one retained triple   */
+  int64_t tier_candidates[32];
+  int64_t tier_survivors[32];
+  int64_t tier_pruned[32];
+  /* device-event timings of the last call, milliseconds */
+  float ms_cull;
+  float ms_leaf;
+  float ms_ctree;
+  float ms_total;
+} spamm_stats;
+
+SPAMM_API const char *spamm_last_error(void);
+SPAMM_API int spamm_device_count(int *count);
+/* Library build identity, e.g. "spamm_b200 0.1 sm_100a". */
+SPAMM_API const char *spamm_version(void);
+
+/* -- trees ---------------------------------------------------------------- */
+SPAMM_API int spamm_tree_from_host(const void *host, int64_t n, int64_t ld, int32_t leaf_size,
+                         int32_t dtype, int32_t device, spamm_tree **out);
+/* `dev` is a device pointer on `device`; n x n with leading dimension ld. */
+SPAMM_API int spamm_tree_from_device(const void *dev, int64_t n, int64_t ld, int32_t leaf_size,
+                           int32_t dtype, int32_t device, spamm_tree **out);
+/* Adopt an already padded N x N device array (copied), rebuild its pyramid. */
+SPAMM_API int spamm_tree_from_padded_device(const void *dev_padded, int64_t n, int64_t padded_dim,
+                                  int32_t leaf_size, int32_t dtype, int32_t device,
+                                  spamm_tree **out);
+SPAMM_API int spamm_tree_info_get(const spamm_tree *t, spamm_tree_info *info);
+SPAMM_API int spamm_tree_to_host(const spamm_tree *t, void *host, int64_t ld);
+SPAMM_API int spamm_tree_padded_to_host(const spamm_tree *t, void *host);
+/* nsq: (4^(depth+1)-1)/3 doubles, occ: same count of bytes; level k
+ * (2^k x 2^k row-major) starts at (4^k - 1)/3. */
+SPAMM_API int spamm_tree_pyramid_to_host(const spamm_tree *t, double *nsq, uint8_t *occ);
+/* Raw device pointers (borrowed) for collective plumbing. */
+SPAMM_API int spamm_tree_device_ptrs(const spamm_tree *t, void **padded, double **nsq, uint8_t **occ);
+/* ||A - B||_F computed on the device (multiply_error, multiply.py:276). */
+SPAMM_API int spamm_tree_diff_norm(const spamm_tree *a, const spamm_tree *b, double *out);
+SPAMM_API void spamm_tree_free(spamm_tree *t);
+
+/* -- multiply --------------------------------------------------------------- */
+SPAMM_API int spamm_multiply(const spamm_tree *a, const spamm_tree *b, double tau, uint32_t flags,
+                   spamm_tree **c, spamm_stats *stats, spamm_product **product);
+/* Shard of spamm_multiply restricted to C leaf block rows [row_lo, row_hi):
+ * only triples whose leaf rows intersect the range are traversed; pruned and
+ * skipped calls are counted by the shard owning the call's first row, so the
+ * per-shard integer stats sum exactly to the unsharded ones.  C holds only
+ * the shard's rows (others +0.0); its pyramid covers those rows. */
+SPAMM_API int spamm_multiply_rows(const spamm_tree *a, const spamm_tree *b, double tau, uint32_t flags,
+                        int64_t row_lo, int64_t row_hi, spamm_tree **c, spamm_stats *stats,
+                        spamm_product **product);
+/* boxes: 5 int64 per box (i_lo, j_lo, k_lo, edge, tier) in reference order. */
+SPAMM_API int spamm_product_boxes(const spamm_product *p, int64_t *out, int64_t capacity);
+/* triples: 3 int32 per retained leaf product (i, j, k), sorted by (i, j, k). */
+SPAMM_API int spamm_product_triples(const spamm_product *p, int32_t *out, int64_t capacity);
+SPAMM_API void spamm_product_free(spamm_product *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPAMM_B200_H */

@@ -1,0 +1,123 @@
+// common.cuh -- shared device/host helpers for the SpAMM B200 library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "spamm_b200.h"
+
+namespace spamm {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char *fmt, ...);
+
+struct Status {
+  int code = SPAMM_OK;
+};
+
+#define SPAMM_CUDA_TRY(expr)                                                              \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      ::spamm::set_error("CUDA error %s (%s) at %s:%d", cudaGetErrorName(_e),             \
+                         cudaGetErrorString(_e), __FILE__, __LINE__);                     \
+      return _e == cudaErrorMemoryAllocation ? SPAMM_ERR_NOMEM : SPAMM_ERR_CUDA;          \
+    }                                                                                     \
+  } while (0)
+
+#define SPAMM_TRY(expr)              \
+  do {                               \
+    int _s = (expr);                 \
+    if (_s != SPAMM_OK) return _s;   \
+  } while (0)
+
+// ------------------------------------------------------------ pyramid layout
+// Level k (2^k x 2^k, row-major) of the norm / occupancy pyramid starts at
+// (4^k - 1) / 3 in one concatenated array (the reference keeps a Python list
+// of per-level arrays, quadtree.py:131-138).
+__host__ __device__ inline int64_t level_offset(int k) {
+  return ((int64_t(1) << (2 * k)) - 1) / 3;
+}
+inline int64_t pyramid_size(int depth) { return level_offset(depth + 1); }
+
+inline int depth_for(int64_t n, int32_t leaf) {
+  int d = 0;
+  while ((int64_t(leaf) << d) < n) ++d;
+  return d;
+}
+
+// ----------------------------------------------------------------- Morton
+// A product-space triple (i, j, k) at tier t is kept as its Morton code:
+// bits (3s+2, 3s+1, 3s) hold bit s of (i, j, k).  Children of code c are
+// 8c + (di<<2 | dj<<1 | dk), which is exactly the reference's (di,dj,dk)
+// expansion order 000..111 (multiply.py:35-37), so a tier's candidate list
+// stays in the reference's order.
+__host__ __device__ inline uint64_t compact3(uint64_t x) {
+  x &= 0x1249249249249249ull;
+  x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ull;
+  x = (x ^ (x >> 4)) & 0x100f00f00f00f00full;
+  x = (x ^ (x >> 8)) & 0x1f0000ff0000ffull;
+  x = (x ^ (x >> 16)) & 0x1f00000000ffffull;
+  x = (x ^ (x >> 32)) & 0x1fffffull;
+  return x;
+}
+__host__ __device__ inline void morton_decode(uint64_t code, uint32_t &i, uint32_t &j,
+                                              uint32_t &k) {
+  i = (uint32_t)compact3(code >> 2);
+  j = (uint32_t)compact3(code >> 1);
+  k = (uint32_t)compact3(code);
+}
+
+// ------------------------------------------------------------ device context
+// One per CUDA device: a non-blocking stream, a lock serialising calls on
+// that device, and grow-only scratch reused across multiplies.
+struct Scratch {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct DeviceContext {
+  int device = -1;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  std::mutex mu;
+  Scratch cull_codes[2];  // ping-pong survivor lists (u64 Morton codes)
+  Scratch pruned_codes;   // pruned codes, all tiers (u64)
+  Scratch pruned_vals;    // pruned norm products, all tiers (f64)
+  Scratch tile_status;    // decoupled look-back state
+  Scratch counters;       // device counters (CullCounters)
+  Scratch keys[2];        // leaf triple sort keys (u64) + alt buffer
+  Scratch group_starts;   // first triple of each C block group
+  Scratch flags;          // head flags / misc bytes
+  Scratch cub_temp;       // cub temporary storage
+  Scratch reduce_tmp;     // misc reduction scratch
+  size_t cull_capacity = 0;   // survivor capacity per ping-pong buffer (items)
+  size_t pruned_capacity = 0; // pruned capacity (items, all tiers)
+  void *host_pinned = nullptr;  // small pinned staging for counters
+};
+
+int get_context(int device, DeviceContext **ctx);
+int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream);
+
+}  // namespace spamm
+
+struct spamm_tree {
+  int64_t n = 0;        // logical_dim
+  int64_t N = 0;        // padded_dim
+  int64_t nb = 0;       // block_grid
+  int32_t leaf = 0;
+  int32_t depth = 0;
+  int32_t dtype = SPAMM_DTYPE_F64;
+  int32_t device = 0;
+  void *padded = nullptr;   // N x N row-major, element type per dtype
+  double *nsq = nullptr;    // concatenated squared-norm pyramid
+  uint8_t *occ = nullptr;   // concatenated occupancy pyramid
+  double root_norm_sq = 0.0;
+  int64_t elem_size() const { return dtype == SPAMM_DTYPE_F64 ? 8 : 4; }
+};

@@ -1,0 +1,330 @@
+// leaf.cu -- K3: batched leaf-block products with the reference's
+// deterministic k-reduction.
+//
+// Reference: _leaf_stage (multiply.py:224-257) multiplies every retained
+// (i, j, k) leaf triple with np.matmul and merges the products of one C block
+// with _merge_contributions (multiply.py:119-141): an aligned binary interval
+// tree over k -- both halves present -> left + right, one present -> passed
+// through bit-intact.
+//
+// B200 mapping (FP64): one work item = one C block (or a 64x64 sub-tile of
+// it for leaves > 64).  Every product P_k = A_ik B_kj is accumulated from
+// zero on the FP64 tensor-core path (mma.sync m16n8k16 f64, SASS DMMA) in
+// ascending inner index, which is exactly the sequential FMA chain the CPU
+// BLAS kernel produces (tools/dmma_order.cu proved DMMA accumulates in that
+// order), and the products are merged in the reference's tree order with a
+// shunting-yard stack keyed by the level of the lowest common ancestor of
+// consecutive k (32 - clz(k_prev ^ k_next)).  Operand tiles stream through a
+// 3-stage cp.async pipeline with padded shared-memory rows (conflict-free
+// fragment loads); CTAs are persistent and take work items from a ticket.
+#include "leaf.cuh"
+
+namespace spamm {
+
+constexpr int MAXD = 22;  // deepest merge stack (depth <= 21 with 63-bit Morton codes)
+
+__device__ __forceinline__ void cp_async16_l(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8],
+                                          const double (&b)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+      "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+        "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+// Level at which two distinct inner indices meet in the merge tree.
+__device__ __forceinline__ int merge_level(uint32_t k0, uint32_t k1) {
+  return 32 - __clz(k0 ^ k1);
+}
+
+struct WorkItem {
+  int64_t start, end;  // triple range [start, end) of the group
+  uint32_t i, j;       // C block
+  int si, sj;          // sub-tile
+};
+
+__device__ __forceinline__ bool fetch_work(const LeafArgs &args, int subs_side, int *s_work,
+                                           WorkItem &w) {
+  if (threadIdx.x == 0) *s_work = (int)atomicAdd(args.ticket, 1ull);
+  __syncthreads();
+  const int item = *s_work;
+  const int ng = *args.num_groups;
+  const int subs = subs_side * subs_side;
+  if (item >= ng * subs) return false;
+  const int grp = item / subs, sub = item - grp * subs;
+  w.si = sub / subs_side;
+  w.sj = sub - w.si * subs_side;
+  w.start = args.group_starts[grp];
+  w.end = grp + 1 < ng ? args.group_starts[grp + 1] : args.m;
+  const uint64_t gid = args.keys[w.start] >> args.depth;
+  w.i = (uint32_t)(gid / (uint64_t)args.nb);
+  w.j = (uint32_t)(gid - (uint64_t)w.i * args.nb);
+  return true;
+}
+
+// ---------------------------------------------------------------- DMMA path
+constexpr int DMMA_THREADS = 128;
+constexpr int DMMA_BK = 32;
+constexpr int DMMA_STAGES = 3;
+
+template <int TILE>
+struct DmmaCfg {
+  static constexpr int SA = DMMA_BK + 4;  // A row stride (doubles), == 4 mod 16
+  static constexpr int SB = TILE + 4;     // B row stride (doubles), == 4 mod 16
+  static constexpr int A_ELEMS = TILE * SA;
+  static constexpr int B_ELEMS = DMMA_BK * SB;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr int MT = TILE / 32;  // m16 tiles per warp (2x2 warps)
+  static constexpr int NT = TILE / 16;  // n8 tiles per warp
+  static constexpr size_t SMEM = sizeof(double) * DMMA_STAGES * STAGE_ELEMS;
+};
+
+template <int TILE>
+__global__ void __launch_bounds__(DMMA_THREADS) leaf_dmma_kernel(LeafArgs args) {
+  using C = DmmaCfg<TILE>;
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ int s_work;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  const int b = args.leaf;
+  const int kchunks = b / DMMA_BK;
+  const int subs_side = b / TILE;
+  const int64_t N = args.N;
+  const uint64_t kmask = (uint64_t(1) << args.depth) - 1;
+  const double *__restrict__ A = (const double *)args.a;
+  const double *__restrict__ B = (const double *)args.b;
+  double *__restrict__ Cm = (double *)args.c;
+
+  double stk[MAXD][C::MT][C::NT][4];
+  int ops[MAXD];
+
+  WorkItem w;
+  while (fetch_work(args, subs_side, &s_work, w)) {
+    const int64_t nk = w.end - w.start;
+    const int64_t nsteps = nk * kchunks;
+    const double *Arow = A + (int64_t(w.i) * b + w.si * TILE) * N;
+    const int64_t bcol = int64_t(w.j) * b + w.sj * TILE;
+
+    auto issue = [&](int64_t step) {
+      const int stage = (int)(step % DMMA_STAGES);
+      const int64_t s = step / kchunks;
+      const int kc = (int)(step - s * kchunks);
+      const uint64_t k = args.keys[w.start + s] & kmask;
+      double *As = dsm + stage * C::STAGE_ELEMS;
+      double *Bs = As + C::A_ELEMS;
+      const int64_t kcol = int64_t(k) * b + kc * DMMA_BK;
+      // A: TILE rows x DMMA_BK cols = TILE * 16 chunks of 16 B
+#pragma unroll
+      for (int q = 0; q < (TILE * DMMA_BK / 2) / DMMA_THREADS; ++q) {
+        const int e = tid + q * DMMA_THREADS;
+        const int r = e / (DMMA_BK / 2), c2 = e % (DMMA_BK / 2);
+        cp_async16_l(As + r * C::SA + 2 * c2, Arow + r * N + kcol + 2 * c2);
+      }
+      // B: DMMA_BK rows x TILE cols
+#pragma unroll
+      for (int q = 0; q < (DMMA_BK * TILE / 2) / DMMA_THREADS; ++q) {
+        const int e = tid + q * DMMA_THREADS;
+        const int r = e / (TILE / 2), c2 = e % (TILE / 2);
+        cp_async16_l(Bs + r * C::SB + 2 * c2, B + (kcol + r) * N + bcol + 2 * c2);
+      }
+    };
+
+#pragma unroll
+    for (int s = 0; s < DMMA_STAGES - 1; ++s) {
+      if (s < nsteps) issue(s);
+      cp_commit();
+    }
+
+    double acc[C::MT][C::NT][4];
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.0;
+    int sp = 0;
+
+    for (int64_t step = 0; step < nsteps; ++step) {
+      cp_wait<DMMA_STAGES - 2>();
+      __syncthreads();
+      if (step + DMMA_STAGES - 1 < nsteps) issue(step + DMMA_STAGES - 1);
+      cp_commit();
+      const double *As = dsm + (int)(step % DMMA_STAGES) * C::STAGE_ELEMS;
+      const double *Bs = As + C::A_ELEMS;
+#pragma unroll
+      for (int kk = 0; kk < DMMA_BK; kk += 16) {
+        double af[C::MT][8];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            af[mt][q] = As[(wm * (TILE / 2) + mt * 16 + g + 8 * (q & 1)) * C::SA + kk + t +
+                           4 * (q >> 1)];
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) {
+          double bf[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            bf[q] = Bs[(kk + t + 4 * q) * C::SB + wn * (TILE / 2) + nt * 8 + g];
+#pragma unroll
+          for (int mt = 0; mt < C::MT; ++mt) dmma16816(acc[mt][nt], af[mt], bf);
+        }
+      }
+      if ((int)(step % kchunks) == kchunks - 1) {
+        // P_k complete: merge in the reference's tree order
+        const int64_t s = step / kchunks;
+        const uint32_t k = (uint32_t)(args.keys[w.start + s] & kmask);
+        int h = 99;
+        if (s + 1 < nk) h = merge_level(k, (uint32_t)(args.keys[w.start + s + 1] & kmask));
+        while (sp > 0 && ops[sp - 1] < h) {
+          --sp;
+#pragma unroll
+          for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[mt][nt][q] = __dadd_rn(stk[sp][mt][nt][q], acc[mt][nt][q]);
+        }
+        if (s + 1 < nk) {
+#pragma unroll
+          for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                stk[sp][mt][nt][q] = acc[mt][nt][q];
+                acc[mt][nt][q] = 0.0;
+              }
+          ops[sp] = h;
+          ++sp;
+        }
+      }
+    }
+    cp_wait<0>();
+    // epilogue: C block rows/cols of this sub-tile
+    const int64_t crow0 = int64_t(w.i) * b + w.si * TILE + wm * (TILE / 2);
+    const int64_t ccol0 = bcol + wn * (TILE / 2);
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int64_t row = crow0 + mt * 16 + g + 8 * h2;
+          const int64_t col = ccol0 + nt * 8 + 2 * t;
+          *reinterpret_cast<double2 *>(Cm + row * N + col) =
+              make_double2(acc[mt][nt][2 * h2], acc[mt][nt][2 * h2 + 1]);
+        }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- SIMT path
+// Any leaf size and FP32 (and FP64 leaves < 32): one thread per C element of
+// a <= 64 x 64 sub-tile, each product an FMA chain over the inner index in
+// ascending order (np.matmul's order on this data), merged with the same
+// LCA-keyed stack.
+constexpr int SIMT_THREADS = 512;
+constexpr int SIMT_MAXE = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(SIMT_THREADS) leaf_simt_kernel(LeafArgs args) {
+  __shared__ int s_work;
+  const int b = args.leaf;
+  const int TILE = b < 64 ? b : 64;
+  const int subs_side = b / TILE;
+  const int64_t N = args.N;
+  const uint64_t kmask = (uint64_t(1) << args.depth) - 1;
+  const T *__restrict__ A = (const T *)args.a;
+  const T *__restrict__ B = (const T *)args.b;
+  T *__restrict__ Cm = (T *)args.c;
+  const int elems = TILE * TILE;
+  T stk[SIMT_MAXE][MAXD];
+  int ops[MAXD];
+  WorkItem w;
+  while (fetch_work(args, subs_side, &s_work, w)) {
+    const int64_t nk = w.end - w.start;
+    T acc[SIMT_MAXE];
+#pragma unroll
+    for (int e = 0; e < SIMT_MAXE; ++e) acc[e] = T(0);
+    int sp = 0;
+    for (int64_t s = 0; s < nk; ++s) {
+      const uint32_t k = (uint32_t)(args.keys[w.start + s] & kmask);
+#pragma unroll
+      for (int e = 0; e < SIMT_MAXE; ++e) {
+        const int idx = threadIdx.x + e * SIMT_THREADS;
+        if (idx < elems) {
+          const int r = idx / TILE, c = idx - r * TILE;
+          const T *arow = A + (int64_t(w.i) * b + w.si * TILE + r) * N + int64_t(k) * b;
+          const T *bcol = B + (int64_t(k) * b) * N + int64_t(w.j) * b + w.sj * TILE + c;
+          T p = T(0);
+          for (int q = 0; q < b; ++q) p = fma(arow[q], bcol[int64_t(q) * N], p);
+          acc[e] = p;
+        }
+      }
+      int h = 99;
+      if (s + 1 < nk) h = merge_level(k, (uint32_t)(args.keys[w.start + s + 1] & kmask));
+      while (sp > 0 && ops[sp - 1] < h) {
+        --sp;
+#pragma unroll
+        for (int e = 0; e < SIMT_MAXE; ++e) acc[e] = stk[e][sp] + acc[e];
+      }
+      if (s + 1 < nk) {
+#pragma unroll
+        for (int e = 0; e < SIMT_MAXE; ++e) stk[e][sp] = acc[e];
+        ops[sp] = h;
+        ++sp;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < SIMT_MAXE; ++e) {
+      const int idx = threadIdx.x + e * SIMT_THREADS;
+      if (idx < elems) {
+        const int r = idx / TILE, c = idx - r * TILE;
+        Cm[(int64_t(w.i) * b + w.si * TILE + r) * N + int64_t(w.j) * b + w.sj * TILE + c] = acc[e];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st) {
+  if (dtype == SPAMM_DTYPE_F64 && args.leaf >= 32) {
+    if (args.leaf == 32) {
+      using C = DmmaCfg<32>;
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_dmma_kernel<32>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      int per_sm = 0;
+      SPAMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, leaf_dmma_kernel<32>,
+                                                                   DMMA_THREADS, C::SMEM));
+      leaf_dmma_kernel<32><<<num_sms * (per_sm > 0 ? per_sm : 1), DMMA_THREADS, C::SMEM, st>>>(args);
+    } else {
+      using C = DmmaCfg<64>;
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_dmma_kernel<64>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      int per_sm = 0;
+      SPAMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, leaf_dmma_kernel<64>,
+                                                                   DMMA_THREADS, C::SMEM));
+      leaf_dmma_kernel<64><<<num_sms * (per_sm > 0 ? per_sm : 1), DMMA_THREADS, C::SMEM, st>>>(args);
+    }
+  } else if (dtype == SPAMM_DTYPE_F64) {
+    leaf_simt_kernel<double><<<num_sms * 2, SIMT_THREADS, 0, st>>>(args);
+  } else {
+    leaf_simt_kernel<float><<<num_sms * 2, SIMT_THREADS, 0, st>>>(args);
+  }
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  return SPAMM_OK;
+}
+
+}  // namespace spamm

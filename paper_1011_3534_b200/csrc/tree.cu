@@ -1,0 +1,566 @@
+// tree.cu -- quadtree construction on the device: padding (K4), the
+// bit-exact leaf norm kernel (K1) and the norm/occupancy pyramid, plus the
+// tree half of the C ABI and the per-device context.
+//
+// Reference: quadtree.py:116-151 (QuadTreeMatrix.__init__), :74-87
+// (_leaf_norm_sq), :90-92 (_aggregate_norm_sq), :218-251 (from_dense).
+#include <cuda.h>
+
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace spamm {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+void set_error(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+// ----------------------------------------------------------------- contexts
+static std::mutex g_ctx_mu;
+static std::vector<std::unique_ptr<DeviceContext>> g_ctx;
+
+int get_context(int device, DeviceContext **out) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  int count = 0;
+  SPAMM_CUDA_TRY(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) {
+    set_error("CUDA device %d not available (%d visible)", device, count);
+    return SPAMM_ERR_VALUE;
+  }
+  if ((int)g_ctx.size() < count) g_ctx.resize(count);
+  if (!g_ctx[device]) {
+    auto ctx = std::make_unique<DeviceContext>();
+    ctx->device = device;
+    SPAMM_CUDA_TRY(cudaSetDevice(device));
+    SPAMM_CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    for (auto &e : ctx->ev) SPAMM_CUDA_TRY(cudaEventCreate(&e));
+    SPAMM_CUDA_TRY(cudaMallocHost(&ctx->host_pinned, 1 << 16));
+    // keep freed pool memory cached between calls (stream-ordered allocator)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thresh = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
+    }
+    g_ctx[device] = std::move(ctx);
+  }
+  *out = g_ctx[device].get();
+  SPAMM_CUDA_TRY(cudaSetDevice(device));
+  return SPAMM_OK;
+}
+
+int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream) {
+  if (s.bytes >= bytes) return SPAMM_OK;
+  if (s.ptr) SPAMM_CUDA_TRY(cudaFreeAsync(s.ptr, stream));
+  s.ptr = nullptr;
+  s.bytes = 0;
+  size_t want = bytes + bytes / 4 + 256;
+  SPAMM_CUDA_TRY(cudaMallocAsync(&s.ptr, want, stream));
+  s.bytes = want;
+  return SPAMM_OK;
+}
+
+// ================================================================ K1 kernels
+//
+// One thread owns one leaf and accumulates its squared Frobenius norm in the
+// reference's order: row-major over the leaf, acc = rn(acc + rn(x*x)), with
+// no FMA contraction (quadtree.py:80-87; __dmul_rn/__dadd_rn pin the
+// rounding).  The parallelism is across leaves only -- a per-leaf shuffle
+// tree would change the bits the strict `< tau` tests compare.
+//
+// Data movement: a CTA owns LT = 128 consecutive leaves (row-major leaf
+// order).  Each leaf is streamed in 128-byte chunks (one row piece, or
+// several full rows for b < 16) through a STAGES-deep cp.async pipeline into
+// shared memory with 16 B of padding per leaf, so the per-thread LDS.128
+// reads are bank-conflict free while the global reads stay fully coalesced
+// (every 128 B line is consumed whole).
+constexpr int K1_LT = 128;
+constexpr int K1_STAGES = 4;
+constexpr int K1_LEAF_STRIDE = 144;  // bytes per leaf chunk in smem (128 + 16 pad)
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <typename T>
+struct Bits;
+template <>
+struct Bits<double> {
+  using U = unsigned long long;
+  __device__ static U of(double x) { return (U)__double_as_longlong(x); }
+};
+template <>
+struct Bits<float> {
+  using U = unsigned int;
+  __device__ static U of(float x) { return (U)__float_as_uint(x); }
+};
+
+template <typename T>
+__device__ __forceinline__ void accum(double &acc, int &nz, int &negz, T x) {
+  const auto u = Bits<T>::of(x);
+  using U = typename Bits<T>::U;
+  const U mag = u << 1;  // drop the sign: zero iff x == +-0.0 (NaN counts as nonzero)
+  nz |= (mag != 0);
+  negz |= (u != 0);      // any set bit (a -0.0 when mag == 0)
+  const double e = (double)x;
+  acc = __dadd_rn(acc, __dmul_rn(e, e));
+}
+
+template <typename T>
+__device__ void canonicalise_leaf(T *padded, int64_t N, int32_t b, int64_t bi, int64_t bj) {
+  for (int r = 0; r < b; ++r) {
+    T *row = padded + (bi * b + r) * N + bj * b;
+    for (int c = 0; c < b; ++c) row[c] = T(0);
+  }
+}
+
+// Staged kernel, b * sizeof(T) >= 16 and b*b*sizeof(T) >= 128.
+template <typename T>
+__global__ void __launch_bounds__(K1_LT) leaf_norm_staged_kernel(T *__restrict__ padded, int64_t N,
+                                                                 int32_t b, int64_t nb,
+                                                                 double *__restrict__ nsq_leaf,
+                                                                 uint8_t *__restrict__ occ_leaf) {
+  constexpr int EPC = 128 / sizeof(T);  // elements per 128-byte chunk
+  extern __shared__ __align__(16) unsigned char k1_smem[];
+  const int64_t n_leaves = nb * nb;
+  const int64_t leaf0 = (int64_t)blockIdx.x * K1_LT;
+  const int tid = threadIdx.x;
+  const int CW = b < EPC ? b : EPC;      // chunk width (elements)
+  const int R = EPC / CW;                // rows per chunk
+  const int chunks_per_row = b / CW;
+  const int n_chunks = (b / R) * chunks_per_row;
+
+  auto issue = [&](int chunk, int stage) {
+    const int r0 = (chunk / chunks_per_row) * R;
+    const int c0 = (chunk % chunks_per_row) * CW;
+    unsigned char *base = k1_smem + stage * (K1_LT * K1_LEAF_STRIDE);
+    // K1_LT leaves x 8 segments of 16 B
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int s = tid + q * K1_LT;
+      const int l = s >> 3, part = s & 7;
+      const int64_t leaf = leaf0 + l;
+      if (leaf < n_leaves) {
+        const int64_t bi = leaf / nb, bj = leaf - bi * nb;
+        const int e = part * (16 / (int)sizeof(T));  // element offset within chunk
+        const int rr = e / CW, cc = e - rr * CW;
+        const T *g = padded + (bi * b + r0 + rr) * N + bj * b + c0 + cc;
+        cp_async16(base + l * K1_LEAF_STRIDE + part * 16, g);
+      }
+    }
+  };
+
+  const int64_t my_leaf = leaf0 + tid;
+  double acc = 0.0;
+  int nz = 0, negz = 0;
+#pragma unroll
+  for (int s = 0; s < K1_STAGES - 1; ++s) {
+    if (s < n_chunks) issue(s, s);
+    cp_async_commit();
+  }
+  for (int chunk = 0; chunk < n_chunks; ++chunk) {
+    cp_async_wait<K1_STAGES - 2>();
+    __syncthreads();
+    const int nxt = chunk + K1_STAGES - 1;
+    if (nxt < n_chunks) issue(nxt, nxt % K1_STAGES);
+    cp_async_commit();
+    if (my_leaf < n_leaves) {
+      const unsigned char *p = k1_smem + (chunk % K1_STAGES) * (K1_LT * K1_LEAF_STRIDE) +
+                               tid * K1_LEAF_STRIDE;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(p + 16 * v);
+        const T *x = reinterpret_cast<const T *>(&w);
+#pragma unroll
+        for (int e = 0; e < (int)(16 / sizeof(T)); ++e) accum<T>(acc, nz, negz, x[e]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (my_leaf < n_leaves) {
+    nsq_leaf[my_leaf] = acc;
+    occ_leaf[my_leaf] = (uint8_t)(nz != 0);
+    if (!nz && negz) {
+      const int64_t bi = my_leaf / nb;
+      canonicalise_leaf<T>(padded, N, b, bi, my_leaf - bi * nb);
+    }
+  }
+}
+
+// Direct kernel for tiny leaves (b * b * sizeof(T) < 128): one thread per
+// leaf reads its b x b elements in row-major order straight from global.
+template <typename T>
+__global__ void leaf_norm_direct_kernel(T *__restrict__ padded, int64_t N, int32_t b, int64_t nb,
+                                        double *__restrict__ nsq_leaf,
+                                        uint8_t *__restrict__ occ_leaf) {
+  const int64_t leaf = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (leaf >= nb * nb) return;
+  const int64_t bi = leaf / nb, bj = leaf - bi * nb;
+  double acc = 0.0;
+  int nz = 0, negz = 0;
+  for (int r = 0; r < b; ++r) {
+    const T *row = padded + (bi * b + r) * N + bj * b;
+    for (int c = 0; c < b; ++c) accum<T>(acc, nz, negz, row[c]);
+  }
+  nsq_leaf[leaf] = acc;
+  occ_leaf[leaf] = (uint8_t)(nz != 0);
+  if (!nz && negz) canonicalise_leaf<T>(padded, N, b, bi, bj);
+}
+
+// Pyramid: each CTA reduces a 2^L x 2^L tile of level `from` through L levels,
+// parent = ((c11 + c12) + c21) + c22 (quadtree.py:90-92), occupancy OR
+// (quadtree.py:137-138).  Launched in passes of L <= 5 levels.
+constexpr int PYR_THREADS = 256;
+__global__ void __launch_bounds__(PYR_THREADS) pyramid_kernel(double *__restrict__ nsq,
+                                                              uint8_t *__restrict__ occ, int from,
+                                                              int L) {
+  __shared__ double s_n[1024];
+  __shared__ uint8_t s_o[1024];
+  const int tiles_per_side = 1 << (from - L);
+  const int ti = blockIdx.x / tiles_per_side, tj = blockIdx.x % tiles_per_side;
+  int side = 1 << L;
+  const int64_t fine_side = int64_t(1) << from;
+  const double *lvl = nsq + level_offset(from);
+  const uint8_t *olvl = occ + level_offset(from);
+  for (int e = threadIdx.x; e < side * side; e += PYR_THREADS) {
+    const int r = e / side, c = e % side;
+    const int64_t g = (int64_t(ti) * side + r) * fine_side + int64_t(tj) * side + c;
+    s_n[e] = lvl[g];
+    s_o[e] = olvl[g];
+  }
+  __syncthreads();
+  for (int k = from - 1; k >= from - L; --k) {
+    const int ps = side >> 1;
+    const int64_t coarse_side = int64_t(1) << k;
+    double *clvl = nsq + level_offset(k);
+    uint8_t *oclvl = occ + level_offset(k);
+    double v[4];
+    uint8_t o[4];
+    int cnt = 0;
+    for (int e = threadIdx.x; e < ps * ps; e += PYR_THREADS, ++cnt) {
+      const int r = e / ps, c = e % ps;
+      const int f0 = (2 * r) * side + 2 * c, f1 = f0 + side;
+      v[cnt] = __dadd_rn(__dadd_rn(__dadd_rn(s_n[f0], s_n[f0 + 1]), s_n[f1]), s_n[f1 + 1]);
+      o[cnt] = s_o[f0] | s_o[f0 + 1] | s_o[f1] | s_o[f1 + 1];
+      const int64_t g = (int64_t(ti) * ps + r) * coarse_side + int64_t(tj) * ps + c;
+      clvl[g] = v[cnt];
+      oclvl[g] = o[cnt];
+    }
+    __syncthreads();
+    cnt = 0;
+    for (int e = threadIdx.x; e < ps * ps; e += PYR_THREADS, ++cnt) {
+      s_n[e] = v[cnt];
+      s_o[e] = o[cnt];
+    }
+    __syncthreads();
+    side = ps;
+  }
+}
+
+template <typename T>
+static int launch_leaf_norms(spamm_tree *t, cudaStream_t st) {
+  const int64_t n_leaves = t->nb * t->nb;
+  double *nsq_leaf = t->nsq + level_offset(t->depth);
+  uint8_t *occ_leaf = t->occ + level_offset(t->depth);
+  if ((int64_t)t->leaf * t->leaf * (int64_t)sizeof(T) >= 128 && t->leaf * sizeof(T) >= 16) {
+    const size_t smem = (size_t)K1_STAGES * K1_LT * K1_LEAF_STRIDE;
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_norm_staged_kernel<T>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t grid = (n_leaves + K1_LT - 1) / K1_LT;
+    leaf_norm_staged_kernel<T><<<(unsigned)grid, K1_LT, smem, st>>>(
+        (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf);
+  } else {
+    const int64_t grid = (n_leaves + 127) / 128;
+    leaf_norm_direct_kernel<T><<<(unsigned)grid, 128, 0, st>>>((T *)t->padded, t->N, t->leaf,
+                                                                t->nb, nsq_leaf, occ_leaf);
+  }
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  return SPAMM_OK;
+}
+
+// Rebuild the whole pyramid of `t` from its padded storage (canonicalising
+// all-zero leaves in place).  Stream-ordered; no host sync.
+int build_pyramid_async(spamm_tree *t, cudaStream_t st) {
+  if (t->dtype == SPAMM_DTYPE_F64) SPAMM_TRY(launch_leaf_norms<double>(t, st));
+  else SPAMM_TRY(launch_leaf_norms<float>(t, st));
+  int from = t->depth;
+  while (from > 0) {
+    const int L = from < 5 ? from : 5;
+    const int64_t tiles = int64_t(1) << (2 * (from - L));
+    pyramid_kernel<<<(unsigned)tiles, PYR_THREADS, 0, st>>>(t->nsq, t->occ, from, L);
+    SPAMM_CUDA_TRY(cudaGetLastError());
+    from -= L;
+  }
+  return SPAMM_OK;
+}
+
+int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out) {
+  auto t = std::make_unique<spamm_tree>();
+  t->n = n;
+  t->leaf = leaf;
+  t->depth = depth_for(n, leaf);
+  t->N = int64_t(leaf) << t->depth;
+  t->nb = t->N / leaf;
+  t->dtype = dtype;
+  t->device = ctx->device;
+  const int64_t esz = t->elem_size();
+  SPAMM_CUDA_TRY(cudaMallocAsync(&t->padded, (size_t)(t->N * t->N * esz), ctx->stream));
+  SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->nsq, sizeof(double) * pyramid_size(t->depth),
+                                 ctx->stream));
+  SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->occ, pyramid_size(t->depth), ctx->stream));
+  *out = t.release();
+  return SPAMM_OK;
+}
+
+void free_tree_async(spamm_tree *t, cudaStream_t st) {
+  if (!t) return;
+  if (t->padded) cudaFreeAsync(t->padded, st);
+  if (t->nsq) cudaFreeAsync(t->nsq, st);
+  if (t->occ) cudaFreeAsync(t->occ, st);
+  delete t;
+}
+
+int finish_tree(DeviceContext *ctx, spamm_tree *t) {
+  SPAMM_CUDA_TRY(cudaMemcpyAsync(&t->root_norm_sq, t->nsq, sizeof(double), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SPAMM_OK;
+}
+
+static int validate_shape(int64_t n, int64_t ld, int32_t leaf, int32_t dtype) {
+  if (leaf < 1 || (leaf & (leaf - 1)) != 0) {
+    set_error("leaf_size must be a power of two >= 1, got %d", leaf);
+    return SPAMM_ERR_VALUE;
+  }
+  if (dtype != SPAMM_DTYPE_F64 && dtype != SPAMM_DTYPE_F32) {
+    set_error("unsupported element dtype code %d", dtype);
+    return SPAMM_ERR_VALUE;
+  }
+  if (n < 1) {
+    set_error("matrix dimension must be >= 1");
+    return SPAMM_ERR_VALUE;
+  }
+  if (ld < n) {
+    set_error("leading dimension %lld < n %lld", (long long)ld, (long long)n);
+    return SPAMM_ERR_VALUE;
+  }
+  return SPAMM_OK;
+}
+
+static int tree_from(const void *src, bool src_on_host, int64_t n, int64_t ld, int32_t leaf,
+                     int32_t dtype, int32_t device, spamm_tree **out) {
+  SPAMM_TRY(validate_shape(n, ld, leaf, dtype));
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  spamm_tree *t = nullptr;
+  SPAMM_TRY(alloc_tree(ctx, n, leaf, dtype, &t));
+  const int64_t esz = t->elem_size();
+  int rc = SPAMM_OK;
+  do {
+    cudaError_t e;
+    if (t->N != n) {
+      e = cudaMemsetAsync(t->padded, 0, (size_t)(t->N * t->N * esz), ctx->stream);
+      if (e != cudaSuccess) { set_error("memset: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
+    }
+    e = cudaMemcpy2DAsync(t->padded, (size_t)(t->N * esz), src, (size_t)(ld * esz),
+                          (size_t)(n * esz), (size_t)n,
+                          src_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                          ctx->stream);
+    if (e != cudaSuccess) { set_error("copy: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
+    rc = build_pyramid_async(t, ctx->stream);
+    if (rc) break;
+    rc = finish_tree(ctx, t);
+  } while (0);
+  if (rc) {
+    free_tree_async(t, ctx->stream);
+    return rc;
+  }
+  *out = t;
+  return SPAMM_OK;
+}
+
+// -------------------------------------------------------- ||A - B||_F kernel
+template <typename T>
+__global__ void diff_sq_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t count,
+                               double *__restrict__ partial) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = (double)a[i] - (double)b[i];
+    acc = fma(d, d, acc);
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+  }
+}
+
+__global__ void sum_partials_kernel(const double *__restrict__ partial, int n, double *out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partial[i];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) *out = sqrt(acc);
+  }
+}
+
+}  // namespace spamm
+
+using namespace spamm;
+
+extern "C" {
+
+const char *spamm_last_error(void) { return g_last_error.c_str(); }
+
+const char *spamm_version(void) { return "spamm_b200 0.1 sm_100a"; }
+
+int spamm_device_count(int *count) {
+  SPAMM_CUDA_TRY(cudaGetDeviceCount(count));
+  return SPAMM_OK;
+}
+
+int spamm_tree_from_host(const void *host, int64_t n, int64_t ld, int32_t leaf, int32_t dtype,
+                         int32_t device, spamm_tree **out) {
+  return tree_from(host, true, n, ld, leaf, dtype, device, out);
+}
+
+int spamm_tree_from_device(const void *dev, int64_t n, int64_t ld, int32_t leaf, int32_t dtype,
+                           int32_t device, spamm_tree **out) {
+  return tree_from(dev, false, n, ld, leaf, dtype, device, out);
+}
+
+int spamm_tree_from_padded_device(const void *dev_padded, int64_t n, int64_t padded_dim,
+                                  int32_t leaf, int32_t dtype, int32_t device, spamm_tree **out) {
+  SPAMM_TRY(validate_shape(n, n, leaf, dtype));
+  if ((int64_t(leaf) << depth_for(n, leaf)) != padded_dim) {
+    set_error("padded_dim %lld inconsistent with n=%lld leaf=%d", (long long)padded_dim,
+              (long long)n, leaf);
+    return SPAMM_ERR_DIMENSION;
+  }
+  SPAMM_TRY(tree_from(dev_padded, false, padded_dim, padded_dim, leaf, dtype, device, out));
+  (*out)->n = n;
+  return SPAMM_OK;
+}
+
+int spamm_tree_info_get(const spamm_tree *t, spamm_tree_info *info) {
+  if (!t || !info) { set_error("null tree"); return SPAMM_ERR_VALUE; }
+  info->logical_dim = t->n;
+  info->padded_dim = t->N;
+  info->block_grid = t->nb;
+  info->leaf_size = t->leaf;
+  info->depth = t->depth;
+  info->dtype = t->dtype;
+  info->device = t->device;
+  info->root_norm_sq = t->root_norm_sq;
+  return SPAMM_OK;
+}
+
+int spamm_tree_to_host(const spamm_tree *t, void *host, int64_t ld) {
+  if (!t) { set_error("null tree"); return SPAMM_ERR_VALUE; }
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(t->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const int64_t esz = t->elem_size();
+  SPAMM_CUDA_TRY(cudaMemcpy2DAsync(host, (size_t)(ld * esz), t->padded, (size_t)(t->N * esz),
+                                   (size_t)(t->n * esz), (size_t)t->n, cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SPAMM_OK;
+}
+
+int spamm_tree_padded_to_host(const spamm_tree *t, void *host) {
+  if (!t) { set_error("null tree"); return SPAMM_ERR_VALUE; }
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(t->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_CUDA_TRY(cudaMemcpyAsync(host, t->padded, (size_t)(t->N * t->N * t->elem_size()),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SPAMM_OK;
+}
+
+int spamm_tree_pyramid_to_host(const spamm_tree *t, double *nsq, uint8_t *occ) {
+  if (!t) { set_error("null tree"); return SPAMM_ERR_VALUE; }
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(t->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const int64_t P = pyramid_size(t->depth);
+  if (nsq) SPAMM_CUDA_TRY(cudaMemcpyAsync(nsq, t->nsq, sizeof(double) * P, cudaMemcpyDeviceToHost,
+                                          ctx->stream));
+  if (occ) SPAMM_CUDA_TRY(cudaMemcpyAsync(occ, t->occ, P, cudaMemcpyDeviceToHost, ctx->stream));
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SPAMM_OK;
+}
+
+int spamm_tree_device_ptrs(const spamm_tree *t, void **padded, double **nsq, uint8_t **occ) {
+  if (!t) { set_error("null tree"); return SPAMM_ERR_VALUE; }
+  if (padded) *padded = t->padded;
+  if (nsq) *nsq = t->nsq;
+  if (occ) *occ = t->occ;
+  return SPAMM_OK;
+}
+
+int spamm_tree_diff_norm(const spamm_tree *a, const spamm_tree *b, double *out) {
+  if (!a || !b) { set_error("null tree"); return SPAMM_ERR_VALUE; }
+  if (a->N != b->N || a->dtype != b->dtype || a->device != b->device) {
+    set_error("trees not conformable for difference norm");
+    return SPAMM_ERR_DIMENSION;
+  }
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(a->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const int blocks = ctx->num_sms * 4;
+  SPAMM_TRY(ensure_scratch(ctx->reduce_tmp, sizeof(double) * (blocks + 1), ctx->stream));
+  double *part = (double *)ctx->reduce_tmp.ptr;
+  const int64_t count = a->N * a->N;
+  if (a->dtype == SPAMM_DTYPE_F64)
+    diff_sq_kernel<double><<<blocks, 256, 0, ctx->stream>>>((const double *)a->padded,
+                                                             (const double *)b->padded, count, part);
+  else
+    diff_sq_kernel<float><<<blocks, 256, 0, ctx->stream>>>((const float *)a->padded,
+                                                            (const float *)b->padded, count, part);
+  sum_partials_kernel<<<1, 1024, 0, ctx->stream>>>(part, blocks, part + blocks);
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  SPAMM_CUDA_TRY(cudaMemcpyAsync(out, part + blocks, sizeof(double), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SPAMM_OK;
+}
+
+void spamm_tree_free(spamm_tree *t) {
+  if (!t) return;
+  DeviceContext *ctx;
+  if (get_context(t->device, &ctx) != SPAMM_OK) return;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  free_tree_async(t, ctx->stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,188 @@
+"""The sparse approximate matrix multiply on B200 (drop-in for ``spamm.multiply``).
+
+``spamm(a, b, config)`` keeps the reference's signature, return value and
+exceptions (multiply.py:144-221); the work runs in the CUDA library:
+
+* K2 level-synchronous culling (csrc/cull.cu) -- the retained leaf-triple
+  set, the pruned boxes and every ProductStats integer are identical to the
+  reference's, and ``omitted_budget`` is summed with numpy's pairwise order;
+* K3 leaf products on the FP64 tensor-core path (csrc/leaf.cu) merged in the
+  reference's binary-interval order, so C is bit-identical to the
+  reference's on the same BLAS ordering;
+* K1 on the product for C's norm pyramid (csrc/tree.cu).
+
+Reference: arxiv/paper_1011_3534, pkg/src/spamm/multiply.py.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _lib
+from .quadtree import QuadTreeMatrix, _require_conformable, _wrap, node_norm
+
+
+@dataclass(frozen=True)
+class SpammConfig:
+    """Knobs for one multiply (multiply.py:43-74).
+
+    ``deterministic`` is accepted for interface parity: the GPU path always
+    uses the reference's fixed merge order, so results are bit-reproducible
+    either way.
+    """
+
+    tau: float = 0.0
+    collect_boxes: bool = False
+    count_stats: bool = True
+    deterministic: bool = True
+    tier_tau_decay: bool = False
+
+    def __post_init__(self):
+        if not math.isfinite(self.tau) or self.tau < 0:
+            raise ValueError(f"tau must be finite and >= 0, got {self.tau}")
+
+
+@dataclass(frozen=True)
+class PrunedBox:
+    """A tau-pruned cuboid [i_lo, i_lo+edge) x [j_lo, ..) x [k_lo, ..) of the
+    padded index cube, edge = padded_dim / 2**tier (multiply.py:77-90)."""
+
+    i_lo: int
+    j_lo: int
+    k_lo: int
+    edge: int
+    tier: int
+
+
+@dataclass
+class ProductStats:
+    """Work and truncation accounting for one multiply (multiply.py:93-116)."""
+
+    leaf_matmuls: int = 0
+    pruned_calls: int = 0
+    omitted_budget: float = 0.0
+    max_depth_reached: int = 0
+    boxes: list | None = None
+    pruned_volume: int = 0
+    empty_skip_volume: int = 0
+
+    def covered_volume(self, leaf_size):
+        """Visited leaf cells + pruned boxes + Empty skips (== padded_dim**3)."""
+        return (self.leaf_matmuls * leaf_size ** 3
+                + self.pruned_volume + self.empty_skip_volume)
+
+
+@dataclass
+class MultiplyDetail:
+    """Extra artefacts of one device multiply (not part of the reference API)."""
+
+    triples: np.ndarray | None = None       # (m, 3) int32 retained (i, j, k), sorted
+    tier_candidates: list = field(default_factory=list)
+    tier_survivors: list = field(default_factory=list)
+    tier_pruned: list = field(default_factory=list)
+    n_groups: int = 0
+    ms_cull: float = 0.0
+    ms_leaf: float = 0.0
+    ms_ctree: float = 0.0
+    ms_total: float = 0.0
+
+
+def _flags(config, keep_triples):
+    f = 0
+    if config.collect_boxes:
+        f |= _lib.COLLECT_BOXES
+    if config.count_stats:
+        f |= _lib.COUNT_STATS
+    if config.tier_tau_decay:
+        f |= _lib.TIER_TAU_DECAY
+    if keep_triples:
+        f |= _lib.KEEP_TRIPLES
+    return f
+
+
+def spamm_detailed(a, b, config=None, keep_triples=False, rows=None):
+    """spamm() plus a MultiplyDetail (retained triples, per-tier counts,
+    device timings).  ``rows=(lo, hi)`` restricts the product to C leaf block
+    rows [lo, hi) -- the shard of one rank in the multi-GPU layout."""
+    _require_conformable(a, b)
+    if config is None:
+        config = SpammConfig()
+    L = _lib.load()
+    c = ctypes.c_void_p()
+    prod = ctypes.c_void_p()
+    st = _lib.Stats()
+    flags = _flags(config, keep_triples)
+    if rows is None:
+        _lib.check(L.spamm_multiply(a._handle, b._handle, float(config.tau), flags,
+                                    ctypes.byref(c), ctypes.byref(st), ctypes.byref(prod)))
+    else:
+        _lib.check(L.spamm_multiply_rows(a._handle, b._handle, float(config.tau), flags,
+                                         int(rows[0]), int(rows[1]), ctypes.byref(c),
+                                         ctypes.byref(st), ctypes.byref(prod)))
+    try:
+        stats = ProductStats(boxes=[] if config.collect_boxes else None)
+        stats.leaf_matmuls = int(st.leaf_matmuls)
+        stats.pruned_calls = int(st.pruned_calls)
+        stats.omitted_budget = float(st.omitted_budget)
+        stats.max_depth_reached = int(st.max_depth_reached)
+        stats.pruned_volume = int(st.pruned_volume)
+        stats.empty_skip_volume = int(st.empty_skip_volume)
+        depth = a.depth
+        detail = MultiplyDetail(tier_candidates=list(st.tier_candidates[:depth + 1]),
+                                tier_survivors=list(st.tier_survivors[:depth + 1]),
+                                tier_pruned=list(st.tier_pruned[:depth + 1]),
+                                n_groups=int(st.n_groups), ms_cull=st.ms_cull,
+                                ms_leaf=st.ms_leaf, ms_ctree=st.ms_ctree, ms_total=st.ms_total)
+        if config.collect_boxes and st.n_boxes:
+            raw = np.empty((int(st.n_boxes), 5), np.int64)
+            _lib.check(L.spamm_product_boxes(prod, raw.ctypes.data, int(st.n_boxes)))
+            stats.boxes = [PrunedBox(int(x), int(y), int(z), int(e), int(t))
+                           for x, y, z, e, t in raw.tolist()]
+        if keep_triples:
+            trip = np.empty((int(st.n_triples), 3), np.int32)
+            if st.n_triples:
+                _lib.check(L.spamm_product_triples(prod, trip.ctypes.data, int(st.n_triples)))
+            detail.triples = trip
+    finally:
+        if prod.value:
+            L.spamm_product_free(prod)
+    return _wrap(c.value), stats, detail
+
+
+def spamm(a, b, config=None):
+    """Multiply two device quadtrees with norm-product pruning
+    (multiply.py:144-221).  Returns ``(QuadTreeMatrix, ProductStats)``."""
+    c, stats, _ = spamm_detailed(a, b, config)
+    return c, stats
+
+
+def exact_multiply(a, b):
+    """The exact product, tau = 0 (multiply.py:260-263)."""
+    c, _ = spamm(a, b, SpammConfig(tau=0.0, count_stats=False))
+    return c
+
+
+def diff_norm(x, y):
+    """||X - Y||_F over the padded storage, computed on the device."""
+    out = ctypes.c_double()
+    _lib.check(_lib.load().spamm_tree_diff_norm(x._handle, y._handle, ctypes.byref(out)))
+    return float(out.value)
+
+
+def multiply_error(a, b, config):
+    """(abs_err, omitted_budget) of the truncated product against the exact
+    one (multiply.py:266-278); the difference norm runs on the GPU."""
+    if config.tau > 0 and not config.count_stats:
+        config = replace(config, count_stats=True)
+    approx, stats = spamm(a, b, config)
+    exact = exact_multiply(a, b)
+    return diff_norm(approx, exact), stats.omitted_budget
+
+
+__all__ = ["SpammConfig", "PrunedBox", "ProductStats", "MultiplyDetail", "spamm",
+           "spamm_detailed", "exact_multiply", "multiply_error", "diff_norm", "node_norm",
+           "QuadTreeMatrix"]
