@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""bench.py -- SpAMM on B200: retained-leaf FP64 TFLOP/s on BASELINE config 2.
+
+Metric (BASELINE.json): "SpAMM time & retained-leaf FP64 TFLOP/s vs tau".
+Workload (BASELINE.json configs[1]): n = 4096, leaf 64,
+A = B = sym(u0 * 0.95^|i-j|) (seeded synthetic, numpy PCG64 seed 0), tau
+swept over {1e-4, 1e-6, 1e-8, 1e-10}.  One step = one spamm() per tau on
+device-resident trees (cull + leaf products + C's tree), i.e. the sweep.
+
+* value      retained-leaf FLOP (2 b^3 per retained triple) / device time,
+             TFLOP/s; each spamm timed with CUDA events on the library's own
+             stream; L2 flushed (256 MiB write) before every multiply.
+* e2e        the same metric through the public API with host buffers:
+             from_dense(pinned A) -> spamm per tau -> to_dense(pinned C),
+             host->device and device->host copies inside the timed region.
+* roofline   the leaf-product kernel (K3) against the measured FP64 DMMA peak
+             (profiles/fp64_peaks.json, measured on this pool's B200s).
+* cpu_baseline / --impl reference: the C restatement of the reference
+             algorithm (oracle/, OpenMP over all host cores) on the same inputs.
+
+Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference];
+N > 1 under torch.distributed.run (one process per GPU, NCCL).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpAMM time & retained-leaf FP64 TFLOP/s vs tau, n=4096-65536, 1/2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3_l2", "c3_l3", "c5"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu/context")
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def leaf_flops(leaf, retained):
+    return 2.0 * leaf ** 3 * retained
+
+
+# ------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        rows = []
+        if self.path and os.path.exists(self.path):
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 9 and f[1].isdigit():
+                    rows.append(f)
+            os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [int(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        loaded = [x for x in sm if x > 600] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": int(rows[0][2]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- the oracle
+def cpu_reference(a, leaf, taus, steps, warmup):
+    """Time the oracle port (C restatement of the reference, OpenMP over all
+    host cores) on the same workload: per tau cull + leaf stage + C's tree on
+    prebuilt operand pyramids, like the GPU's value leg."""
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    from oracle import oracle
+
+    pa = oracle.pad(a, leaf)
+    na, oa = oracle.build_pyramid(pa, leaf)
+    N = pa.shape[0]
+    depth = oracle.depth_for(N, leaf)
+    times, flops = [], 0.0
+    for step in range(warmup + steps):
+        t0 = time.perf_counter()
+        f = 0.0
+        for tau in taus:
+            st, trip, _, _ = oracle.cull(na, oa, na, oa, depth, N, tau, collect_boxes=False)
+            c = oracle.leaf_stage(pa, pa, leaf, trip)
+            oracle.build_pyramid(c, leaf)
+            f += leaf_flops(leaf, st["leaf_matmuls"])
+        dt = time.perf_counter() - t0
+        if step >= warmup:
+            times.append(dt)
+            flops += f
+    return flops / sum(times) / 1e12, sum(times) / len(times), int(os.environ["OMP_NUM_THREADS"])
+
+
+def run_reference(args, cfg_name):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1011_3534_b200 import workloads
+    a, _, leaf, taus = workloads.make_config(cfg_name)
+    steps = max(1, args.steps)
+    warm = max(0, args.warmup)
+    value, sec_per_step, cores = cpu_reference(a, leaf, taus, steps, warm)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": sec_per_step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))",
+        "config": {"workload": f"{cfg_name}: n={a.shape[0]} leaf={leaf} taus={list(taus)}",
+                   "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"full {cfg_name} tau sweep per step"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- the GPU
+def fp64_peak():
+    path = os.path.join(ROOT, "profiles", "fp64_peaks.json")
+    with open(path) as fh:
+        p = json.load(fh)
+    peak = max(v for k, v in p.items() if k.startswith("dmma_") and k.endswith("_tflops"))
+    return peak, "profiles/fp64_peaks.json (DMMA mma.sync f64 microbenchmark, this pool's B200)"
+
+
+def k3_traffic():
+    path = os.path.join(ROOT, "profiles", "k3_traffic.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return json.load(fh)
+    return None
+
+
+def run_b200(args, cfg_name):
+    import torch
+    import paper_1011_3534_b200 as sp
+    from paper_1011_3534_b200 import workloads
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    sp.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    a_host, _, leaf, taus = workloads.make_config(cfg_name)
+    n = a_host.shape[0]
+    from paper_1011_3534_b200 import distributed as spd
+
+    shard = spd.row_shard(rank, world, n, leaf) if world > 1 else None
+    a = sp.from_dense(a_host, leaf_size=leaf)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def one_step(collect=None):
+        f, ms, gemm, launches = 0.0, 0.0, 0.0, 0
+        per_tau = []
+        for tau in taus:
+            flush.zero_()
+            torch.cuda.synchronize()
+            c, st, det = sp.spamm_detailed(a, a, sp.SpammConfig(tau=tau), rows=shard)
+            f += leaf_flops(leaf, st.leaf_matmuls)
+            ms += det.ms_total
+            gemm += det.ms_gemm
+            launches += det.kernel_launches
+            per_tau.append((tau, st.leaf_matmuls, det.ms_total, det.ms_gemm, det.ms_cull,
+                            det.ms_ctree, det.n_groups))
+            del c
+        return f, ms, gemm, launches, per_tau
+
+    for _ in range(args.warmup):
+        one_step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    tot_f = tot_ms = tot_gemm = 0.0
+    launches = 0
+    per_tau_all = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            f, ms, gemm, la, per_tau = one_step()
+            if world > 1:
+                t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                ms = float(t.item())
+                fl = torch.tensor([f], dtype=torch.float64, device="cuda")
+                torch.distributed.all_reduce(fl)
+                f = float(fl.item())
+            tot_f += f
+            tot_ms += ms
+            tot_gemm += gemm
+            launches += la
+            per_tau_all.append(per_tau)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = clk.summary()
+    value = tot_f / (tot_ms * 1e-3) / 1e12
+    ms_per_step = tot_ms / args.steps
+
+    # per-tau table from the last step
+    table = [{"tau": t, "retained": r, "frac_of_nb3": r / (a.block_grid ** 3), "ms": m,
+              "gemm_ms": g, "cull_ms": cu, "ctree_ms": ct, "c_blocks": ng,
+              "tflops": leaf_flops(leaf, r) / (m * 1e-3) / 1e12}
+             for (t, r, m, g, cu, ct, ng) in per_tau_all[-1]]
+
+    peak, peak_src = fp64_peak()
+    # K3 roofline from this rank's own flops and K3 event time
+    local_f = sum(leaf_flops(leaf, x[1]) for step in per_tau_all for x in step)
+    local_gemm = sum(x[3] for step in per_tau_all for x in step)
+    achieved = local_f / (local_gemm * 1e-3) / 1e12 if local_gemm > 0 else 0.0
+    traffic = k3_traffic()
+    roofline = {"bound": "tensor", "kernel": "leaf_dmma_kernel<64> (K3)", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "peak_source": peak_src,
+                "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                "algorithmic": "2*b^3 flop per retained leaf triple / K3 event time"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy PCG64, SURVEY §8(d))",
+        "config": {"workload": f"{cfg_name}: n={n} leaf={leaf} A=B=sym(u*0.95^|i-j|), "
+                               f"tau sweep {list(taus)}, one spamm per tau per step",
+                   "l2": "flushed (256 MiB write) before every multiply",
+                   "parallelism": f"C block-row shards x{world}" if world > 1 else "single GPU",
+                   "per_tau": table},
+        "roofline": roofline,
+        "clocks": clocks,
+        "gpu_launches": launches // max(args.steps, 1),
+    }
+
+    if rank == 0 and world == 1 and not args.profile:
+        # --- context: dense cuBLAS DGEMM on the same matrix
+        at = torch.from_numpy(a_host).cuda()
+        for _ in range(2):
+            torch.matmul(at, at)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        torch.matmul(at, at)
+        e1.record()
+        torch.cuda.synchronize()
+        dg = e0.elapsed_time(e1)
+        line["config"]["context_dense_cublas_dgemm"] = {
+            "ms": dg, "tflops": 2.0 * n ** 3 / (dg * 1e-3) / 1e12}
+        del at
+
+    if not args.no_e2e and not args.profile and world == 1:
+        pin_a = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+        pin_a[...] = a_host
+        pin_c = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+        for it in range(args.warmup + args.steps):
+            if it == args.warmup:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                e_f = 0.0
+            at = sp.from_dense(pin_a, leaf_size=leaf)
+            f = 0.0
+            for tau in taus:
+                c, st = sp.spamm(at, at, sp.SpammConfig(tau=tau))
+                c.to_dense(out=pin_c)
+                f += leaf_flops(leaf, st.leaf_matmuls)
+                del c
+            del at
+            if it >= args.warmup:
+                e_f += f
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        line["e2e"] = {"value": e_f / el / 1e12, "unit": "TFLOP/s",
+                       "h2d_bytes_per_step": n * n * 8,
+                       "d2h_bytes_per_step": len(taus) * n * n * 8,
+                       "ms_per_step": el / args.steps * 1e3,
+                       "timing": "host wall clock around synchronous public-API calls"}
+
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
+        cv, sec, cores = cpu_reference(a_host, leaf, taus, 1, 1)
+        line["cpu_baseline"] = {"value": cv, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                                "sample": f"one full {cfg_name} tau sweep ({sec:.2f} s) after "
+                                          "one warm-up sweep",
+                                "ms_per_step": sec * 1e3}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args, args.config)
+    else:
+        run_b200(args, args.config)
+
+
+if __name__ == "__main__":
+    main()

@@ -91,6 +91,8 @@ typedef struct {
   float ms_leaf;
   float ms_ctree;
   float ms_total;
+  float ms_gemm;           /* the leaf-product kernel (K3) alone          */
+  int32_t kernel_launches; /* kernels this call launched                  */
 } spamm_stats;
 
 SPAMM_API const char *spamm_last_error(void);

@@ -56,7 +56,8 @@ class Stats(ctypes.Structure):
                 ("tier_survivors", ctypes.c_int64 * 32),
                 ("tier_pruned", ctypes.c_int64 * 32),
                 ("ms_cull", ctypes.c_float), ("ms_leaf", ctypes.c_float),
-                ("ms_ctree", ctypes.c_float), ("ms_total", ctypes.c_float)]
+                ("ms_ctree", ctypes.c_float), ("ms_total", ctypes.c_float),
+                ("ms_gemm", ctypes.c_float), ("kernel_launches", ctypes.c_int32)]
 
 
 _lock = threading.Lock()

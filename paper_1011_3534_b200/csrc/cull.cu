@@ -17,9 +17,8 @@
 // order-preserving single-pass scan: warp ballots/prefix sums inside the
 // tile, decoupled look-back across tiles.  Counts stay on the device, so a
 // whole traversal is launched without a host round trip.
-#include <cuda/atomic>
-
 #include "cull.cuh"
+#include "scan.cuh"
 
 namespace spamm {
 
@@ -27,21 +26,11 @@ constexpr int CULL_THREADS = 256;
 constexpr int CULL_ITEMS = 4;
 constexpr int CULL_TILE = CULL_THREADS * CULL_ITEMS;
 
-// tile status word: [63:62] flag, [61:31] active count, [30:0] pruned count
-constexpr unsigned long long ST_AGG = 1ull << 62;
-constexpr unsigned long long ST_PREFIX = 2ull << 62;
-constexpr unsigned long long ST_FLAGS = 3ull << 62;
-constexpr unsigned long long ST_VALUES = ~ST_FLAGS;
-
-__device__ __forceinline__ unsigned long long pack_ap(unsigned a, unsigned p) {
-  return ((unsigned long long)a << 31) | p;
-}
-
 __global__ void __launch_bounds__(CULL_THREADS) cull_tier_kernel(CullTierArgs args) {
   __shared__ unsigned long long s_warp[CULL_THREADS / 32];
   __shared__ unsigned long long s_excl;
   __shared__ unsigned long long s_tile;
-  __shared__ unsigned long long s_counts[3];  // skip(owned), pruned(owned), alive
+  __shared__ unsigned s_counts[2];  // owned Empty skips, alive
   CullCounters *cc = args.counters;
   const int tier = args.tier;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -68,15 +57,14 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_tier_kernel(CullTierArgs ar
 
   for (;;) {
     if (threadIdx.x == 0) s_tile = atomicAdd(&cc->ticket[tier], 1ull);
-    if (threadIdx.x < 3) s_counts[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
     __syncthreads();
     const unsigned long long tile = s_tile;
     if (tile >= n_tiles) break;
 
     uint64_t code[CULL_ITEMS];
     double npv[CULL_ITEMS];
-    unsigned act_mask = 0, prn_mask = 0;
-    unsigned n_skip = 0, n_prn = 0, n_alive = 0;
+    unsigned act_mask = 0, prn_mask = 0, n_skip = 0, n_alive = 0;
 #pragma unroll
     for (int q = 0; q < CULL_ITEMS; ++q) {
       const unsigned long long c = tile * CULL_TILE + threadIdx.x * CULL_ITEMS + q;
@@ -100,97 +88,39 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_tier_kernel(CullTierArgs ar
           if (pruned && owned) {
             prn_mask |= 1u << q;
             npv[q] = np_;
-            ++n_prn;
           }
           if (!alive && owned) ++n_skip;
         }
       }
     }
-    // ---- block-wide exclusive scan of (active, pruned) counts (in order)
-    const unsigned my_a = __popc(act_mask), my_p = __popc(prn_mask);
-    unsigned long long v = pack_ap(my_a, my_p);
-    unsigned long long incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    // stats (integers: order independent)
-    unsigned s0 = n_skip, s1 = n_prn, s2 = n_alive;
+    // integer stats: order independent
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      n_skip += __shfl_xor_sync(0xffffffffu, n_skip, o);
+      n_alive += __shfl_xor_sync(0xffffffffu, n_alive, o);
     }
     if (lane == 0) {
-      atomicAdd(&s_counts[0], (unsigned long long)s0);
-      atomicAdd(&s_counts[1], (unsigned long long)s1);
-      atomicAdd(&s_counts[2], (unsigned long long)s2);
+      atomicAdd(&s_counts[0], n_skip);
+      atomicAdd(&s_counts[1], n_alive);
     }
-    __syncthreads();
+    // order-preserving compaction offsets of (active, pruned) within the tile
+    unsigned long long tile_total;
+    const unsigned long long in_tile =
+        block_exclusive<CULL_THREADS>(pack2(__popc(act_mask), __popc(prn_mask)), s_warp,
+                                      &tile_total);
     if (warp == 0) {
-      unsigned long long w = lane < CULL_THREADS / 32 ? s_warp[lane] : 0ull;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      if (lane < CULL_THREADS / 32) s_warp[lane] = w;  // inclusive over warps
-      const unsigned long long tile_total = __shfl_sync(0xffffffffu, w, CULL_THREADS / 32 - 1);
-      // ---- decoupled look-back
-      unsigned long long excl = 0;
-      if (tile == 0) {
-        if (lane == 0) {
-          cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(args.tile_status[0]);
-          st.store(ST_PREFIX | tile_total, cuda::memory_order_release);
-        }
-      } else {
-        if (lane == 0) {
-          cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(args.tile_status[tile]);
-          st.store(ST_AGG | tile_total, cuda::memory_order_release);
-        }
-        long long pred = (long long)tile - 1;
-        for (;;) {
-          const long long idx = pred - lane;
-          unsigned long long s = ST_PREFIX;  // virtual zero prefix before tile 0
-          if (idx >= 0) {
-            cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(args.tile_status[idx]);
-            do {
-              s = st.load(cuda::memory_order_acquire);
-            } while ((s & ST_FLAGS) == 0);
-          }
-          const unsigned pmask = __ballot_sync(0xffffffffu, (s & ST_FLAGS) == ST_PREFIX);
-          const int stop = pmask ? __ffs(pmask) - 1 : 31;
-          unsigned long long val = lane <= stop ? (s & ST_VALUES) : 0ull;
-#pragma unroll
-          for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-          excl += val;
-          if (pmask) break;
-          pred -= 32;
-        }
-        if (lane == 0) {
-          cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(args.tile_status[tile]);
-          st.store(ST_PREFIX | (excl + tile_total), cuda::memory_order_release);
-        }
-      }
+      const unsigned long long excl = lookback_exclusive(args.tile_status, tile, tile_total);
       if (lane == 0) {
         s_excl = excl;
-        atomicAdd(&cc->n_active[tier], tile_total >> 31);
-        atomicAdd(&cc->n_pruned[tier], tile_total & 0x7fffffffull);
-        atomicAdd(&cc->n_skip[tier], s_counts[0]);
-        atomicAdd(&cc->n_alive[tier], s_counts[2]);
+        atomicAdd(&cc->n_active[tier], (unsigned long long)unpack_a(tile_total));
+        atomicAdd(&cc->n_pruned[tier], (unsigned long long)unpack_b(tile_total));
+        atomicAdd(&cc->n_skip[tier], (unsigned long long)s_counts[0]);
+        atomicAdd(&cc->n_alive[tier], (unsigned long long)s_counts[1]);
       }
     }
     __syncthreads();
-    // ---- scatter in candidate order
-    const unsigned long long base =
-        s_excl + (warp ? s_warp[warp - 1] : 0ull) + (incl - v);
-    unsigned a_pos = (unsigned)(base >> 31);
-    unsigned p_pos = (unsigned)(base & 0x7fffffffull);
-    const unsigned long long a_base = (unsigned long long)a_pos;
-    (void)a_base;
+    const unsigned long long base = s_excl + in_tile;
+    unsigned a_pos = unpack_a(base), p_pos = unpack_b(base);
 #pragma unroll
     for (int q = 0; q < CULL_ITEMS; ++q) {
       if (act_mask & (1u << q)) {
@@ -376,10 +306,12 @@ int launch_cull(const CullPlan &plan, cudaStream_t st) {
     if (grid == 0) grid = 1;
     cull_tier_kernel<<<grid, CULL_THREADS, 0, st>>>(args);
     SPAMM_CUDA_TRY(cudaGetLastError());
+    if (plan.launches) ++*plan.launches;
   }
   tier_budget_kernel<<<plan.depth + 1, PW_THREADS, 0, st>>>(plan.pruned_vals, plan.counters);
   budget_total_kernel<<<1, 1, 0, st>>>(plan.counters, plan.depth + 1);
   SPAMM_CUDA_TRY(cudaGetLastError());
+  if (plan.launches) *plan.launches += 2;
   return SPAMM_OK;
 }
 

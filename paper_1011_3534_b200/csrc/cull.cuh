@@ -51,6 +51,7 @@ struct CullPlan {
   CullCounters *counters;
   int64_t row_lo, row_hi;
   int max_ctas;
+  int *launches;  // kernel launch counter (may be null)
 };
 
 int launch_cull(const CullPlan &plan, cudaStream_t st);

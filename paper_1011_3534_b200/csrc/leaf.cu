@@ -56,87 +56,113 @@ struct WorkItem {
 
 __device__ __forceinline__ bool fetch_work(const LeafArgs &args, int subs_side, int *s_work,
                                            WorkItem &w) {
-  if (threadIdx.x == 0) *s_work = (int)atomicAdd(args.ticket, 1ull);
+  if (threadIdx.x == 0) *s_work = (int)atomicAdd(&args.lc->gemm_ticket, 1ull);
   __syncthreads();
   const int item = *s_work;
-  const int ng = *args.num_groups;
+  const int ng = (int)args.lc->num_groups;
   const int subs = subs_side * subs_side;
   if (item >= ng * subs) return false;
   const int grp = item / subs, sub = item - grp * subs;
   w.si = sub / subs_side;
   w.sj = sub - w.si * subs_side;
+  unsigned long long m = *args.n_codes;
+  if (m > args.capacity) m = args.capacity;
   w.start = args.group_starts[grp];
-  w.end = grp + 1 < ng ? args.group_starts[grp + 1] : args.m;
-  const uint64_t gid = args.keys[w.start] >> args.depth;
+  w.end = grp + 1 < ng ? args.group_starts[grp + 1] : (int64_t)m;
+  const uint32_t gid = args.group_ids[grp];
   w.i = (uint32_t)(gid / (uint64_t)args.nb);
   w.j = (uint32_t)(gid - (uint64_t)w.i * args.nb);
   return true;
 }
 
 // ---------------------------------------------------------------- DMMA path
-constexpr int DMMA_THREADS = 128;
 constexpr int DMMA_BK = 32;
 constexpr int DMMA_STAGES = 3;
+constexpr int KS_SMEM = 1024;  // group k lists up to this length are staged in smem
 
-template <int TILE>
+// Shared-memory tiles are dense (rows of 256 B for A, 512 B for B) with the
+// 16-byte chunks of each 128-byte segment XOR-swizzled by (row & 3) << 1.
+// That makes the m16n8k16 fragment loads (4 rows x 2 chunks per half-warp)
+// hit 32 distinct banks, and keeps every 128-byte global line landing in one
+// 128-byte shared segment for the cp.async copies.
+__device__ __forceinline__ int swz(int row, int col) {  // element offset within a row
+  const int chunk = col >> 1;
+  return (((chunk & ~7) | ((chunk & 7) ^ ((row & 3) << 1))) << 1) | (col & 1);
+}
+
+template <int TILE, int WM, int WN>
 struct DmmaCfg {
-  static constexpr int SA = DMMA_BK + 4;  // A row stride (doubles), == 4 mod 16
-  static constexpr int SB = TILE + 4;     // B row stride (doubles), == 4 mod 16
+  static constexpr int THREADS = 32 * WM * WN;
+  static constexpr int SA = DMMA_BK;      // A row length (doubles)
+  static constexpr int SB = TILE;         // B row length (doubles)
   static constexpr int A_ELEMS = TILE * SA;
   static constexpr int B_ELEMS = DMMA_BK * SB;
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-  static constexpr int MT = TILE / 32;  // m16 tiles per warp (2x2 warps)
-  static constexpr int NT = TILE / 16;  // n8 tiles per warp
+  static constexpr int WTM = TILE / WM;   // warp tile rows
+  static constexpr int WTN = TILE / WN;   // warp tile cols
+  static constexpr int MT = WTM / 16;     // m16 tiles per warp
+  static constexpr int NT = WTN / 8;      // n8 tiles per warp
   static constexpr size_t SMEM = sizeof(double) * DMMA_STAGES * STAGE_ELEMS;
+  static_assert(MT >= 1 && NT >= 1, "warp tile too small");
+  static_assert((TILE * DMMA_BK / 2) % THREADS == 0 && (DMMA_BK * TILE / 2) % THREADS == 0, "");
 };
 
-template <int TILE>
-__global__ void __launch_bounds__(DMMA_THREADS) leaf_dmma_kernel(LeafArgs args) {
-  using C = DmmaCfg<TILE>;
+template <int TILE, int WM, int WN>
+__global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) {
+  using C = DmmaCfg<TILE, WM, WN>;
   extern __shared__ __align__(16) double dsm[];
   __shared__ int s_work;
+  __shared__ uint32_t s_ks[KS_SMEM];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  const int wm = warp / WN, wn = warp % WN, g = lane >> 2, t = lane & 3;
   const int b = args.leaf;
-  const int kchunks = b / DMMA_BK;
+  const int kchunks = b / DMMA_BK;             // a power of two
+  const int kshift = __ffs(kchunks) - 1;
   const int subs_side = b / TILE;
   const int64_t N = args.N;
-  const uint64_t kmask = (uint64_t(1) << args.depth) - 1;
   const double *__restrict__ A = (const double *)args.a;
   const double *__restrict__ B = (const double *)args.b;
   double *__restrict__ Cm = (double *)args.c;
 
+  // Merge stack of the reference's tree order (see merge_level): pending
+  // left operands are keyed by tree level; the op levels on the stack are
+  // strictly decreasing from bottom to top, so they form a bit mask whose
+  // lowest set bit is the top.  The top value lives in registers; deeper
+  // ones in stk[level] (local memory), written back only when dirty.
   double stk[MAXD][C::MT][C::NT][4];
-  int ops[MAXD];
+  double top[C::MT][C::NT][4];
 
   WorkItem w;
   while (fetch_work(args, subs_side, &s_work, w)) {
     const int64_t nk = w.end - w.start;
     const int64_t nsteps = nk * kchunks;
+    const bool ks_in_smem = nk <= KS_SMEM;
+    if (ks_in_smem)
+      for (int e = tid; e < nk; e += C::THREADS) s_ks[e] = args.ks[w.start + e];
+    __syncthreads();
+    const uint32_t *ks = ks_in_smem ? s_ks : args.ks + w.start;
     const double *Arow = A + (int64_t(w.i) * b + w.si * TILE) * N;
     const int64_t bcol = int64_t(w.j) * b + w.sj * TILE;
 
     auto issue = [&](int64_t step) {
       const int stage = (int)(step % DMMA_STAGES);
-      const int64_t s = step / kchunks;
-      const int kc = (int)(step - s * kchunks);
-      const uint64_t k = args.keys[w.start + s] & kmask;
+      const int64_t s = step >> kshift;
+      const int kc = (int)(step & (kchunks - 1));
+      const uint32_t k = ks[s];
       double *As = dsm + stage * C::STAGE_ELEMS;
       double *Bs = As + C::A_ELEMS;
       const int64_t kcol = int64_t(k) * b + kc * DMMA_BK;
-      // A: TILE rows x DMMA_BK cols = TILE * 16 chunks of 16 B
 #pragma unroll
-      for (int q = 0; q < (TILE * DMMA_BK / 2) / DMMA_THREADS; ++q) {
-        const int e = tid + q * DMMA_THREADS;
+      for (int q = 0; q < (TILE * DMMA_BK / 2) / C::THREADS; ++q) {
+        const int e = tid + q * C::THREADS;
         const int r = e / (DMMA_BK / 2), c2 = e % (DMMA_BK / 2);
-        cp_async16_l(As + r * C::SA + 2 * c2, Arow + r * N + kcol + 2 * c2);
+        cp_async16_l(As + r * C::SA + swz(r, 2 * c2), Arow + r * N + kcol + 2 * c2);
       }
-      // B: DMMA_BK rows x TILE cols
 #pragma unroll
-      for (int q = 0; q < (DMMA_BK * TILE / 2) / DMMA_THREADS; ++q) {
-        const int e = tid + q * DMMA_THREADS;
+      for (int q = 0; q < (DMMA_BK * TILE / 2) / C::THREADS; ++q) {
+        const int e = tid + q * C::THREADS;
         const int r = e / (TILE / 2), c2 = e % (TILE / 2);
-        cp_async16_l(Bs + r * C::SB + 2 * c2, B + (kcol + r) * N + bcol + 2 * c2);
+        cp_async16_l(Bs + r * C::SB + swz(r, 2 * c2), B + (kcol + r) * N + bcol + 2 * c2);
       }
     };
 
@@ -153,7 +179,8 @@ __global__ void __launch_bounds__(DMMA_THREADS) leaf_dmma_kernel(LeafArgs args) 
       for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.0;
-    int sp = 0;
+    uint32_t pending = 0;    // levels with a pending left operand
+    bool top_dirty = false;  // top[] not yet written to stk[ctz(pending)]
 
     for (int64_t step = 0; step < nsteps; ++step) {
       cp_wait<DMMA_STAGES - 2>();
@@ -168,53 +195,75 @@ __global__ void __launch_bounds__(DMMA_THREADS) leaf_dmma_kernel(LeafArgs args) 
 #pragma unroll
         for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            af[mt][q] = As[(wm * (TILE / 2) + mt * 16 + g + 8 * (q & 1)) * C::SA + kk + t +
-                           4 * (q >> 1)];
+          for (int q = 0; q < 8; ++q) {
+            const int r = wm * C::WTM + mt * 16 + g + 8 * (q & 1);
+            af[mt][q] = As[r * C::SA + swz(r, kk + t + 4 * (q >> 1))];
+          }
 #pragma unroll
         for (int nt = 0; nt < C::NT; ++nt) {
           double bf[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            bf[q] = Bs[(kk + t + 4 * q) * C::SB + wn * (TILE / 2) + nt * 8 + g];
+          for (int q = 0; q < 4; ++q) {
+            const int r = kk + t + 4 * q;
+            bf[q] = Bs[r * C::SB + swz(r, wn * C::WTN + nt * 8 + g)];
+          }
 #pragma unroll
           for (int mt = 0; mt < C::MT; ++mt) dmma16816(acc[mt][nt], af[mt], bf);
         }
       }
-      if ((int)(step % kchunks) == kchunks - 1) {
+      if ((int)(step & (kchunks - 1)) == kchunks - 1) {
         // P_k complete: merge in the reference's tree order
-        const int64_t s = step / kchunks;
-        const uint32_t k = (uint32_t)(args.keys[w.start + s] & kmask);
-        int h = 99;
-        if (s + 1 < nk) h = merge_level(k, (uint32_t)(args.keys[w.start + s + 1] & kmask));
-        while (sp > 0 && ops[sp - 1] < h) {
-          --sp;
+        const int64_t s = step >> kshift;
+        const uint32_t k = ks[s];
+        int h = 31;
+        if (s + 1 < nk) h = merge_level(k, ks[s + 1]);
+        while (pending && (__ffs(pending) - 1) < h) {
 #pragma unroll
           for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
             for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-              for (int q = 0; q < 4; ++q) acc[mt][nt][q] = __dadd_rn(stk[sp][mt][nt][q], acc[mt][nt][q]);
+              for (int q = 0; q < 4; ++q) acc[mt][nt][q] = __dadd_rn(top[mt][nt][q], acc[mt][nt][q]);
+          pending &= pending - 1;
+          if (pending) {
+            const int lv = __ffs(pending) - 1;
+#pragma unroll
+            for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) top[mt][nt][q] = stk[lv][mt][nt][q];
+            top_dirty = false;
+          }
         }
         if (s + 1 < nk) {
+          if (pending && top_dirty) {
+            const int lv = __ffs(pending) - 1;
+#pragma unroll
+            for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) stk[lv][mt][nt][q] = top[mt][nt][q];
+          }
 #pragma unroll
           for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
             for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                stk[sp][mt][nt][q] = acc[mt][nt][q];
+                top[mt][nt][q] = acc[mt][nt][q];
                 acc[mt][nt][q] = 0.0;
               }
-          ops[sp] = h;
-          ++sp;
+          top_dirty = true;
+          pending |= 1u << h;
         }
       }
     }
     cp_wait<0>();
     // epilogue: C block rows/cols of this sub-tile
-    const int64_t crow0 = int64_t(w.i) * b + w.si * TILE + wm * (TILE / 2);
-    const int64_t ccol0 = bcol + wn * (TILE / 2);
+    const int64_t crow0 = int64_t(w.i) * b + w.si * TILE + wm * C::WTM;
+    const int64_t ccol0 = bcol + wn * C::WTN;
 #pragma unroll
     for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
@@ -228,6 +277,18 @@ __global__ void __launch_bounds__(DMMA_THREADS) leaf_dmma_kernel(LeafArgs args) 
         }
     __syncthreads();
   }
+}
+
+template <int TILE, int WM, int WN>
+static int launch_dmma(const LeafArgs &args, int num_sms, cudaStream_t st) {
+  using C = DmmaCfg<TILE, WM, WN>;
+  auto kern = leaf_dmma_kernel<TILE, WM, WN>;
+  SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)C::SMEM));
+  int per_sm = 0;
+  SPAMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM));
+  kern<<<num_sms * (per_sm > 0 ? per_sm : 1), C::THREADS, C::SMEM, st>>>(args);
+  return SPAMM_OK;
 }
 
 // ---------------------------------------------------------------- SIMT path
@@ -245,7 +306,6 @@ __global__ void __launch_bounds__(SIMT_THREADS) leaf_simt_kernel(LeafArgs args) 
   const int TILE = b < 64 ? b : 64;
   const int subs_side = b / TILE;
   const int64_t N = args.N;
-  const uint64_t kmask = (uint64_t(1) << args.depth) - 1;
   const T *__restrict__ A = (const T *)args.a;
   const T *__restrict__ B = (const T *)args.b;
   T *__restrict__ Cm = (T *)args.c;
@@ -260,7 +320,7 @@ __global__ void __launch_bounds__(SIMT_THREADS) leaf_simt_kernel(LeafArgs args) 
     for (int e = 0; e < SIMT_MAXE; ++e) acc[e] = T(0);
     int sp = 0;
     for (int64_t s = 0; s < nk; ++s) {
-      const uint32_t k = (uint32_t)(args.keys[w.start + s] & kmask);
+      const uint32_t k = args.ks[w.start + s];
 #pragma unroll
       for (int e = 0; e < SIMT_MAXE; ++e) {
         const int idx = threadIdx.x + e * SIMT_THREADS;
@@ -274,7 +334,7 @@ __global__ void __launch_bounds__(SIMT_THREADS) leaf_simt_kernel(LeafArgs args) 
         }
       }
       int h = 99;
-      if (s + 1 < nk) h = merge_level(k, (uint32_t)(args.keys[w.start + s + 1] & kmask));
+      if (s + 1 < nk) h = merge_level(k, args.ks[w.start + s + 1]);
       while (sp > 0 && ops[sp - 1] < h) {
         --sp;
 #pragma unroll
@@ -299,31 +359,17 @@ __global__ void __launch_bounds__(SIMT_THREADS) leaf_simt_kernel(LeafArgs args) 
   }
 }
 
-int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st) {
+int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches) {
   if (dtype == SPAMM_DTYPE_F64 && args.leaf >= 32) {
-    if (args.leaf == 32) {
-      using C = DmmaCfg<32>;
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_dmma_kernel<32>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      int per_sm = 0;
-      SPAMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, leaf_dmma_kernel<32>,
-                                                                   DMMA_THREADS, C::SMEM));
-      leaf_dmma_kernel<32><<<num_sms * (per_sm > 0 ? per_sm : 1), DMMA_THREADS, C::SMEM, st>>>(args);
-    } else {
-      using C = DmmaCfg<64>;
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_dmma_kernel<64>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      int per_sm = 0;
-      SPAMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, leaf_dmma_kernel<64>,
-                                                                   DMMA_THREADS, C::SMEM));
-      leaf_dmma_kernel<64><<<num_sms * (per_sm > 0 ? per_sm : 1), DMMA_THREADS, C::SMEM, st>>>(args);
-    }
+    if (args.leaf == 32) SPAMM_TRY((launch_dmma<32, 2, 2>(args, num_sms, st)));
+    else SPAMM_TRY((launch_dmma<64, 2, 4>(args, num_sms, st)));
   } else if (dtype == SPAMM_DTYPE_F64) {
     leaf_simt_kernel<double><<<num_sms * 2, SIMT_THREADS, 0, st>>>(args);
   } else {
     leaf_simt_kernel<float><<<num_sms * 2, SIMT_THREADS, 0, st>>>(args);
   }
   SPAMM_CUDA_TRY(cudaGetLastError());
+  if (launches) ++*launches;
   return SPAMM_OK;
 }
 

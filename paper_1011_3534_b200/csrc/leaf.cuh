@@ -1,20 +1,23 @@
 // leaf.cuh -- K3 interfaces (see leaf.cu).
 #pragma once
 #include "common.cuh"
+#include "group.cuh"
 
 namespace spamm {
 
 struct LeafArgs {
-  const void *a, *b;               // padded operands (N x N row-major)
-  void *c;                         // padded product (zeroed by the caller)
-  int64_t N, nb, m;                // padded dim, block grid, number of triples
+  const void *a, *b;                  // padded operands (N x N row-major)
+  void *c;                            // padded product (zeroed by the caller)
+  int64_t N, nb;
   int32_t leaf, depth;
-  const uint64_t *keys;            // sorted (i*nb + j) << depth | k
-  const int *group_starts;         // first triple of each C block
-  const int *num_groups;           // device-resident group count
-  unsigned long long *ticket;      // zeroed work ticket
+  const unsigned long long *n_codes;  // device count of retained triples
+  unsigned long long capacity;        // clamp for n_codes
+  const uint32_t *ks;                 // inner indices, sorted within each group
+  const uint32_t *group_ids;          // C block i*nb + j of each group
+  const uint32_t *group_starts;       // first triple of each group
+  LeafCounters *lc;                   // num_groups + work ticket
 };
 
-int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st);
+int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches);
 
 }  // namespace spamm

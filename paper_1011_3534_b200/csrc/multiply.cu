@@ -2,13 +2,20 @@
 // grouping, K3 (leaf products + merge) and K1 on the product (C's tree).
 //
 // Reference: spamm() multiply.py:144-221 and _leaf_stage :224-257.
-#include <cub/cub.cuh>
-
+//
+// The whole multiply is one fixed launch sequence on the device's stream:
+// every size the host must pass is static (tree geometry, buffer capacities)
+// and every data-dependent count stays on the device, so the host
+// synchronises exactly once, at the end, to read the statistics.  If a
+// capacity turned out too small (flagged by the kernels), the call is re-run
+// with larger buffers; capacities persist per device, so this happens at
+// most a few times per process.
 #include <algorithm>
 #include <memory>
 #include <vector>
 
 #include "cull.cuh"
+#include "group.cuh"
 #include "leaf.cuh"
 
 struct spamm_product {
@@ -20,33 +27,8 @@ namespace spamm {
 
 int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out);
 void free_tree_async(spamm_tree *t, cudaStream_t st);
-int build_pyramid_async(spamm_tree *t, cudaStream_t st);
+int build_pyramid_async(spamm_tree *t, cudaStream_t st, int *launches);
 int finish_tree(DeviceContext *ctx, spamm_tree *t);
-
-struct LeafCounters {
-  int num_groups;
-  int pad_;
-  unsigned long long ticket;
-};
-
-// Leaf triple (Morton code at the leaf tier) -> grouping key (i*nb + j) << depth | k.
-// Sorting by this key reproduces _leaf_stage's lexsort by (i, j, k) (multiply.py:231-233).
-__global__ void codes_to_keys_kernel(const uint64_t *__restrict__ codes, int64_t m, int depth,
-                                     int64_t nb, uint64_t *__restrict__ keys) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t i, j, k;
-    morton_decode(codes[p], i, j, k);
-    keys[p] = ((uint64_t(i) * nb + j) << depth) | k;
-  }
-}
-
-__global__ void group_heads_kernel(const uint64_t *__restrict__ keys, int64_t m, int depth,
-                                   uint8_t *__restrict__ flags) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
-       p += (int64_t)gridDim.x * blockDim.x)
-    flags[p] = p == 0 || (keys[p] >> depth) != (keys[p - 1] >> depth);
-}
 
 static int check_conformable(const spamm_tree *a, const spamm_tree *b) {
   // quadtree.py:209-215
@@ -71,6 +53,21 @@ static int check_conformable(const spamm_tree *a, const spamm_tree *b) {
   return SPAMM_OK;
 }
 
+struct HostCounters {
+  CullCounters cull;
+  LeafCounters leaf;
+};
+
+#define SPAMM_CUDA_BREAK(expr)                                                          \
+  {                                                                                     \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess) {                                                            \
+      set_error("CUDA error %s at %s:%d", cudaGetErrorString(_e), __FILE__, __LINE__); \
+      rc = _e == cudaErrorMemoryAllocation ? SPAMM_ERR_NOMEM : SPAMM_ERR_CUDA;          \
+      break;                                                                            \
+    }                                                                                   \
+  }
+
 static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, uint32_t flags,
                          int64_t row_lo, int64_t row_hi, spamm_tree **c_out, spamm_stats *stats,
                          spamm_product **product) {
@@ -84,8 +81,9 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
               (long long)row_hi, (long long)a->nb);
     return SPAMM_ERR_VALUE;
   }
-  if (a->depth >= MAX_TIERS - 1 || a->depth > 21) {
-    set_error("quadtree depth %d exceeds the supported 21 tiers", a->depth);
+  if (a->depth > 21 || a->nb * a->nb >= (int64_t(1) << 31)) {
+    set_error("quadtree depth %d / block grid %lld exceeds the supported range", a->depth,
+              (long long)a->nb);
     return SPAMM_ERR_VALUE;
   }
   DeviceContext *ctx;
@@ -94,20 +92,36 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   cudaStream_t st = ctx->stream;
   const int depth = a->depth;
   const int64_t nb = a->nb;
+  const int64_t G = nb * nb;
 
-  SPAMM_CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
-  // ---------------------------------------------------------------- K2 cull
-  if (ctx->cull_capacity == 0) ctx->cull_capacity = std::max<size_t>(1 << 16, 2 * nb * nb);
-  if (ctx->pruned_capacity == 0) ctx->pruned_capacity = std::max<size_t>(1 << 16, 2 * nb * nb);
-  CullCounters *hc = (CullCounters *)ctx->host_pinned;
+  if (ctx->cull_capacity == 0) ctx->cull_capacity = std::max<size_t>(1 << 16, 2 * G);
+  if (ctx->pruned_capacity == 0) ctx->pruned_capacity = std::max<size_t>(1 << 16, 2 * G);
+  HostCounters *hc = (HostCounters *)ctx->host_pinned;
+  spamm_tree *c = nullptr;
+  SPAMM_TRY(alloc_tree(ctx, a->n, a->leaf, a->dtype, &c));
+  int rc = SPAMM_OK;
+  int launches = 0;
   for (int attempt = 0;; ++attempt) {
+    launches = 0;
     const size_t cap = ctx->cull_capacity, pcap = ctx->pruned_capacity;
-    SPAMM_TRY(ensure_scratch(ctx->cull_codes[0], cap * sizeof(uint64_t), st));
-    SPAMM_TRY(ensure_scratch(ctx->cull_codes[1], cap * sizeof(uint64_t), st));
-    SPAMM_TRY(ensure_scratch(ctx->pruned_vals, pcap * sizeof(double), st));
-    SPAMM_TRY(ensure_scratch(ctx->pruned_codes, pcap * sizeof(uint64_t), st));
-    SPAMM_TRY(ensure_scratch(ctx->tile_status, tile_status_bytes(cap), st));
-    SPAMM_TRY(ensure_scratch(ctx->counters, sizeof(CullCounters) + sizeof(LeafCounters), st));
+    const size_t gcap = std::min<size_t>(cap, (size_t)G);
+    if ((rc = ensure_scratch(ctx->cull_codes[0], cap * sizeof(uint64_t), st))) break;
+    if ((rc = ensure_scratch(ctx->cull_codes[1], cap * sizeof(uint64_t), st))) break;
+    if ((rc = ensure_scratch(ctx->pruned_vals, pcap * sizeof(double), st))) break;
+    if ((rc = ensure_scratch(ctx->pruned_codes, pcap * sizeof(uint64_t), st))) break;
+    if ((rc = ensure_scratch(ctx->tile_status,
+                             std::max(tile_status_bytes(cap), group_tile_status_bytes(nb)), st)))
+      break;
+    if ((rc = ensure_scratch(ctx->counters, sizeof(CullCounters) + sizeof(LeafCounters), st)))
+      break;
+    if ((rc = ensure_scratch(ctx->keys[0], 2 * sizeof(uint32_t) * G, st))) break;  // counts, offsets
+    if ((rc = ensure_scratch(ctx->group_starts, 2 * sizeof(uint32_t) * gcap, st))) break;
+    if ((rc = ensure_scratch(ctx->keys[1], sizeof(uint32_t) * cap, st))) break;  // ks
+    CullCounters *dcc = (CullCounters *)ctx->counters.ptr;
+    LeafCounters *dlc = (LeafCounters *)((char *)ctx->counters.ptr + sizeof(CullCounters));
+
+    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[0], st));
+    // ---------------------------------------------------------------- K2 cull
     CullPlan plan{};
     plan.depth = depth;
     for (int t = 0; t <= depth; ++t)
@@ -123,167 +137,154 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     plan.pruned_codes = (uint64_t *)ctx->pruned_codes.ptr;
     plan.pruned_capacity = pcap;
     plan.tile_status = (unsigned long long *)ctx->tile_status.ptr;
-    plan.counters = (CullCounters *)ctx->counters.ptr;
+    plan.counters = dcc;
     plan.row_lo = row_lo;
     plan.row_hi = row_hi;
     plan.max_ctas = ctx->num_sms * 4;
-    SPAMM_TRY(launch_cull(plan, st));
-    SPAMM_CUDA_TRY(cudaMemcpyAsync(hc, ctx->counters.ptr, sizeof(CullCounters),
-                                   cudaMemcpyDeviceToHost, st));
-    SPAMM_CUDA_TRY(cudaStreamSynchronize(st));
-    if (!hc->overflow) break;
+    plan.launches = &launches;
+    if ((rc = launch_cull(plan, st))) break;
+    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
+
+    // ------------------------------------------------- grouping by C block
+    SPAMM_CUDA_BREAK(cudaMemsetAsync(dlc, 0, sizeof(LeafCounters), st));
+    GroupArgs ga{};
+    ga.codes = plan.codes[depth & 1];
+    ga.n_codes = &dcc->n_active[depth];
+    ga.capacity = cap;
+    ga.depth = depth;
+    ga.nb = nb;
+    ga.counts = (uint32_t *)ctx->keys[0].ptr;
+    ga.offsets = ga.counts + G;
+    ga.group_ids = (uint32_t *)ctx->group_starts.ptr;
+    ga.group_starts = ga.group_ids + gcap;
+    ga.ks = (uint32_t *)ctx->keys[1].ptr;
+    ga.tile_status = plan.tile_status;
+    ga.lc = dlc;
+    if ((rc = launch_grouping(ga, (int64_t)cap, ctx->num_sms, st, &launches))) break;
+
+    // ------------------------------------------------ K3 leaf products -> C
+    SPAMM_CUDA_BREAK(cudaMemsetAsync(c->padded, 0, (size_t)(c->N * c->N * c->elem_size()), st));
+    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[2], st));
+    LeafArgs la{};
+    la.a = a->padded;
+    la.b = b->padded;
+    la.c = c->padded;
+    la.N = a->N;
+    la.nb = nb;
+    la.leaf = a->leaf;
+    la.depth = depth;
+    la.n_codes = ga.n_codes;
+    la.capacity = cap;
+    la.ks = ga.ks;
+    la.group_ids = ga.group_ids;
+    la.group_starts = ga.group_starts;
+    la.lc = dlc;
+    if ((rc = launch_leaf(la, a->dtype, ctx->num_sms, st, &launches))) break;
+    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[3], st));
+
+    // ------------------------------------------- C's tree (multiply.py:220)
+    if ((rc = build_pyramid_async(c, st, &launches))) break;
+    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
+    SPAMM_CUDA_BREAK(cudaMemcpyAsync(&hc->cull, dcc, sizeof(CullCounters), cudaMemcpyDeviceToHost, st));
+    SPAMM_CUDA_BREAK(cudaMemcpyAsync(&hc->leaf, dlc, sizeof(LeafCounters), cudaMemcpyDeviceToHost, st));
+    SPAMM_CUDA_BREAK(cudaMemcpyAsync(&c->root_norm_sq, c->nsq, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SPAMM_CUDA_BREAK(cudaStreamSynchronize(st));
+    if (!hc->cull.overflow) break;
     unsigned long long need = 0, pneed = 0;
     for (int t = 0; t <= depth; ++t) {
-      need = std::max(need, hc->n_active[t]);
-      pneed += hc->n_pruned[t];
+      need = std::max(need, hc->cull.n_active[t]);
+      pneed += hc->cull.n_pruned[t];
     }
     ctx->cull_capacity = std::max<size_t>(2 * cap, need + need / 8);
     ctx->pruned_capacity = std::max<size_t>(need > cap ? pcap : 2 * pcap, pneed + pneed / 8);
     if (attempt > 40) {
       set_error("culling capacity did not converge");
-      return SPAMM_ERR_INTERNAL;
+      rc = SPAMM_ERR_INTERNAL;
+      break;
     }
   }
-  SPAMM_CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
-
-  // --------------------------------------------------------- stats (host)
-  spamm_stats s{};
-  const bool counting = (flags & SPAMM_COUNT_STATS) != 0;
-  for (int t = 0; t <= depth; ++t) {
-    s.tier_candidates[t] = (int64_t)hc->n_cand[t];
-    s.tier_survivors[t] = (int64_t)hc->n_active[t];
-    s.tier_pruned[t] = (int64_t)hc->n_pruned[t];
-    if (hc->n_cand[t] > 0) s.max_depth_reached = t;  // multiply.py:181
-    if (counting) {
-      const int64_t edge = a->N >> t;
-      const int64_t vol = edge * edge * edge;
-      s.pruned_calls += (int64_t)(hc->n_skip[t] + hc->n_pruned[t]);
-      s.empty_skip_volume += (int64_t)hc->n_skip[t] * vol;
-      s.pruned_volume += (int64_t)hc->n_pruned[t] * vol;
-    }
-  }
-  const int64_t m = (int64_t)hc->n_active[depth];
-  if (counting) {
-    s.leaf_matmuls = m;
-    s.omitted_budget = hc->budget;
-  }
-  s.n_triples = m;
-  int64_t total_pruned = 0;
-  for (int t = 0; t <= depth; ++t) total_pruned += (int64_t)hc->n_pruned[t];
-  s.n_boxes = (flags & SPAMM_COLLECT_BOXES) ? total_pruned : 0;
-
-  // ----------------------------------------------------- C tree + leaf stage
-  spamm_tree *c = nullptr;
-  SPAMM_TRY(alloc_tree(ctx, a->n, a->leaf, a->dtype, &c));
-  int rc = SPAMM_OK;
-  std::vector<uint64_t> host_keys;
-  do {
-    cudaError_t e = cudaMemsetAsync(c->padded, 0, (size_t)(c->N * c->N * c->elem_size()), st);
-    if (e != cudaSuccess) { set_error("memset C: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-    if (m > 0) {
-      uint64_t *codes = (uint64_t *)ctx->cull_codes[depth & 1].ptr;
-      if ((rc = ensure_scratch(ctx->keys[0], m * sizeof(uint64_t), st))) break;
-      if ((rc = ensure_scratch(ctx->keys[1], m * sizeof(uint64_t), st))) break;
-      if ((rc = ensure_scratch(ctx->flags, m, st))) break;
-      if ((rc = ensure_scratch(ctx->group_starts, m * sizeof(int), st))) break;
-      uint64_t *k0 = (uint64_t *)ctx->keys[0].ptr, *k1 = (uint64_t *)ctx->keys[1].ptr;
-      const int grid = (int)std::min<int64_t>((m + 255) / 256, ctx->num_sms * 8);
-      codes_to_keys_kernel<<<grid, 256, 0, st>>>(codes, m, depth, nb, k0);
-      size_t sort_bytes = 0, sel_bytes = 0;
-      const int end_bit = std::max(1, 3 * depth);
-      cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, k0, k1, m, 0, end_bit, st);
-      LeafCounters *lc = (LeafCounters *)((char *)ctx->counters.ptr + sizeof(CullCounters));
-      cub::CountingInputIterator<int> ids(0);
-      cub::DeviceSelect::Flagged(nullptr, sel_bytes, ids, (uint8_t *)ctx->flags.ptr,
-                                 (int *)ctx->group_starts.ptr, &lc->num_groups, m, st);
-      if ((rc = ensure_scratch(ctx->cub_temp, std::max(sort_bytes, sel_bytes), st))) break;
-      sort_bytes = sel_bytes = ctx->cub_temp.bytes;
-      e = cub::DeviceRadixSort::SortKeys(ctx->cub_temp.ptr, sort_bytes, k0, k1, m, 0, end_bit, st);
-      if (e != cudaSuccess) { set_error("sort: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-      group_heads_kernel<<<grid, 256, 0, st>>>(k1, m, depth, (uint8_t *)ctx->flags.ptr);
-      e = cub::DeviceSelect::Flagged(ctx->cub_temp.ptr, sel_bytes, ids, (uint8_t *)ctx->flags.ptr,
-                                     (int *)ctx->group_starts.ptr, &lc->num_groups, m, st);
-      if (e != cudaSuccess) { set_error("select: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-      e = cudaMemsetAsync(&lc->ticket, 0, sizeof(unsigned long long), st);
-      if (e != cudaSuccess) { set_error("memset: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-      LeafArgs la{};
-      la.a = a->padded;
-      la.b = b->padded;
-      la.c = c->padded;
-      la.N = a->N;
-      la.nb = nb;
-      la.m = m;
-      la.leaf = a->leaf;
-      la.depth = depth;
-      la.keys = k1;
-      la.group_starts = (const int *)ctx->group_starts.ptr;
-      la.num_groups = &lc->num_groups;
-      la.ticket = &lc->ticket;
-      if ((rc = launch_leaf(la, a->dtype, ctx->num_sms, st))) break;
-      if (flags & SPAMM_KEEP_TRIPLES) {
-        host_keys.resize(m);
-        e = cudaMemcpyAsync(host_keys.data(), k1, m * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
-        if (e != cudaSuccess) { set_error("copy: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-      }
-      e = cudaMemcpyAsync(&s.n_groups, &lc->num_groups, sizeof(int), cudaMemcpyDeviceToHost, st);
-      if (e != cudaSuccess) { set_error("copy: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-    }
-    e = cudaEventRecord(ctx->ev[2], st);
-    if (e != cudaSuccess) { set_error("event: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-    // C's tree: the reference rebuilds it with QuadTreeMatrix.__init__ (multiply.py:220)
-    if ((rc = build_pyramid_async(c, st))) break;
-    e = cudaEventRecord(ctx->ev[3], st);
-    if (e != cudaSuccess) { set_error("event: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-    if ((rc = finish_tree(ctx, c))) break;  // syncs the stream
-  } while (0);
   if (rc) {
     free_tree_async(c, st);
     return rc;
   }
-  s.n_groups &= 0xffffffffll;
+  const CullCounters &cc = hc->cull;
+
+  // --------------------------------------------------------- stats (host)
+  spamm_stats s{};
+  const bool counting = (flags & SPAMM_COUNT_STATS) != 0;
+  int64_t total_pruned = 0;
+  for (int t = 0; t <= depth; ++t) {
+    s.tier_candidates[t] = (int64_t)cc.n_cand[t];
+    s.tier_survivors[t] = (int64_t)cc.n_active[t];
+    s.tier_pruned[t] = (int64_t)cc.n_pruned[t];
+    total_pruned += (int64_t)cc.n_pruned[t];
+    if (cc.n_cand[t] > 0) s.max_depth_reached = t;  // multiply.py:181
+    if (counting) {
+      const int64_t edge = a->N >> t;
+      const int64_t vol = edge * edge * edge;
+      s.pruned_calls += (int64_t)(cc.n_skip[t] + cc.n_pruned[t]);
+      s.empty_skip_volume += (int64_t)cc.n_skip[t] * vol;
+      s.pruned_volume += (int64_t)cc.n_pruned[t] * vol;
+    }
+  }
+  const int64_t m = (int64_t)cc.n_active[depth];
+  if (counting) {
+    s.leaf_matmuls = m;
+    s.omitted_budget = cc.budget;
+  }
+  s.n_triples = m;
+  s.n_groups = hc->leaf.num_groups;
+  s.n_boxes = (flags & SPAMM_COLLECT_BOXES) ? total_pruned : 0;
+  s.kernel_launches = launches;
   cudaEventElapsedTime(&s.ms_cull, ctx->ev[0], ctx->ev[1]);
-  cudaEventElapsedTime(&s.ms_leaf, ctx->ev[1], ctx->ev[2]);
-  cudaEventElapsedTime(&s.ms_ctree, ctx->ev[2], ctx->ev[3]);
-  cudaEventElapsedTime(&s.ms_total, ctx->ev[0], ctx->ev[3]);
+  cudaEventElapsedTime(&s.ms_leaf, ctx->ev[1], ctx->ev[3]);
+  cudaEventElapsedTime(&s.ms_gemm, ctx->ev[2], ctx->ev[3]);
+  cudaEventElapsedTime(&s.ms_ctree, ctx->ev[3], ctx->ev[4]);
+  cudaEventElapsedTime(&s.ms_total, ctx->ev[0], ctx->ev[4]);
 
   // ------------------------------------------------------- product records
   if (product) {
     auto p = std::make_unique<spamm_product>();
-    if (flags & SPAMM_COLLECT_BOXES) {
+    cudaError_t e = cudaSuccess;
+    if ((flags & SPAMM_COLLECT_BOXES) && total_pruned) {
       std::vector<uint64_t> codes(total_pruned);
-      if (total_pruned) {
-        cudaError_t e = cudaMemcpy(codes.data(), ctx->pruned_codes.ptr,
-                                   total_pruned * sizeof(uint64_t), cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) {
-          free_tree_async(c, st);
-          set_error("copy boxes: %s", cudaGetErrorString(e));
-          return SPAMM_ERR_CUDA;
-        }
-      }
+      e = cudaMemcpy(codes.data(), ctx->pruned_codes.ptr, total_pruned * sizeof(uint64_t),
+                     cudaMemcpyDeviceToHost);
       p->boxes.reserve(5 * total_pruned);
       int64_t pos = 0;
-      for (int t = 0; t <= depth; ++t) {
+      for (int t = 0; t <= depth && e == cudaSuccess; ++t) {
         const int64_t edge = a->N >> t;
-        for (unsigned long long q = 0; q < hc->n_pruned[t]; ++q, ++pos) {
+        for (unsigned long long q = 0; q < cc.n_pruned[t]; ++q, ++pos) {
           uint32_t i, j, k;
           morton_decode(codes[pos], i, j, k);
-          p->boxes.push_back(int64_t(i) * edge);
-          p->boxes.push_back(int64_t(j) * edge);
-          p->boxes.push_back(int64_t(k) * edge);
-          p->boxes.push_back(edge);
-          p->boxes.push_back(t);
+          p->boxes.insert(p->boxes.end(),
+                          {int64_t(i) * edge, int64_t(j) * edge, int64_t(k) * edge, edge, t});
         }
       }
     }
-    if (flags & SPAMM_KEEP_TRIPLES) {
-      const uint64_t kmask = (uint64_t(1) << depth) - 1;
+    if ((flags & SPAMM_KEEP_TRIPLES) && m && e == cudaSuccess) {
+      const int64_t ng = s.n_groups;
+      const size_t gcap = std::min<size_t>(ctx->cull_capacity, G);
+      std::vector<uint32_t> ids(ng), starts(ng), ks(m);
+      e = cudaMemcpy(ids.data(), ctx->group_starts.ptr, ng * sizeof(uint32_t),
+                     cudaMemcpyDeviceToHost);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(starts.data(), (uint32_t *)ctx->group_starts.ptr + gcap,
+                       ng * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(ks.data(), ctx->keys[1].ptr, m * sizeof(uint32_t), cudaMemcpyDeviceToHost);
       p->triples.reserve(3 * m);
-      for (int64_t q = 0; q < m; ++q) {
-        const uint64_t gid = host_keys[q] >> depth;
-        p->triples.push_back((int32_t)(gid / nb));
-        p->triples.push_back((int32_t)(gid % nb));
-        p->triples.push_back((int32_t)(host_keys[q] & kmask));
+      for (int64_t q = 0; q < ng && e == cudaSuccess; ++q) {
+        const int64_t end = q + 1 < ng ? starts[q + 1] : m;
+        for (int64_t x = starts[q]; x < end; ++x)
+          p->triples.insert(p->triples.end(), {(int32_t)(ids[q] / nb), (int32_t)(ids[q] % nb),
+                                               (int32_t)ks[x]});
       }
+    }
+    if (e != cudaSuccess) {
+      free_tree_async(c, st);
+      set_error("copy of product records: %s", cudaGetErrorString(e));
+      return SPAMM_ERR_CUDA;
     }
     *product = p.release();
   }

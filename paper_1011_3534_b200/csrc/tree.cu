@@ -79,15 +79,20 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream) {
 // rounding).  The parallelism is across leaves only -- a per-leaf shuffle
 // tree would change the bits the strict `< tau` tests compare.
 //
-// Data movement: a CTA owns LT = 128 consecutive leaves (row-major leaf
-// order).  Each leaf is streamed in 128-byte chunks (one row piece, or
-// several full rows for b < 16) through a STAGES-deep cp.async pipeline into
-// shared memory with 16 B of padding per leaf, so the per-thread LDS.128
-// reads are bank-conflict free while the global reads stay fully coalesced
-// (every 128 B line is consumed whole).
-constexpr int K1_LT = 128;
-constexpr int K1_STAGES = 4;
-constexpr int K1_LEAF_STRIDE = 144;  // bytes per leaf chunk in smem (128 + 16 pad)
+// Data movement: a CTA owns K1_LT = 32 consecutive leaves (row-major leaf
+// order); its first warp runs the 32 sequential chains, all four warps feed
+// a K1_STAGES-deep cp.async pipeline.  Each stage holds one 512-byte piece
+// of every leaf (a full leaf row for b = 64 doubles; several rows for
+// smaller leaves), stored with 16 B of padding per leaf so the per-lane
+// LDS.128 reads are bank-conflict free while every global read consumes
+// whole 128-byte lines.  Small CTAs spread even a 64 x 64-leaf tree over
+// the whole chip; the deep pipeline keeps ~100 KB in flight per SM, which
+// is what HBM3e needs to stream at full rate.
+constexpr int K1_LT = 32;
+constexpr int K1_THREADS = 128;
+constexpr int K1_STAGES = 6;
+constexpr int K1_CHUNK = 512;                  // bytes per leaf per stage
+constexpr int K1_LEAF_STRIDE = K1_CHUNK + 16;  // smem bytes per leaf per stage
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -131,40 +136,57 @@ __device__ void canonicalise_leaf(T *padded, int64_t N, int32_t b, int64_t bi, i
   }
 }
 
-// Staged kernel, b * sizeof(T) >= 16 and b*b*sizeof(T) >= 128.
+// Staged kernel: requires b * sizeof(T) >= 16.
 template <typename T>
-__global__ void __launch_bounds__(K1_LT) leaf_norm_staged_kernel(T *__restrict__ padded, int64_t N,
-                                                                 int32_t b, int64_t nb,
-                                                                 double *__restrict__ nsq_leaf,
-                                                                 uint8_t *__restrict__ occ_leaf) {
-  constexpr int EPC = 128 / sizeof(T);  // elements per 128-byte chunk
+__global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restrict__ padded,
+                                                                      int64_t N, int32_t b,
+                                                                      int64_t nb,
+                                                                      double *__restrict__ nsq_leaf,
+                                                                      uint8_t *__restrict__ occ_leaf) {
   extern __shared__ __align__(16) unsigned char k1_smem[];
   const int64_t n_leaves = nb * nb;
   const int64_t leaf0 = (int64_t)blockIdx.x * K1_LT;
   const int tid = threadIdx.x;
+  const int64_t bb = (int64_t)b * b;
+  const int EPC = (int)(bb < K1_CHUNK / (int)sizeof(T) ? bb : K1_CHUNK / (int)sizeof(T));
   const int CW = b < EPC ? b : EPC;      // chunk width (elements)
   const int R = EPC / CW;                // rows per chunk
   const int chunks_per_row = b / CW;
   const int n_chunks = (b / R) * chunks_per_row;
+  const int segs = EPC * (int)sizeof(T) / 16;  // 16-byte segments per leaf chunk
+  const int EPS = 16 / (int)sizeof(T);         // elements per segment
 
-  auto issue = [&](int chunk, int stage) {
-    const int r0 = (chunk / chunks_per_row) * R;
-    const int c0 = (chunk % chunks_per_row) * CW;
-    unsigned char *base = k1_smem + stage * (K1_LT * K1_LEAF_STRIDE);
-    // K1_LT leaves x 8 segments of 16 B
+  // Each thread copies the same (leaf, 16-byte segment) slots in every chunk;
+  // resolve their global addresses once (no 64-bit divisions in the loop).
+  constexpr int MAX_SLOTS = K1_LT * (K1_CHUNK / 16) / K1_THREADS;
+  const T *slot_ptr[MAX_SLOTS];
+  unsigned slot_dst[MAX_SLOTS];
+  int n_slots = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int s = tid + q * K1_LT;
-      const int l = s >> 3, part = s & 7;
+  for (int q = 0; q < MAX_SLOTS; ++q) {
+    const int s = tid + q * K1_THREADS;
+    slot_ptr[q] = nullptr;
+    slot_dst[q] = 0;
+    if (s < K1_LT * segs) {
+      const int l = s / segs, part = s - l * segs;
       const int64_t leaf = leaf0 + l;
       if (leaf < n_leaves) {
         const int64_t bi = leaf / nb, bj = leaf - bi * nb;
-        const int e = part * (16 / (int)sizeof(T));  // element offset within chunk
+        const int e = part * EPS;
         const int rr = e / CW, cc = e - rr * CW;
-        const T *g = padded + (bi * b + r0 + rr) * N + bj * b + c0 + cc;
-        cp_async16(base + l * K1_LEAF_STRIDE + part * 16, g);
+        slot_ptr[q] = padded + (bi * b + rr) * N + bj * b + cc;
+        slot_dst[q] = l * K1_LEAF_STRIDE + part * 16;
+        n_slots = q + 1;
       }
     }
+  }
+  const int shift_cpr = __ffs(chunks_per_row) - 1;  // chunks_per_row is a power of two
+  auto issue = [&](int chunk, int stage) {
+    const int64_t off = (int64_t)((chunk >> shift_cpr) * R) * N + (chunk & (chunks_per_row - 1)) * CW;
+    unsigned char *base = k1_smem + stage * (K1_LT * K1_LEAF_STRIDE);
+#pragma unroll
+    for (int q = 0; q < MAX_SLOTS; ++q)
+      if (q < n_slots && slot_ptr[q]) cp_async16(base + slot_dst[q], slot_ptr[q] + off);
   };
 
   const int64_t my_leaf = leaf0 + tid;
@@ -181,11 +203,10 @@ __global__ void __launch_bounds__(K1_LT) leaf_norm_staged_kernel(T *__restrict__
     const int nxt = chunk + K1_STAGES - 1;
     if (nxt < n_chunks) issue(nxt, nxt % K1_STAGES);
     cp_async_commit();
-    if (my_leaf < n_leaves) {
+    if (tid < K1_LT && my_leaf < n_leaves) {
       const unsigned char *p = k1_smem + (chunk % K1_STAGES) * (K1_LT * K1_LEAF_STRIDE) +
                                tid * K1_LEAF_STRIDE;
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
+      for (int v = 0; v < segs; ++v) {
         const uint4 w = *reinterpret_cast<const uint4 *>(p + 16 * v);
         const T *x = reinterpret_cast<const T *>(&w);
 #pragma unroll
@@ -194,7 +215,7 @@ __global__ void __launch_bounds__(K1_LT) leaf_norm_staged_kernel(T *__restrict__
     }
   }
   cp_async_wait<0>();
-  if (my_leaf < n_leaves) {
+  if (tid < K1_LT && my_leaf < n_leaves) {
     nsq_leaf[my_leaf] = acc;
     occ_leaf[my_leaf] = (uint8_t)(nz != 0);
     if (!nz && negz) {
@@ -279,12 +300,12 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st) {
   const int64_t n_leaves = t->nb * t->nb;
   double *nsq_leaf = t->nsq + level_offset(t->depth);
   uint8_t *occ_leaf = t->occ + level_offset(t->depth);
-  if ((int64_t)t->leaf * t->leaf * (int64_t)sizeof(T) >= 128 && t->leaf * sizeof(T) >= 16) {
+  if (t->leaf * sizeof(T) >= 16) {
     const size_t smem = (size_t)K1_STAGES * K1_LT * K1_LEAF_STRIDE;
     SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_norm_staged_kernel<T>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t grid = (n_leaves + K1_LT - 1) / K1_LT;
-    leaf_norm_staged_kernel<T><<<(unsigned)grid, K1_LT, smem, st>>>(
+    leaf_norm_staged_kernel<T><<<(unsigned)grid, K1_THREADS, smem, st>>>(
         (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf);
   } else {
     const int64_t grid = (n_leaves + 127) / 128;
@@ -297,15 +318,17 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st) {
 
 // Rebuild the whole pyramid of `t` from its padded storage (canonicalising
 // all-zero leaves in place).  Stream-ordered; no host sync.
-int build_pyramid_async(spamm_tree *t, cudaStream_t st) {
+int build_pyramid_async(spamm_tree *t, cudaStream_t st, int *launches) {
   if (t->dtype == SPAMM_DTYPE_F64) SPAMM_TRY(launch_leaf_norms<double>(t, st));
   else SPAMM_TRY(launch_leaf_norms<float>(t, st));
+  if (launches) ++*launches;
   int from = t->depth;
   while (from > 0) {
     const int L = from < 5 ? from : 5;
     const int64_t tiles = int64_t(1) << (2 * (from - L));
     pyramid_kernel<<<(unsigned)tiles, PYR_THREADS, 0, st>>>(t->nsq, t->occ, from, L);
     SPAMM_CUDA_TRY(cudaGetLastError());
+    if (launches) ++*launches;
     from -= L;
   }
   return SPAMM_OK;
@@ -385,7 +408,7 @@ static int tree_from(const void *src, bool src_on_host, int64_t n, int64_t ld, i
                           src_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                           ctx->stream);
     if (e != cudaSuccess) { set_error("copy: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-    rc = build_pyramid_async(t, ctx->stream);
+    rc = build_pyramid_async(t, ctx->stream, nullptr);
     if (rc) break;
     rc = finish_tree(ctx, t);
   } while (0);

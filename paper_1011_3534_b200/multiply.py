@@ -89,6 +89,8 @@ class MultiplyDetail:
     ms_leaf: float = 0.0
     ms_ctree: float = 0.0
     ms_total: float = 0.0
+    ms_gemm: float = 0.0
+    kernel_launches: int = 0
 
 
 def _flags(config, keep_triples):
@@ -136,7 +138,8 @@ def spamm_detailed(a, b, config=None, keep_triples=False, rows=None):
                                 tier_survivors=list(st.tier_survivors[:depth + 1]),
                                 tier_pruned=list(st.tier_pruned[:depth + 1]),
                                 n_groups=int(st.n_groups), ms_cull=st.ms_cull,
-                                ms_leaf=st.ms_leaf, ms_ctree=st.ms_ctree, ms_total=st.ms_total)
+                                ms_leaf=st.ms_leaf, ms_ctree=st.ms_ctree, ms_total=st.ms_total,
+                                ms_gemm=st.ms_gemm, kernel_launches=int(st.kernel_launches))
         if config.collect_boxes and st.n_boxes:
             raw = np.empty((int(st.n_boxes), 5), np.int64)
             _lib.check(L.spamm_product_boxes(prod, raw.ctypes.data, int(st.n_boxes)))

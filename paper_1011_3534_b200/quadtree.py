@@ -202,10 +202,18 @@ class QuadTreeMatrix:
         return self._occupied[self.depth]
 
     # -- queries --------------------------------------------------------------
-    def to_dense(self):
-        """Fresh n x n host array with the padding stripped (quadtree.py:184-187)."""
+    def to_dense(self, out=None):
+        """Fresh n x n host array with the padding stripped (quadtree.py:184-187).
+
+        ``out`` (extension): an existing C-contiguous n x n host array of the
+        tree's dtype to copy into -- e.g. pinned memory for fast transfers.
+        """
         n = self.logical_dim
-        out = np.empty((n, n), dtype=self.dtype)
+        if out is None:
+            out = np.empty((n, n), dtype=self.dtype)
+        elif (out.shape != (n, n) or out.dtype != self.dtype
+              or not out.flags.c_contiguous or not out.flags.writeable):
+            raise ValueError("out must be a writeable C-contiguous (n, n) array of the tree dtype")
         _lib.check(_lib.load().spamm_tree_to_host(self._handle, out.ctypes.data, n))
         return out
 
@@ -288,9 +296,9 @@ def identity(n, leaf_size=4, dtype=None):
     return from_dense(np.eye(n), leaf_size=leaf_size, dtype=dtype)
 
 
-def to_dense(m):
+def to_dense(m, out=None):
     """Function form of m.to_dense() (quadtree.py:264-266)."""
-    return m.to_dense()
+    return m.to_dense(out=out)
 
 
 def node_norm(m):
