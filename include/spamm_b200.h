@@ -93,6 +93,9 @@ typedef struct {
   float ms_total;
   float ms_gemm;           /* the leaf-product kernel (K3) alone          */
   int32_t kernel_launches; /* kernels this call launched                  */
+  /* traversal-kernel phase boundaries (device %globaltimer, us since start):
+   * prefix end, barrier, grid tiers..., histogram, scan, scatter, sort */
+  float traverse_phase_us[14];
 } spamm_stats;
 
 SPAMM_API const char *spamm_last_error(void);

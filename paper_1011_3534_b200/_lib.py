@@ -57,7 +57,8 @@ class Stats(ctypes.Structure):
                 ("tier_pruned", ctypes.c_int64 * 32),
                 ("ms_cull", ctypes.c_float), ("ms_leaf", ctypes.c_float),
                 ("ms_ctree", ctypes.c_float), ("ms_total", ctypes.c_float),
-                ("ms_gemm", ctypes.c_float), ("kernel_launches", ctypes.c_int32)]
+                ("ms_gemm", ctypes.c_float), ("kernel_launches", ctypes.c_int32),
+                ("traverse_phase_us", ctypes.c_float * 14)]
 
 
 _lock = threading.Lock()

@@ -85,17 +85,17 @@ struct DeviceContext {
   int device = -1;
   int num_sms = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;       // overlaps memory-bound fills with compute
+  cudaEvent_t fork = nullptr, join = nullptr;
   cudaEvent_t ev[8] = {};
   std::mutex mu;
   Scratch cull_codes[2];  // ping-pong survivor lists (u64 Morton codes)
   Scratch pruned_codes;   // pruned codes, all tiers (u64)
   Scratch pruned_vals;    // pruned norm products, all tiers (f64)
   Scratch tile_status;    // decoupled look-back state
-  Scratch counters;       // device counters (CullCounters)
-  Scratch keys[2];        // leaf triple sort keys (u64) + alt buffer
-  Scratch group_starts;   // first triple of each C block group
-  Scratch flags;          // head flags / misc bytes
-  Scratch cub_temp;       // cub temporary storage
+  Scratch counters;       // device counters (TraverseCounters) + grid barrier
+  Scratch keys[2];        // bucket counts/offsets, grouped inner indices
+  Scratch group_starts;   // non-empty C blocks and their first triple
   Scratch reduce_tmp;     // misc reduction scratch
   size_t cull_capacity = 0;   // survivor capacity per ping-pong buffer (items)
   size_t pruned_capacity = 0; // pruned capacity (items, all tiers)
@@ -103,7 +103,7 @@ struct DeviceContext {
 };
 
 int get_context(int device, DeviceContext **ctx);
-int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream);
+int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed = false);
 
 }  // namespace spamm
 
@@ -118,6 +118,7 @@ struct spamm_tree {
   void *padded = nullptr;   // N x N row-major, element type per dtype
   double *nsq = nullptr;    // concatenated squared-norm pyramid
   uint8_t *occ = nullptr;   // concatenated occupancy pyramid
+  double *nrm = nullptr;    // rn(sqrt(nsq)): the factors of the pruning test
   double root_norm_sq = 0.0;
   int64_t elem_size() const { return dtype == SPAMM_DTYPE_F64 ? 8 : 4; }
 };

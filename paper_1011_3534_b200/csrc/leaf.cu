@@ -43,6 +43,14 @@ __device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8],
         "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
+// One DMMA.8x8x4: C(8x8) += A(8x4) B(4x8), f64, inner index ascending.  Not
+// volatile, so the scheduler may interleave independent accumulators.
+__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
 // Level at which two distinct inner indices meet in the merge tree.
 __device__ __forceinline__ int merge_level(uint32_t k0, uint32_t k1) {
   return 32 - __clz(k0 ^ k1);
@@ -56,10 +64,10 @@ struct WorkItem {
 
 __device__ __forceinline__ bool fetch_work(const LeafArgs &args, int subs_side, int *s_work,
                                            WorkItem &w) {
-  if (threadIdx.x == 0) *s_work = (int)atomicAdd(&args.lc->gemm_ticket, 1ull);
+  if (threadIdx.x == 0) *s_work = (int)atomicAdd(&args.tc->gemm_ticket, 1ull);
   __syncthreads();
   const int item = *s_work;
-  const int ng = (int)args.lc->num_groups;
+  const int ng = (int)args.tc->num_groups;
   const int subs = subs_side * subs_side;
   if (item >= ng * subs) return false;
   const int grp = item / subs, sub = item - grp * subs;
@@ -110,6 +118,8 @@ struct DmmaCfg {
 template <int TILE, int WM, int WN>
 __global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) {
   using C = DmmaCfg<TILE, WM, WN>;
+  constexpr int QA = (TILE * DMMA_BK / 2) / C::THREADS;  // 16-B copies per thread, A stage
+  constexpr int QB = (DMMA_BK * TILE / 2) / C::THREADS;  // 16-B copies per thread, B stage
   extern __shared__ __align__(16) double dsm[];
   __shared__ int s_work;
   __shared__ uint32_t s_ks[KS_SMEM];
@@ -123,6 +133,35 @@ __global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) 
   const double *__restrict__ A = (const double *)args.a;
   const double *__restrict__ B = (const double *)args.b;
   double *__restrict__ Cm = (double *)args.c;
+
+  // ---- loop-invariant shared-memory fragment offsets (elements in a stage).
+  // Fragment rows of A are wm*WTM + mt*16 + 8h + g and rows of B are
+  // kk + 4*s4 + t, so the swizzle key (row & 3) is g & 3 for A and t for B.
+  const int a_row0 = (wm * C::WTM + g) * C::SA;
+  int a_col[2][4];
+#pragma unroll
+  for (int kq = 0; kq < 2; ++kq)
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4) a_col[kq][s4] = swz(g, 16 * kq + 4 * s4 + t);
+  int b_col[C::NT];
+#pragma unroll
+  for (int nt = 0; nt < C::NT; ++nt)
+    b_col[nt] = C::A_ELEMS + t * C::SB + swz(t, wn * C::WTN + nt * 8 + g);
+  // ---- loop-invariant copy slots (smem offset, global offset from the tile origin)
+  int sA[QA], sB[QB];
+  int64_t gA[QA], gB[QB];
+#pragma unroll
+  for (int q = 0; q < QA; ++q) {
+    const int e = tid + q * C::THREADS, r = e / (DMMA_BK / 2), c2 = e % (DMMA_BK / 2);
+    sA[q] = r * C::SA + swz(r, 2 * c2);
+    gA[q] = (int64_t)r * N + 2 * c2;
+  }
+#pragma unroll
+  for (int q = 0; q < QB; ++q) {
+    const int e = tid + q * C::THREADS, r = e / (TILE / 2), c2 = e % (TILE / 2);
+    sB[q] = C::A_ELEMS + r * C::SB + swz(r, 2 * c2);
+    gB[q] = (int64_t)r * N + 2 * c2;
+  }
 
   // Merge stack of the reference's tree order (see merge_level): pending
   // left operands are keyed by tree level; the op levels on the stack are
@@ -141,29 +180,18 @@ __global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) 
       for (int e = tid; e < nk; e += C::THREADS) s_ks[e] = args.ks[w.start + e];
     __syncthreads();
     const uint32_t *ks = ks_in_smem ? s_ks : args.ks + w.start;
-    const double *Arow = A + (int64_t(w.i) * b + w.si * TILE) * N;
-    const int64_t bcol = int64_t(w.j) * b + w.sj * TILE;
+    const double *a_org = A + (int64_t(w.i) * b + w.si * TILE) * N;
+    const double *b_org = B + int64_t(w.j) * b + w.sj * TILE;
 
     auto issue = [&](int64_t step) {
-      const int stage = (int)(step % DMMA_STAGES);
-      const int64_t s = step >> kshift;
-      const int kc = (int)(step & (kchunks - 1));
-      const uint32_t k = ks[s];
-      double *As = dsm + stage * C::STAGE_ELEMS;
-      double *Bs = As + C::A_ELEMS;
-      const int64_t kcol = int64_t(k) * b + kc * DMMA_BK;
+      double *stg = dsm + (int)(step % DMMA_STAGES) * C::STAGE_ELEMS;
+      const int64_t kcol = int64_t(ks[step >> kshift]) * b + (int)(step & (kchunks - 1)) * DMMA_BK;
+      const double *asrc = a_org + kcol;
+      const double *bsrc = b_org + kcol * N;
 #pragma unroll
-      for (int q = 0; q < (TILE * DMMA_BK / 2) / C::THREADS; ++q) {
-        const int e = tid + q * C::THREADS;
-        const int r = e / (DMMA_BK / 2), c2 = e % (DMMA_BK / 2);
-        cp_async16_l(As + r * C::SA + swz(r, 2 * c2), Arow + r * N + kcol + 2 * c2);
-      }
+      for (int q = 0; q < QA; ++q) cp_async16_l(stg + sA[q], asrc + gA[q]);
 #pragma unroll
-      for (int q = 0; q < (DMMA_BK * TILE / 2) / C::THREADS; ++q) {
-        const int e = tid + q * C::THREADS;
-        const int r = e / (TILE / 2), c2 = e % (TILE / 2);
-        cp_async16_l(Bs + r * C::SB + swz(r, 2 * c2), B + (kcol + r) * N + bcol + 2 * c2);
-      }
+      for (int q = 0; q < QB; ++q) cp_async16_l(stg + sB[q], bsrc + gB[q]);
     };
 
 #pragma unroll
@@ -187,29 +215,34 @@ __global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) 
       __syncthreads();
       if (step + DMMA_STAGES - 1 < nsteps) issue(step + DMMA_STAGES - 1);
       cp_commit();
-      const double *As = dsm + (int)(step % DMMA_STAGES) * C::STAGE_ELEMS;
-      const double *Bs = As + C::A_ELEMS;
+      const double *stg = dsm + (int)(step % DMMA_STAGES) * C::STAGE_ELEMS;
+      const double *Ab = stg + a_row0;
 #pragma unroll
-      for (int kk = 0; kk < DMMA_BK; kk += 16) {
-        double af[C::MT][8];
+      for (int kq = 0; kq < 2; ++kq) {
+        // fragments of four k4 steps; every accumulator sees its inner index
+        // in ascending order (k4 steps in order, each DMMA ascending inside)
+        double af[C::MT][2][4], bf[C::NT][4];
 #pragma unroll
         for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int r = wm * C::WTM + mt * 16 + g + 8 * (q & 1);
-            af[mt][q] = As[r * C::SA + swz(r, kk + t + 4 * (q >> 1))];
-          }
+          for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt) {
-          double bf[4];
+            for (int s4 = 0; s4 < 4; ++s4)
+              af[mt][h][s4] = Ab[(mt * 16 + 8 * h) * C::SA + a_col[kq][s4]];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int r = kk + t + 4 * q;
-            bf[q] = Bs[r * C::SB + swz(r, wn * C::WTN + nt * 8 + g)];
-          }
+        for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-          for (int mt = 0; mt < C::MT; ++mt) dmma16816(acc[mt][nt], af[mt], bf);
-        }
+          for (int s4 = 0; s4 < 4; ++s4)
+            bf[nt][s4] = stg[(16 * kq + 4 * s4) * C::SB + b_col[nt]];
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+          for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int nt = 0; nt < C::NT; ++nt)
+                dmma884(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1], af[mt][h][s4], bf[nt][s4]);
       }
       if ((int)(step & (kchunks - 1)) == kchunks - 1) {
         // P_k complete: merge in the reference's tree order
@@ -262,19 +295,16 @@ __global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) 
     }
     cp_wait<0>();
     // epilogue: C block rows/cols of this sub-tile
-    const int64_t crow0 = int64_t(w.i) * b + w.si * TILE + wm * C::WTM;
-    const int64_t ccol0 = bcol + wn * C::WTN;
+    double *crow = Cm + (int64_t(w.i) * b + w.si * TILE + wm * C::WTM + g) * N +
+                   int64_t(w.j) * b + w.sj * TILE + wn * C::WTN + 2 * t;
 #pragma unroll
     for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int64_t row = crow0 + mt * 16 + g + 8 * h2;
-          const int64_t col = ccol0 + nt * 8 + 2 * t;
-          *reinterpret_cast<double2 *>(Cm + row * N + col) =
+        for (int h2 = 0; h2 < 2; ++h2)
+          *reinterpret_cast<double2 *>(crow + (int64_t)(mt * 16 + 8 * h2) * N + nt * 8) =
               make_double2(acc[mt][nt][2 * h2], acc[mt][nt][2 * h2 + 1]);
-        }
     __syncthreads();
   }
 }

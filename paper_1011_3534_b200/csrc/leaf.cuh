@@ -1,7 +1,7 @@
 // leaf.cuh -- K3 interfaces (see leaf.cu).
 #pragma once
 #include "common.cuh"
-#include "group.cuh"
+#include "traverse.cuh"
 
 namespace spamm {
 
@@ -15,7 +15,7 @@ struct LeafArgs {
   const uint32_t *ks;                 // inner indices, sorted within each group
   const uint32_t *group_ids;          // C block i*nb + j of each group
   const uint32_t *group_starts;       // first triple of each group
-  LeafCounters *lc;                   // num_groups + work ticket
+  TraverseCounters *tc;               // num_groups + work ticket
 };
 
 int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches);

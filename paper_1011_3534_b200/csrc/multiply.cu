@@ -14,9 +14,8 @@
 #include <memory>
 #include <vector>
 
-#include "cull.cuh"
-#include "group.cuh"
 #include "leaf.cuh"
+#include "traverse.cuh"
 
 struct spamm_product {
   std::vector<int64_t> boxes;    // 5 per box: i_lo, j_lo, k_lo, edge, tier
@@ -27,7 +26,8 @@ namespace spamm {
 
 int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out);
 void free_tree_async(spamm_tree *t, cudaStream_t st);
-int build_pyramid_async(spamm_tree *t, cudaStream_t st, int *launches);
+int build_pyramid_async(spamm_tree *t, cudaStream_t st, int *launches, const uint32_t *list,
+                        const unsigned *list_count, int64_t list_cap);
 int finish_tree(DeviceContext *ctx, spamm_tree *t);
 
 static int check_conformable(const spamm_tree *a, const spamm_tree *b) {
@@ -53,10 +53,6 @@ static int check_conformable(const spamm_tree *a, const spamm_tree *b) {
   return SPAMM_OK;
 }
 
-struct HostCounters {
-  CullCounters cull;
-  LeafCounters leaf;
-};
 
 #define SPAMM_CUDA_BREAK(expr)                                                          \
   {                                                                                     \
@@ -96,7 +92,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
 
   if (ctx->cull_capacity == 0) ctx->cull_capacity = std::max<size_t>(1 << 16, 2 * G);
   if (ctx->pruned_capacity == 0) ctx->pruned_capacity = std::max<size_t>(1 << 16, 2 * G);
-  HostCounters *hc = (HostCounters *)ctx->host_pinned;
+  TraverseCounters *hc = (TraverseCounters *)ctx->host_pinned;
   spamm_tree *c = nullptr;
   SPAMM_TRY(alloc_tree(ctx, a->n, a->leaf, a->dtype, &c));
   int rc = SPAMM_OK;
@@ -105,65 +101,66 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     launches = 0;
     const size_t cap = ctx->cull_capacity, pcap = ctx->pruned_capacity;
     const size_t gcap = std::min<size_t>(cap, (size_t)G);
+    const size_t st_tier = traverse_status_entries(cap), st_grp = group_status_entries(nb);
     if ((rc = ensure_scratch(ctx->cull_codes[0], cap * sizeof(uint64_t), st))) break;
     if ((rc = ensure_scratch(ctx->cull_codes[1], cap * sizeof(uint64_t), st))) break;
     if ((rc = ensure_scratch(ctx->pruned_vals, pcap * sizeof(double), st))) break;
     if ((rc = ensure_scratch(ctx->pruned_codes, pcap * sizeof(uint64_t), st))) break;
+    // look-back state must start (and is left by the kernel) all-zero
     if ((rc = ensure_scratch(ctx->tile_status,
-                             std::max(tile_status_bytes(cap), group_tile_status_bytes(nb)), st)))
+                             sizeof(unsigned long long) * (2 * st_tier + st_grp), st, true)))
       break;
-    if ((rc = ensure_scratch(ctx->counters, sizeof(CullCounters) + sizeof(LeafCounters), st)))
-      break;
+    if ((rc = ensure_scratch(ctx->counters, sizeof(TraverseCounters) + 64, st, true))) break;
     if ((rc = ensure_scratch(ctx->keys[0], 2 * sizeof(uint32_t) * G, st))) break;  // counts, offsets
     if ((rc = ensure_scratch(ctx->group_starts, 2 * sizeof(uint32_t) * gcap, st))) break;
     if ((rc = ensure_scratch(ctx->keys[1], sizeof(uint32_t) * cap, st))) break;  // ks
-    CullCounters *dcc = (CullCounters *)ctx->counters.ptr;
-    LeafCounters *dlc = (LeafCounters *)((char *)ctx->counters.ptr + sizeof(CullCounters));
+    TraverseCounters *dtc = (TraverseCounters *)ctx->counters.ptr;
 
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[0], st));
-    // ---------------------------------------------------------------- K2 cull
-    CullPlan plan{};
-    plan.depth = depth;
+    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->fork, st));
+    // ------------------------------------------- K2 traversal + grouping
+    TraverseArgs ta{};
+    ta.depth = depth;
+    ta.nb = nb;
     for (int t = 0; t <= depth; ++t)
-      plan.tau_tier[t] = (flags & SPAMM_TIER_TAU_DECAY) ? tau * ldexp(1.0, -3 * t) : tau;
-    plan.nsq_a = a->nsq;
-    plan.nsq_b = b->nsq;
-    plan.occ_a = a->occ;
-    plan.occ_b = b->occ;
-    plan.codes[0] = (uint64_t *)ctx->cull_codes[0].ptr;
-    plan.codes[1] = (uint64_t *)ctx->cull_codes[1].ptr;
-    plan.capacity = cap;
-    plan.pruned_vals = (double *)ctx->pruned_vals.ptr;
-    plan.pruned_codes = (uint64_t *)ctx->pruned_codes.ptr;
-    plan.pruned_capacity = pcap;
-    plan.tile_status = (unsigned long long *)ctx->tile_status.ptr;
-    plan.counters = dcc;
-    plan.row_lo = row_lo;
-    plan.row_hi = row_hi;
-    plan.max_ctas = ctx->num_sms * 4;
-    plan.launches = &launches;
-    if ((rc = launch_cull(plan, st))) break;
+      ta.tau_tier[t] = (flags & SPAMM_TIER_TAU_DECAY) ? tau * ldexp(1.0, -3 * t) : tau;
+    ta.nrm_a = a->nrm;
+    ta.nrm_b = b->nrm;
+    ta.occ_a = a->occ;
+    ta.occ_b = b->occ;
+    ta.codes[0] = (uint64_t *)ctx->cull_codes[0].ptr;
+    ta.codes[1] = (uint64_t *)ctx->cull_codes[1].ptr;
+    ta.capacity = cap;
+    ta.pruned_vals = (double *)ctx->pruned_vals.ptr;
+    ta.pruned_codes = (uint64_t *)ctx->pruned_codes.ptr;
+    ta.pruned_capacity = pcap;
+    unsigned long long *stb = (unsigned long long *)ctx->tile_status.ptr;
+    ta.status[0] = stb;
+    ta.status[1] = stb + st_tier;
+    ta.status[2] = stb + 2 * st_tier;
+    ta.tc = dtc;
+    ta.row_lo = row_lo;
+    ta.row_hi = row_hi;
+    ta.counts = (uint32_t *)ctx->keys[0].ptr;
+    ta.offsets = ta.counts + G;
+    ta.group_ids = (uint32_t *)ctx->group_starts.ptr;
+    ta.group_starts = ta.group_ids + gcap;
+    ta.ks = (uint32_t *)ctx->keys[1].ptr;
+    ta.barrier = (unsigned *)((char *)ctx->counters.ptr + sizeof(TraverseCounters));
+    if ((rc = launch_traverse(ta, ctx->num_sms, st))) break;
+    ++launches;
+    // C's zero fill runs on the side stream, under the traversal (issued
+    // after the cooperative launch so it cannot delay its residency)
+    SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
+    SPAMM_CUDA_BREAK(cudaMemsetAsync(c->padded, 0, (size_t)(c->N * c->N * c->elem_size()), ctx->side));
+    // C's leaf level: only blocks that receive products are recomputed below
+    SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nsq + level_offset(depth), 0, sizeof(double) * G, ctx->side));
+    SPAMM_CUDA_BREAK(cudaMemsetAsync(c->occ + level_offset(depth), 0, G, ctx->side));
+    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
 
-    // ------------------------------------------------- grouping by C block
-    SPAMM_CUDA_BREAK(cudaMemsetAsync(dlc, 0, sizeof(LeafCounters), st));
-    GroupArgs ga{};
-    ga.codes = plan.codes[depth & 1];
-    ga.n_codes = &dcc->n_active[depth];
-    ga.capacity = cap;
-    ga.depth = depth;
-    ga.nb = nb;
-    ga.counts = (uint32_t *)ctx->keys[0].ptr;
-    ga.offsets = ga.counts + G;
-    ga.group_ids = (uint32_t *)ctx->group_starts.ptr;
-    ga.group_starts = ga.group_ids + gcap;
-    ga.ks = (uint32_t *)ctx->keys[1].ptr;
-    ga.tile_status = plan.tile_status;
-    ga.lc = dlc;
-    if ((rc = launch_grouping(ga, (int64_t)cap, ctx->num_sms, st, &launches))) break;
-
     // ------------------------------------------------ K3 leaf products -> C
-    SPAMM_CUDA_BREAK(cudaMemsetAsync(c->padded, 0, (size_t)(c->N * c->N * c->elem_size()), st));
+    SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[2], st));
     LeafArgs la{};
     la.a = a->padded;
@@ -173,27 +170,27 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     la.nb = nb;
     la.leaf = a->leaf;
     la.depth = depth;
-    la.n_codes = ga.n_codes;
+    la.n_codes = &dtc->n_active[depth];
     la.capacity = cap;
-    la.ks = ga.ks;
-    la.group_ids = ga.group_ids;
-    la.group_starts = ga.group_starts;
-    la.lc = dlc;
+    la.ks = ta.ks;
+    la.group_ids = ta.group_ids;
+    la.group_starts = ta.group_starts;
+    la.tc = dtc;
     if ((rc = launch_leaf(la, a->dtype, ctx->num_sms, st, &launches))) break;
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[3], st));
 
     // ------------------------------------------- C's tree (multiply.py:220)
-    if ((rc = build_pyramid_async(c, st, &launches))) break;
+    if ((rc = build_pyramid_async(c, st, &launches, ta.group_ids, &dtc->num_groups, (int64_t)gcap)))
+      break;
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
-    SPAMM_CUDA_BREAK(cudaMemcpyAsync(&hc->cull, dcc, sizeof(CullCounters), cudaMemcpyDeviceToHost, st));
-    SPAMM_CUDA_BREAK(cudaMemcpyAsync(&hc->leaf, dlc, sizeof(LeafCounters), cudaMemcpyDeviceToHost, st));
+    SPAMM_CUDA_BREAK(cudaMemcpyAsync(hc, dtc, sizeof(TraverseCounters), cudaMemcpyDeviceToHost, st));
     SPAMM_CUDA_BREAK(cudaMemcpyAsync(&c->root_norm_sq, c->nsq, sizeof(double), cudaMemcpyDeviceToHost, st));
     SPAMM_CUDA_BREAK(cudaStreamSynchronize(st));
-    if (!hc->cull.overflow) break;
+    if (!hc->overflow) break;
     unsigned long long need = 0, pneed = 0;
     for (int t = 0; t <= depth; ++t) {
-      need = std::max(need, hc->cull.n_active[t]);
-      pneed += hc->cull.n_pruned[t];
+      need = std::max(need, hc->n_active[t]);
+      pneed += hc->n_pruned[t];
     }
     ctx->cull_capacity = std::max<size_t>(2 * cap, need + need / 8);
     ctx->pruned_capacity = std::max<size_t>(need > cap ? pcap : 2 * pcap, pneed + pneed / 8);
@@ -207,7 +204,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     free_tree_async(c, st);
     return rc;
   }
-  const CullCounters &cc = hc->cull;
+  const TraverseCounters &cc = *hc;
 
   // --------------------------------------------------------- stats (host)
   spamm_stats s{};
@@ -233,9 +230,11 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     s.omitted_budget = cc.budget;
   }
   s.n_triples = m;
-  s.n_groups = hc->leaf.num_groups;
+  s.n_groups = hc->num_groups;
   s.n_boxes = (flags & SPAMM_COLLECT_BOXES) ? total_pruned : 0;
   s.kernel_launches = launches;
+  for (int q = 1; q < 14; ++q)
+    s.traverse_phase_us[q] = cc.phase_ns[q] ? (float)((double)(cc.phase_ns[q] - cc.phase_ns[0]) * 1e-3) : 0.f;
   cudaEventElapsedTime(&s.ms_cull, ctx->ev[0], ctx->ev[1]);
   cudaEventElapsedTime(&s.ms_leaf, ctx->ev[1], ctx->ev[3]);
   cudaEventElapsedTime(&s.ms_gemm, ctx->ev[2], ctx->ev[3]);

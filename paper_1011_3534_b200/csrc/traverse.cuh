@@ -1,0 +1,57 @@
+// traverse.cuh -- K2 interfaces: product-space traversal + leaf grouping.
+#pragma once
+#include "common.cuh"
+
+namespace spamm {
+
+constexpr int MAX_TIERS = 32;
+
+// Device-resident counters of one multiply (zeroed by the kernel itself).
+struct TraverseCounters {
+  unsigned long long ticket[MAX_TIERS];      // tile tickets of the grid-wide tiers
+  unsigned long long n_cand[MAX_TIERS];      // candidates generated
+  unsigned long long n_alive[MAX_TIERS];     // occupancy survivors (intersecting the shard)
+  unsigned long long n_active[MAX_TIERS];    // survivors (next tier's parents)
+  unsigned long long n_pruned[MAX_TIERS];    // tau-pruned calls (owned by the shard)
+  unsigned long long n_skip[MAX_TIERS];      // Empty-operand skips (owned)
+  unsigned long long pruned_base[MAX_TIERS]; // offset of the tier's pruned list
+  double tier_budget[MAX_TIERS];             // numpy-pairwise sum of the tier's pruned products
+  double budget;                             // omitted_budget
+  int overflow;                              // a capacity was exceeded: re-run larger
+  int first_grid_tier;                       // tiers below ran in the single-CTA prefix
+  unsigned num_groups;                       // non-empty C blocks
+  unsigned budgets_done;                     // tiers whose pruned sum is final
+  unsigned long long scan_ticket, sort_ticket, gemm_ticket;
+  unsigned long long dirty_tiles[3];         // status entries to clear before the next call
+  unsigned long long phase_ns[16];           // %globaltimer at phase boundaries (CTA 0)
+};
+
+struct TraverseArgs {
+  int depth;
+  int64_t nb;
+  double tau_tier[MAX_TIERS];
+  const double *nrm_a, *nrm_b;      // rn(sqrt(norm_sq)) pyramids (concatenated levels)
+  const uint8_t *occ_a, *occ_b;
+  uint64_t *codes[2];               // ping-pong survivor lists (Morton codes)
+  unsigned long long capacity;      // items per survivor list
+  double *pruned_vals;              // all tiers, reference order
+  uint64_t *pruned_codes;
+  unsigned long long pruned_capacity;
+  unsigned long long *status[3];    // look-back state: two tier arrays + the group scan
+  TraverseCounters *tc;
+  int64_t row_lo, row_hi;           // C leaf block rows of this shard
+  // grouping outputs
+  uint32_t *counts;                 // nb^2 bucket sizes
+  uint32_t *offsets;                // nb^2 bucket offsets
+  uint32_t *group_ids;              // non-empty buckets, ascending i*nb + j
+  uint32_t *group_starts;           // their offsets into ks
+  uint32_t *ks;                     // inner indices, bucket-major, ascending per bucket
+  unsigned *barrier;                // [0] arrival count, [1] generation
+};
+
+// Launch the cooperative traversal kernel (one launch per multiply).
+int launch_traverse(const TraverseArgs &args, int num_sms, cudaStream_t st);
+size_t traverse_status_entries(size_t capacity);
+size_t group_status_entries(int64_t nb);
+
+}  // namespace spamm

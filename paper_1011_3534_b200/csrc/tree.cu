@@ -6,6 +6,7 @@
 // (_leaf_norm_sq), :90-92 (_aggregate_norm_sq), :218-251 (from_dense).
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -45,6 +46,9 @@ int get_context(int device, DeviceContext **out) {
     SPAMM_CUDA_TRY(cudaSetDevice(device));
     SPAMM_CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
     SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
+    SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming));
     for (auto &e : ctx->ev) SPAMM_CUDA_TRY(cudaEventCreate(&e));
     SPAMM_CUDA_TRY(cudaMallocHost(&ctx->host_pinned, 1 << 16));
     // keep freed pool memory cached between calls (stream-ordered allocator)
@@ -60,7 +64,7 @@ int get_context(int device, DeviceContext **out) {
   return SPAMM_OK;
 }
 
-int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream) {
+int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed) {
   if (s.bytes >= bytes) return SPAMM_OK;
   if (s.ptr) SPAMM_CUDA_TRY(cudaFreeAsync(s.ptr, stream));
   s.ptr = nullptr;
@@ -68,6 +72,7 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream) {
   size_t want = bytes + bytes / 4 + 256;
   SPAMM_CUDA_TRY(cudaMallocAsync(&s.ptr, want, stream));
   s.bytes = want;
+  if (zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(s.ptr, 0, want, stream));
   return SPAMM_OK;
 }
 
@@ -79,20 +84,20 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream) {
 // rounding).  The parallelism is across leaves only -- a per-leaf shuffle
 // tree would change the bits the strict `< tau` tests compare.
 //
-// Data movement: a CTA owns K1_LT = 32 consecutive leaves (row-major leaf
-// order); its first warp runs the 32 sequential chains, all four warps feed
-// a K1_STAGES-deep cp.async pipeline.  Each stage holds one 512-byte piece
-// of every leaf (a full leaf row for b = 64 doubles; several rows for
-// smaller leaves), stored with 16 B of padding per leaf so the per-lane
-// LDS.128 reads are bank-conflict free while every global read consumes
-// whole 128-byte lines.  Small CTAs spread even a 64 x 64-leaf tree over
-// the whole chip; the deep pipeline keeps ~100 KB in flight per SM, which
-// is what HBM3e needs to stream at full rate.
+// Data movement (warp-specialised): a CTA owns K1_LT = 32 leaves; warp 0
+// runs their 32 sequential chains and does nothing else, warps 1-2 stream the
+// leaves through a K1_STAGES-deep ring of 512-byte-per-leaf stages with
+// cp.async, signalling "full" on a per-stage mbarrier as their copies land;
+// warp 0 releases a stage with an "empty" mbarrier arrive.  No block-wide
+// barrier sits on the chain, and the chain's instruction stream is just
+// LDS.128 / DMUL / DADD / LOP3 (zero tests are folded into one OR of the raw
+// bits).  Stages carry 16 B of padding per leaf, so the per-lane LDS.128
+// reads are bank-conflict free while every global read uses whole lines.
 constexpr int K1_LT = 32;
-constexpr int K1_THREADS = 128;
-constexpr int K1_STAGES = 6;
+constexpr int K1_THREADS = 64;                 // warp 0 computes, warp 1 issues TMA copies
 constexpr int K1_CHUNK = 512;                  // bytes per leaf per stage
 constexpr int K1_LEAF_STRIDE = K1_CHUNK + 16;  // smem bytes per leaf per stage
+constexpr int K1_STAGE_BYTES = K1_LT * K1_LEAF_STRIDE;
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -102,6 +107,35 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared.b64 st, [%0];\n}\n" ::"r"(
+      (unsigned)__cvta_generic_to_shared(bar)));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared.b64 st, [%0], %1;\n}\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes));
+}
+// TMA bulk copy global -> shared, completion counted in bytes on `bar`
+__device__ __forceinline__ void tma_bulk_g2s(void *smem, const void *gmem, unsigned bytes,
+                                             uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(smem)),
+      "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+      "r"(parity));
 }
 
 template <typename T>
@@ -117,13 +151,12 @@ struct Bits<float> {
   __device__ static U of(float x) { return (U)__float_as_uint(x); }
 };
 
+// acc = rn(acc + rn(x*x)) in f64, the reference's per-element step; `bits`
+// ORs the raw patterns: (bits << 1) != 0 <=> some element is nonzero (NaN
+// included), bits != 0 with zero magnitude <=> a -0.0 was seen.
 template <typename T>
-__device__ __forceinline__ void accum(double &acc, int &nz, int &negz, T x) {
-  const auto u = Bits<T>::of(x);
-  using U = typename Bits<T>::U;
-  const U mag = u << 1;  // drop the sign: zero iff x == +-0.0 (NaN counts as nonzero)
-  nz |= (mag != 0);
-  negz |= (u != 0);      // any set bit (a -0.0 when mag == 0)
+__device__ __forceinline__ void accum(double &acc, typename Bits<T>::U &bits, T x) {
+  bits |= Bits<T>::of(x);
   const double e = (double)x;
   acc = __dadd_rn(acc, __dmul_rn(e, e));
 }
@@ -137,90 +170,111 @@ __device__ void canonicalise_leaf(T *padded, int64_t N, int32_t b, int64_t bi, i
 }
 
 // Staged kernel: requires b * sizeof(T) >= 16.
-template <typename T>
+template <typename T, int K1_STAGES>
 __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restrict__ padded,
                                                                       int64_t N, int32_t b,
                                                                       int64_t nb,
                                                                       double *__restrict__ nsq_leaf,
-                                                                      uint8_t *__restrict__ occ_leaf) {
+                                                                      uint8_t *__restrict__ occ_leaf,
+                                                                      const uint32_t *__restrict__ list,
+                                                                      const unsigned *list_count) {
+  using U = typename Bits<T>::U;
   extern __shared__ __align__(16) unsigned char k1_smem[];
-  const int64_t n_leaves = nb * nb;
+  __shared__ __align__(8) uint64_t full_bar[K1_STAGES], empty_bar[K1_STAGES];
+  // dense mode: every leaf; list mode: only the listed leaves (C blocks that
+  // received products -- every other leaf of C is exactly zero)
+  const int64_t n_leaves = list ? (int64_t)*list_count : nb * nb;
   const int64_t leaf0 = (int64_t)blockIdx.x * K1_LT;
+  if (leaf0 >= n_leaves) return;
   const int tid = threadIdx.x;
   const int64_t bb = (int64_t)b * b;
   const int EPC = (int)(bb < K1_CHUNK / (int)sizeof(T) ? bb : K1_CHUNK / (int)sizeof(T));
   const int CW = b < EPC ? b : EPC;      // chunk width (elements)
   const int R = EPC / CW;                // rows per chunk
-  const int chunks_per_row = b / CW;
+  const int chunks_per_row = b / CW;     // a power of two
   const int n_chunks = (b / R) * chunks_per_row;
   const int segs = EPC * (int)sizeof(T) / 16;  // 16-byte segments per leaf chunk
-  const int EPS = 16 / (int)sizeof(T);         // elements per segment
+  constexpr int EPS = 16 / (int)sizeof(T);     // elements per segment
 
-  // Each thread copies the same (leaf, 16-byte segment) slots in every chunk;
-  // resolve their global addresses once (no 64-bit divisions in the loop).
-  constexpr int MAX_SLOTS = K1_LT * (K1_CHUNK / 16) / K1_THREADS;
-  const T *slot_ptr[MAX_SLOTS];
-  unsigned slot_dst[MAX_SLOTS];
-  int n_slots = 0;
-#pragma unroll
-  for (int q = 0; q < MAX_SLOTS; ++q) {
-    const int s = tid + q * K1_THREADS;
-    slot_ptr[q] = nullptr;
-    slot_dst[q] = 0;
-    if (s < K1_LT * segs) {
-      const int l = s / segs, part = s - l * segs;
-      const int64_t leaf = leaf0 + l;
-      if (leaf < n_leaves) {
-        const int64_t bi = leaf / nb, bj = leaf - bi * nb;
-        const int e = part * EPS;
-        const int rr = e / CW, cc = e - rr * CW;
-        slot_ptr[q] = padded + (bi * b + rr) * N + bj * b + cc;
-        slot_dst[q] = l * K1_LEAF_STRIDE + part * 16;
-        n_slots = q + 1;
+  if (tid == 0) {
+    for (int s = 0; s < K1_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  __syncthreads();
+
+  if (tid >= 32) {
+    // ------------------------------------------- producer warp (TMA bulk)
+    // lane l streams leaf l: per stage R row pieces of CW elements
+    const int l = tid - 32;
+    const int64_t lx = leaf0 + l;
+    const T *src = nullptr;
+    if (lx < n_leaves) {
+      const int64_t leaf = list ? (int64_t)list[lx] : lx;
+      const int64_t bi = leaf / nb, bj = leaf - bi * nb;
+      src = padded + (bi * b) * N + bj * b;
+    }
+    const int64_t live = n_leaves - leaf0 < K1_LT ? n_leaves - leaf0 : K1_LT;
+    const unsigned stage_bytes = (unsigned)(live * EPC * sizeof(T));
+    const unsigned piece = (unsigned)(CW * sizeof(T));
+    const int shift_cpr = __ffs(chunks_per_row) - 1;
+    for (int chunk = 0; chunk < n_chunks; ++chunk) {
+      const int stage = chunk % K1_STAGES;
+      if (chunk >= K1_STAGES) mbar_wait(&empty_bar[stage], ((chunk / K1_STAGES) - 1) & 1);
+      if (l == 0) mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
+      __syncwarp();
+      if (src) {
+        const int r0 = (chunk >> shift_cpr) * R, c0 = (chunk & (chunks_per_row - 1)) * CW;
+        unsigned char *dst = k1_smem + stage * K1_STAGE_BYTES + l * K1_LEAF_STRIDE;
+        for (int rr = 0; rr < R; ++rr)
+          tma_bulk_g2s(dst + rr * piece, src + (int64_t)(r0 + rr) * N + c0, piece, &full_bar[stage]);
       }
     }
+    return;
   }
-  const int shift_cpr = __ffs(chunks_per_row) - 1;  // chunks_per_row is a power of two
-  auto issue = [&](int chunk, int stage) {
-    const int64_t off = (int64_t)((chunk >> shift_cpr) * R) * N + (chunk & (chunks_per_row - 1)) * CW;
-    unsigned char *base = k1_smem + stage * (K1_LT * K1_LEAF_STRIDE);
-#pragma unroll
-    for (int q = 0; q < MAX_SLOTS; ++q)
-      if (q < n_slots && slot_ptr[q]) cp_async16(base + slot_dst[q], slot_ptr[q] + off);
-  };
 
-  const int64_t my_leaf = leaf0 + tid;
+  // --------------------------------------------------------------- warp 0
+  const int64_t my_x = leaf0 + tid;
+  const bool mine = my_x < n_leaves;
   double acc = 0.0;
-  int nz = 0, negz = 0;
-#pragma unroll
-  for (int s = 0; s < K1_STAGES - 1; ++s) {
-    if (s < n_chunks) issue(s, s);
-    cp_async_commit();
-  }
+  U bits = 0;
   for (int chunk = 0; chunk < n_chunks; ++chunk) {
-    cp_async_wait<K1_STAGES - 2>();
-    __syncthreads();
-    const int nxt = chunk + K1_STAGES - 1;
-    if (nxt < n_chunks) issue(nxt, nxt % K1_STAGES);
-    cp_async_commit();
-    if (tid < K1_LT && my_leaf < n_leaves) {
-      const unsigned char *p = k1_smem + (chunk % K1_STAGES) * (K1_LT * K1_LEAF_STRIDE) +
-                               tid * K1_LEAF_STRIDE;
-      for (int v = 0; v < segs; ++v) {
-        const uint4 w = *reinterpret_cast<const uint4 *>(p + 16 * v);
+    const int stage = chunk % K1_STAGES;
+    mbar_wait(&full_bar[stage], (chunk / K1_STAGES) & 1);
+    if (mine) {
+      const unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + tid * K1_LEAF_STRIDE;
+      int v = 0;
+      for (; v + 8 <= segs; v += 8) {
+        uint4 w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = *reinterpret_cast<const uint4 *>(pp + 16 * (v + u));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const T *x = reinterpret_cast<const T *>(&w[u]);
+#pragma unroll
+          for (int e = 0; e < EPS; ++e) accum<T>(acc, bits, x[e]);
+        }
+      }
+      for (; v < segs; ++v) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(pp + 16 * v);
         const T *x = reinterpret_cast<const T *>(&w);
 #pragma unroll
-        for (int e = 0; e < (int)(16 / sizeof(T)); ++e) accum<T>(acc, nz, negz, x[e]);
+        for (int e = 0; e < EPS; ++e) accum<T>(acc, bits, x[e]);
       }
     }
+    __syncwarp();
+    if (tid == 0) mbar_arrive(&empty_bar[stage]);
   }
-  cp_async_wait<0>();
-  if (tid < K1_LT && my_leaf < n_leaves) {
-    nsq_leaf[my_leaf] = acc;
-    occ_leaf[my_leaf] = (uint8_t)(nz != 0);
-    if (!nz && negz) {
-      const int64_t bi = my_leaf / nb;
-      canonicalise_leaf<T>(padded, N, b, bi, my_leaf - bi * nb);
+  if (mine) {
+    const int64_t leaf = list ? (int64_t)list[my_x] : my_x;
+    const bool nz = (U)(bits << 1) != 0;
+    nsq_leaf[leaf] = acc;
+    occ_leaf[leaf] = (uint8_t)nz;
+    if (!nz && bits) {
+      const int64_t bi = leaf / nb;
+      canonicalise_leaf<T>(padded, N, b, bi, leaf - bi * nb);
     }
   }
 }
@@ -230,19 +284,23 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
 template <typename T>
 __global__ void leaf_norm_direct_kernel(T *__restrict__ padded, int64_t N, int32_t b, int64_t nb,
                                         double *__restrict__ nsq_leaf,
-                                        uint8_t *__restrict__ occ_leaf) {
-  const int64_t leaf = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (leaf >= nb * nb) return;
+                                        uint8_t *__restrict__ occ_leaf,
+                                        const uint32_t *__restrict__ list,
+                                        const unsigned *list_count) {
+  const int64_t lx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (lx >= (list ? (int64_t)*list_count : nb * nb)) return;
+  const int64_t leaf = list ? (int64_t)list[lx] : lx;
   const int64_t bi = leaf / nb, bj = leaf - bi * nb;
   double acc = 0.0;
-  int nz = 0, negz = 0;
+  typename Bits<T>::U bits = 0;
   for (int r = 0; r < b; ++r) {
     const T *row = padded + (bi * b + r) * N + bj * b;
-    for (int c = 0; c < b; ++c) accum<T>(acc, nz, negz, row[c]);
+    for (int c = 0; c < b; ++c) accum<T>(acc, bits, row[c]);
   }
+  const bool nz = (typename Bits<T>::U)(bits << 1) != 0;
   nsq_leaf[leaf] = acc;
-  occ_leaf[leaf] = (uint8_t)(nz != 0);
-  if (!nz && negz) canonicalise_leaf<T>(padded, N, b, bi, bj);
+  occ_leaf[leaf] = (uint8_t)nz;
+  if (!nz && bits) canonicalise_leaf<T>(padded, N, b, bi, bj);
 }
 
 // Pyramid: each CTA reduces a 2^L x 2^L tile of level `from` through L levels,
@@ -295,22 +353,45 @@ __global__ void __launch_bounds__(PYR_THREADS) pyramid_kernel(double *__restrict
   }
 }
 
+// rn(sqrt(norm_sq)) of every node: the factors of the reference's norm
+// product (multiply.py:185), correctly rounded exactly like np.sqrt.
+__global__ void norm_sqrt_kernel(const double *__restrict__ nsq, double *__restrict__ nrm, int64_t P) {
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < P;
+       x += (int64_t)gridDim.x * blockDim.x)
+    nrm[x] = __dsqrt_rn(nsq[x]);
+}
+
 template <typename T>
-static int launch_leaf_norms(spamm_tree *t, cudaStream_t st) {
-  const int64_t n_leaves = t->nb * t->nb;
+static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *list,
+                             const unsigned *list_count, int64_t list_cap) {
+  const int64_t n_leaves = list ? std::min<int64_t>(list_cap, t->nb * t->nb) : t->nb * t->nb;
   double *nsq_leaf = t->nsq + level_offset(t->depth);
   uint8_t *occ_leaf = t->occ + level_offset(t->depth);
   if (t->leaf * sizeof(T) >= 16) {
-    const size_t smem = (size_t)K1_STAGES * K1_LT * K1_LEAF_STRIDE;
-    SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_norm_staged_kernel<T>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // few CTAs: one per SM with a deep ring (DRAM latency needs ~10 stages
+    // in flight per chain); many CTAs: two per SM with a shallower ring
     const int64_t grid = (n_leaves + K1_LT - 1) / K1_LT;
-    leaf_norm_staged_kernel<T><<<(unsigned)grid, K1_THREADS, smem, st>>>(
-        (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
+    if (grid <= sms) {
+      constexpr int S = 12;
+      const size_t smem = (size_t)S * K1_STAGE_BYTES;
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_norm_staged_kernel<T, S>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      leaf_norm_staged_kernel<T, S><<<(unsigned)grid, K1_THREADS, smem, st>>>(
+          (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count);
+    } else {
+      constexpr int S = 6;
+      const size_t smem = (size_t)S * K1_STAGE_BYTES;
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_norm_staged_kernel<T, S>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      leaf_norm_staged_kernel<T, S><<<(unsigned)grid, K1_THREADS, smem, st>>>(
+          (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count);
+    }
   } else {
     const int64_t grid = (n_leaves + 127) / 128;
-    leaf_norm_direct_kernel<T><<<(unsigned)grid, 128, 0, st>>>((T *)t->padded, t->N, t->leaf,
-                                                                t->nb, nsq_leaf, occ_leaf);
+    leaf_norm_direct_kernel<T><<<(unsigned)grid, 128, 0, st>>>(
+        (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count);
   }
   SPAMM_CUDA_TRY(cudaGetLastError());
   return SPAMM_OK;
@@ -318,9 +399,10 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st) {
 
 // Rebuild the whole pyramid of `t` from its padded storage (canonicalising
 // all-zero leaves in place).  Stream-ordered; no host sync.
-int build_pyramid_async(spamm_tree *t, cudaStream_t st, int *launches) {
-  if (t->dtype == SPAMM_DTYPE_F64) SPAMM_TRY(launch_leaf_norms<double>(t, st));
-  else SPAMM_TRY(launch_leaf_norms<float>(t, st));
+int build_pyramid_async(spamm_tree *t, cudaStream_t st, int *launches, const uint32_t *list,
+                        const unsigned *list_count, int64_t list_cap) {
+  if (t->dtype == SPAMM_DTYPE_F64) SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap));
+  else SPAMM_TRY(launch_leaf_norms<float>(t, st, list, list_count, list_cap));
   if (launches) ++*launches;
   int from = t->depth;
   while (from > 0) {
@@ -331,6 +413,10 @@ int build_pyramid_async(spamm_tree *t, cudaStream_t st, int *launches) {
     if (launches) ++*launches;
     from -= L;
   }
+  const int64_t P = pyramid_size(t->depth);
+  norm_sqrt_kernel<<<(unsigned)std::min<int64_t>((P + 255) / 256, 4096), 256, 0, st>>>(t->nsq, t->nrm, P);
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  if (launches) ++*launches;
   return SPAMM_OK;
 }
 
@@ -348,6 +434,8 @@ int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm
   SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->nsq, sizeof(double) * pyramid_size(t->depth),
                                  ctx->stream));
   SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->occ, pyramid_size(t->depth), ctx->stream));
+  SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->nrm, sizeof(double) * pyramid_size(t->depth),
+                                 ctx->stream));
   *out = t.release();
   return SPAMM_OK;
 }
@@ -357,6 +445,7 @@ void free_tree_async(spamm_tree *t, cudaStream_t st) {
   if (t->padded) cudaFreeAsync(t->padded, st);
   if (t->nsq) cudaFreeAsync(t->nsq, st);
   if (t->occ) cudaFreeAsync(t->occ, st);
+  if (t->nrm) cudaFreeAsync(t->nrm, st);
   delete t;
 }
 
@@ -408,7 +497,7 @@ static int tree_from(const void *src, bool src_on_host, int64_t n, int64_t ld, i
                           src_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                           ctx->stream);
     if (e != cudaSuccess) { set_error("copy: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-    rc = build_pyramid_async(t, ctx->stream, nullptr);
+    rc = build_pyramid_async(t, ctx->stream, nullptr, nullptr, nullptr, 0);
     if (rc) break;
     rc = finish_tree(ctx, t);
   } while (0);

@@ -91,6 +91,7 @@ class MultiplyDetail:
     ms_total: float = 0.0
     ms_gemm: float = 0.0
     kernel_launches: int = 0
+    traverse_phase_us: list = field(default_factory=list)
 
 
 def _flags(config, keep_triples):
@@ -139,7 +140,8 @@ def spamm_detailed(a, b, config=None, keep_triples=False, rows=None):
                                 tier_pruned=list(st.tier_pruned[:depth + 1]),
                                 n_groups=int(st.n_groups), ms_cull=st.ms_cull,
                                 ms_leaf=st.ms_leaf, ms_ctree=st.ms_ctree, ms_total=st.ms_total,
-                                ms_gemm=st.ms_gemm, kernel_launches=int(st.kernel_launches))
+                                ms_gemm=st.ms_gemm, kernel_launches=int(st.kernel_launches),
+                                traverse_phase_us=list(st.traverse_phase_us))
         if config.collect_boxes and st.n_boxes:
             raw = np.empty((int(st.n_boxes), 5), np.int64)
             _lib.check(L.spamm_product_boxes(prod, raw.ctypes.data, int(st.n_boxes)))
