@@ -62,6 +62,12 @@ struct WorkItem {
   int si, sj;          // sub-tile
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ bool fetch_work(const LeafArgs &args, int subs_side, int *s_work,
                                            WorkItem &w) {
   if (threadIdx.x == 0) *s_work = (int)atomicAdd(&args.tc->gemm_ticket, 1ull);
@@ -172,7 +178,10 @@ __global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) 
   double top[C::MT][C::NT][4];
 
   WorkItem w;
+  const unsigned long long t_start = gtimer();
+  unsigned items = 0;
   while (fetch_work(args, subs_side, &s_work, w)) {
+    ++items;
     const int64_t nk = w.end - w.start;
     const int64_t nsteps = nk * kchunks;
     const bool ks_in_smem = nk <= KS_SMEM;
@@ -306,6 +315,11 @@ __global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) 
           *reinterpret_cast<double2 *>(crow + (int64_t)(mt * 16 + 8 * h2) * N + nt * 8) =
               make_double2(acc[mt][nt][2 * h2], acc[mt][nt][2 * h2 + 1]);
     __syncthreads();
+  }
+  if (args.timeline && threadIdx.x == 0) {
+    args.timeline[3 * blockIdx.x] = t_start;
+    args.timeline[3 * blockIdx.x + 1] = gtimer();
+    args.timeline[3 * blockIdx.x + 2] = items;
   }
 }
 

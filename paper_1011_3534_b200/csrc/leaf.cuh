@@ -16,6 +16,7 @@ struct LeafArgs {
   const uint32_t *group_ids;          // C block i*nb + j of each group
   const uint32_t *group_starts;       // first triple of each group
   TraverseCounters *tc;               // num_groups + work ticket
+  unsigned long long *timeline;       // optional: per-CTA [start, end, items] (%globaltimer)
 };
 
 int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches);

@@ -11,6 +11,7 @@
 // with larger buffers; capacities persist per device, so this happens at
 // most a few times per process.
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -176,6 +177,12 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     la.group_ids = ta.group_ids;
     la.group_starts = ta.group_starts;
     la.tc = dtc;
+    static const bool want_timeline = getenv("SPAMM_GEMM_TIMELINE") != nullptr;
+    if (want_timeline) {
+      if ((rc = ensure_scratch(ctx->reduce_tmp, sizeof(unsigned long long) * 3 * 4096, st))) break;
+      SPAMM_CUDA_BREAK(cudaMemsetAsync(ctx->reduce_tmp.ptr, 0, sizeof(unsigned long long) * 3 * 4096, st));
+      la.timeline = (unsigned long long *)ctx->reduce_tmp.ptr;
+    }
     if ((rc = launch_leaf(la, a->dtype, ctx->num_sms, st, &launches))) break;
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[3], st));
 
@@ -203,6 +210,28 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   if (rc) {
     free_tree_async(c, st);
     return rc;
+  }
+  if (getenv("SPAMM_GEMM_TIMELINE")) {
+    std::vector<unsigned long long> tl(3 * 4096);
+    cudaMemcpy(tl.data(), ctx->reduce_tmp.ptr, sizeof(unsigned long long) * 3 * 4096,
+               cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    std::vector<double> ends;
+    double busy = 0;
+    int n = 0, items = 0;
+    for (int q = 0; q < 4096; ++q)
+      if (tl[3 * q]) { t0 = std::min(t0, tl[3 * q]); t1 = std::max(t1, tl[3 * q + 1]); }
+    for (int q = 0; q < 4096; ++q)
+      if (tl[3 * q]) {
+        ends.push_back((tl[3 * q + 1] - t0) * 1e-3);
+        busy += (tl[3 * q + 1] - tl[3 * q]) * 1e-3;
+        items += (int)tl[3 * q + 2];
+        ++n;
+      }
+    std::sort(ends.begin(), ends.end());
+    if (n)
+      fprintf(stderr, "[gemm timeline] ctas=%d items=%d span=%.1fus end min/med/p90/max=%.1f/%.1f/%.1f/%.1f busy_avg=%.1fus\n",
+              n, items, (t1 - t0) * 1e-3, ends[0], ends[n / 2], ends[n * 9 / 10], ends[n - 1], busy / n);
   }
   const TraverseCounters &cc = *hc;
 

@@ -84,17 +84,23 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed) {
 // rounding).  The parallelism is across leaves only -- a per-leaf shuffle
 // tree would change the bits the strict `< tau` tests compare.
 //
-// Data movement (warp-specialised): a CTA owns K1_LT = 32 leaves; warp 0
-// runs their 32 sequential chains and does nothing else, warps 1-2 stream the
-// leaves through a K1_STAGES-deep ring of 512-byte-per-leaf stages with
-// cp.async, signalling "full" on a per-stage mbarrier as their copies land;
-// warp 0 releases a stage with an "empty" mbarrier arrive.  No block-wide
-// barrier sits on the chain, and the chain's instruction stream is just
-// LDS.128 / DMUL / DADD / LOP3 (zero tests are folded into one OR of the raw
-// bits).  Stages carry 16 B of padding per leaf, so the per-lane LDS.128
-// reads are bank-conflict free while every global read uses whole lines.
+// Data movement (warp-specialised): a CTA owns K1_LT = 32 leaves.
+//   warps 2-3  stream the leaves through a K1_STAGES-deep ring of
+//              512-byte-per-leaf stages with cp.async; their copies arrive on
+//              the stage's "full" mbarrier as they land;
+//   warp 1     (f64) squares every element in place, rn(x*x), and ORs the
+//              raw bit patterns for the occupancy / -0.0 tests, then arrives
+//              on "squared";
+//   warp 0     runs the 32 sequential chains acc = rn(acc + sq) -- nothing
+//              else sits on the dependent-add critical path -- and releases
+//              the stage on "empty".
+// For f32 storage warp 0 also forms the squares (the f64 squares would not
+// fit in place).  Stages carry 16 B of padding per leaf, so the per-lane
+// LDS.128 reads are bank-conflict free while every global read uses whole
+// 128-byte lines.
 constexpr int K1_LT = 32;
-constexpr int K1_THREADS = 64;                 // warp 0 computes, warp 1 issues TMA copies
+constexpr int K1_PRODUCERS = 64;
+constexpr int K1_THREADS = 64 + K1_PRODUCERS;
 constexpr int K1_CHUNK = 512;                  // bytes per leaf per stage
 constexpr int K1_LEAF_STRIDE = K1_CHUNK + 16;  // smem bytes per leaf per stage
 constexpr int K1_STAGE_BYTES = K1_LT * K1_LEAF_STRIDE;
@@ -116,19 +122,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared.b64 st, [%0];\n}\n" ::"r"(
       (unsigned)__cvta_generic_to_shared(bar)));
 }
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared.b64 st, [%0], %1;\n}\n" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(bar)),
-               "r"(bytes));
-}
-// TMA bulk copy global -> shared, completion counted in bytes on `bar`
-__device__ __forceinline__ void tma_bulk_g2s(void *smem, const void *gmem, unsigned bytes,
-                                             uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          (unsigned)__cvta_generic_to_shared(smem)),
-      "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
-      : "memory");
+// the calling thread's prior cp.async copies arrive on `bar` when they land
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(
+      (unsigned)__cvta_generic_to_shared(bar)));
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
   asm volatile(
@@ -179,14 +176,16 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
                                                                       const uint32_t *__restrict__ list,
                                                                       const unsigned *list_count) {
   using U = typename Bits<T>::U;
+  constexpr bool SQUARER = sizeof(T) == 8;  // warp 1 squares in place (f64 only)
   extern __shared__ __align__(16) unsigned char k1_smem[];
-  __shared__ __align__(8) uint64_t full_bar[K1_STAGES], empty_bar[K1_STAGES];
+  __shared__ __align__(8) uint64_t full_bar[K1_STAGES], sq_bar[K1_STAGES], empty_bar[K1_STAGES];
+  __shared__ U s_bits[K1_LT];
   // dense mode: every leaf; list mode: only the listed leaves (C blocks that
   // received products -- every other leaf of C is exactly zero)
   const int64_t n_leaves = list ? (int64_t)*list_count : nb * nb;
   const int64_t leaf0 = (int64_t)blockIdx.x * K1_LT;
   if (leaf0 >= n_leaves) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t bb = (int64_t)b * b;
   const int EPC = (int)(bb < K1_CHUNK / (int)sizeof(T) ? bb : K1_CHUNK / (int)sizeof(T));
   const int CW = b < EPC ? b : EPC;      // chunk width (elements)
@@ -195,56 +194,106 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
   const int n_chunks = (b / R) * chunks_per_row;
   const int segs = EPC * (int)sizeof(T) / 16;  // 16-byte segments per leaf chunk
   constexpr int EPS = 16 / (int)sizeof(T);     // elements per segment
+  const bool mine = leaf0 + lane < n_leaves;
 
   if (tid == 0) {
     for (int s = 0; s < K1_STAGES; ++s) {
-      mbar_init(&full_bar[s], 1);
+      mbar_init(&full_bar[s], K1_PRODUCERS);
+      mbar_init(&sq_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
   __syncthreads();
 
-  if (tid >= 32) {
-    // ------------------------------------------- producer warp (TMA bulk)
-    // lane l streams leaf l: per stage R row pieces of CW elements
-    const int l = tid - 32;
-    const int64_t lx = leaf0 + l;
-    const T *src = nullptr;
-    if (lx < n_leaves) {
-      const int64_t leaf = list ? (int64_t)list[lx] : lx;
-      const int64_t bi = leaf / nb, bj = leaf - bi * nb;
-      src = padded + (bi * b) * N + bj * b;
+  if (warp >= 2) {
+    // ------------------------------------------------------------ producers
+    const int p = tid - 64;
+    constexpr int MAX_SLOTS = K1_LT * (K1_CHUNK / 16) / K1_PRODUCERS;
+    const T *slot_ptr[MAX_SLOTS];
+    unsigned slot_dst[MAX_SLOTS];
+#pragma unroll
+    for (int q = 0; q < MAX_SLOTS; ++q) {
+      const int sidx = p + q * K1_PRODUCERS;
+      slot_ptr[q] = nullptr;
+      slot_dst[q] = 0;
+      if (sidx < K1_LT * segs) {
+        const int l = sidx / segs, part = sidx - l * segs;
+        const int64_t lx = leaf0 + l;
+        if (lx < n_leaves) {
+          const int64_t leaf = list ? (int64_t)list[lx] : lx;
+          const int64_t bi = leaf / nb, bj = leaf - bi * nb;
+          const int e = part * EPS;
+          const int rr = e / CW, cc = e - rr * CW;
+          slot_ptr[q] = padded + (bi * b + rr) * N + bj * b + cc;
+          slot_dst[q] = l * K1_LEAF_STRIDE + part * 16;
+        }
+      }
     }
-    const int64_t live = n_leaves - leaf0 < K1_LT ? n_leaves - leaf0 : K1_LT;
-    const unsigned stage_bytes = (unsigned)(live * EPC * sizeof(T));
-    const unsigned piece = (unsigned)(CW * sizeof(T));
     const int shift_cpr = __ffs(chunks_per_row) - 1;
     for (int chunk = 0; chunk < n_chunks; ++chunk) {
       const int stage = chunk % K1_STAGES;
       if (chunk >= K1_STAGES) mbar_wait(&empty_bar[stage], ((chunk / K1_STAGES) - 1) & 1);
-      if (l == 0) mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
-      __syncwarp();
-      if (src) {
-        const int r0 = (chunk >> shift_cpr) * R, c0 = (chunk & (chunks_per_row - 1)) * CW;
-        unsigned char *dst = k1_smem + stage * K1_STAGE_BYTES + l * K1_LEAF_STRIDE;
-        for (int rr = 0; rr < R; ++rr)
-          tma_bulk_g2s(dst + rr * piece, src + (int64_t)(r0 + rr) * N + c0, piece, &full_bar[stage]);
+      const int64_t off =
+          (int64_t)((chunk >> shift_cpr) * R) * N + (chunk & (chunks_per_row - 1)) * CW;
+      unsigned char *base = k1_smem + stage * K1_STAGE_BYTES;
+#pragma unroll
+      for (int q = 0; q < MAX_SLOTS; ++q)
+        if (slot_ptr[q]) cp_async16(base + slot_dst[q], slot_ptr[q] + off);
+      cp_async_mbar_arrive(&full_bar[stage]);
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  if (warp == 1) {
+    // ------------------------------------------------ squarer (f64 only)
+    if (SQUARER) {
+      U bits = 0;
+      for (int chunk = 0; chunk < n_chunks; ++chunk) {
+        const int stage = chunk % K1_STAGES;
+        mbar_wait(&full_bar[stage], (chunk / K1_STAGES) & 1);
+        if (mine) {
+          unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + lane * K1_LEAF_STRIDE;
+          int v = 0;
+          for (; v + 8 <= segs; v += 8) {  // batched: loads, then squares, then stores
+            double2 w[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) w[u] = *reinterpret_cast<double2 *>(pp + 16 * (v + u));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              bits |= Bits<T>::of((T)w[u].x) | Bits<T>::of((T)w[u].y);
+              w[u].x = __dmul_rn(w[u].x, w[u].x);
+              w[u].y = __dmul_rn(w[u].y, w[u].y);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) *reinterpret_cast<double2 *>(pp + 16 * (v + u)) = w[u];
+          }
+          for (; v < segs; ++v) {
+            double2 w = *reinterpret_cast<double2 *>(pp + 16 * v);
+            bits |= Bits<T>::of((T)w.x) | Bits<T>::of((T)w.y);
+            w.x = __dmul_rn(w.x, w.x);
+            w.y = __dmul_rn(w.y, w.y);
+            *reinterpret_cast<double2 *>(pp + 16 * v) = w;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sq_bar[stage]);
       }
+      s_bits[lane] = bits;
+      asm volatile("bar.sync 1, 64;\n" ::: "memory");  // hand the bit ORs to warp 0
     }
     return;
   }
 
   // --------------------------------------------------------------- warp 0
-  const int64_t my_x = leaf0 + tid;
-  const bool mine = my_x < n_leaves;
   double acc = 0.0;
   U bits = 0;
   for (int chunk = 0; chunk < n_chunks; ++chunk) {
     const int stage = chunk % K1_STAGES;
-    mbar_wait(&full_bar[stage], (chunk / K1_STAGES) & 1);
+    mbar_wait(SQUARER ? &sq_bar[stage] : &full_bar[stage], (chunk / K1_STAGES) & 1);
     if (mine) {
-      const unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + tid * K1_LEAF_STRIDE;
+      const unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + lane * K1_LEAF_STRIDE;
       int v = 0;
       for (; v + 8 <= segs; v += 8) {
         uint4 w[8];
@@ -252,23 +301,40 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
         for (int u = 0; u < 8; ++u) w[u] = *reinterpret_cast<const uint4 *>(pp + 16 * (v + u));
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const T *x = reinterpret_cast<const T *>(&w[u]);
+          if (SQUARER) {
+            const double *q2 = reinterpret_cast<const double *>(&w[u]);
+            acc = __dadd_rn(acc, q2[0]);
+            acc = __dadd_rn(acc, q2[1]);
+          } else {
+            const T *x = reinterpret_cast<const T *>(&w[u]);
 #pragma unroll
-          for (int e = 0; e < EPS; ++e) accum<T>(acc, bits, x[e]);
+            for (int e = 0; e < EPS; ++e) accum<T>(acc, bits, x[e]);
+          }
         }
       }
       for (; v < segs; ++v) {
         const uint4 w = *reinterpret_cast<const uint4 *>(pp + 16 * v);
-        const T *x = reinterpret_cast<const T *>(&w);
+        if (SQUARER) {
+          const double *q2 = reinterpret_cast<const double *>(&w);
+          acc = __dadd_rn(acc, q2[0]);
+          acc = __dadd_rn(acc, q2[1]);
+        } else {
+          const T *x = reinterpret_cast<const T *>(&w);
 #pragma unroll
-        for (int e = 0; e < EPS; ++e) accum<T>(acc, bits, x[e]);
+          for (int e = 0; e < EPS; ++e) accum<T>(acc, bits, x[e]);
+        }
       }
     }
     __syncwarp();
-    if (tid == 0) mbar_arrive(&empty_bar[stage]);
+    if (lane == 0) mbar_arrive(&empty_bar[stage]);
+  }
+  if (SQUARER) {
+    asm volatile("bar.sync 1, 64;\n" ::: "memory");
+    bits = s_bits[lane];
   }
   if (mine) {
-    const int64_t leaf = list ? (int64_t)list[my_x] : my_x;
+    const int64_t lx = leaf0 + lane;
+    const int64_t leaf = list ? (int64_t)list[lx] : lx;
     const bool nz = (U)(bits << 1) != 0;
     nsq_leaf[leaf] = acc;
     occ_leaf[leaf] = (uint8_t)nz;
