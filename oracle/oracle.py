@@ -49,6 +49,10 @@ def lib():
         L.oracle_cull.argtypes = [vp, vp, vp, vp, ctypes.c_int, i64, dp, ctypes.c_int,
                                   ctypes.c_int, ctypes.c_int, ctypes.POINTER(_CullResult)]
         L.oracle_cull.restype = ctypes.c_int
+        L.oracle_cull_rows.argtypes = [vp, vp, vp, vp, ctypes.c_int, i64, dp, ctypes.c_int,
+                                       ctypes.c_int, ctypes.c_int, i64, i64,
+                                       ctypes.POINTER(_CullResult)]
+        L.oracle_cull_rows.restype = ctypes.c_int
         L.oracle_leaf_stage.argtypes = [vp, vp, ctypes.c_int, i64, i32, vp, i64, vp]
         L.oracle_leaf_stage.restype = ctypes.c_int
         L.oracle_free.argtypes = [vp]
@@ -98,12 +102,15 @@ def build_pyramid(padded, leaf):
 
 
 def cull(nsq_a, occ_a, nsq_b, occ_b, depth, N, tau, tier_tau_decay=False, count_stats=True,
-         collect_boxes=True):
+         collect_boxes=True, rows=None):
+    """Tier traversal; ``rows=(lo, hi)`` restricts it to a C block-row shard."""
     r = _CullResult()
     L = lib()
-    rc = L.oracle_cull(nsq_a.ctypes.data, occ_a.ctypes.data, nsq_b.ctypes.data,
-                       occ_b.ctypes.data, depth, N, float(tau), int(tier_tau_decay),
-                       int(count_stats), int(collect_boxes), ctypes.byref(r))
+    lo, hi = (0, 1 << depth) if rows is None else rows
+    rc = L.oracle_cull_rows(nsq_a.ctypes.data, occ_a.ctypes.data, nsq_b.ctypes.data,
+                            occ_b.ctypes.data, depth, N, float(tau), int(tier_tau_decay),
+                            int(count_stats), int(collect_boxes), int(lo), int(hi),
+                            ctypes.byref(r))
     if rc != 0:
         raise MemoryError("oracle_cull failed")
     trip = np.ctypeslib.as_array(r.triples, shape=(r.n_triples, 3)).copy() if r.n_triples \

@@ -146,10 +146,30 @@ static int cmp_triple(const void *x, const void *y) {
  * in 000..111 order (:35-37, :207-212).  Leaf survivors are returned sorted
  * by (i, j, k) like _leaf_stage's lexsort (:231-233).
  */
+/*
+ * Row-sharded variant (the multi-GPU layout, not in the reference): only
+ * triples whose leaf rows [i << (depth-t), (i+1) << (depth-t)) intersect
+ * [row_lo, row_hi) are traversed, and a pruned / skipped call is counted by
+ * the shard owning its first row.  Summed over disjoint shards covering all
+ * rows, every integer statistic equals the unsharded traversal's.
+ */
+int oracle_cull_rows(const double *nsq_a, const uint8_t *occ_a, const double *nsq_b,
+                     const uint8_t *occ_b, int depth, int64_t N, double tau,
+                     int tier_tau_decay, int count_stats, int collect_boxes,
+                     int64_t row_lo, int64_t row_hi, oracle_cull_result *res);
+
 int oracle_cull(const double *nsq_a, const uint8_t *occ_a, const double *nsq_b,
                 const uint8_t *occ_b, int depth, int64_t N, double tau,
                 int tier_tau_decay, int count_stats, int collect_boxes,
                 oracle_cull_result *res) {
+  return oracle_cull_rows(nsq_a, occ_a, nsq_b, occ_b, depth, N, tau, tier_tau_decay,
+                          count_stats, collect_boxes, 0, (int64_t)1 << depth, res);
+}
+
+int oracle_cull_rows(const double *nsq_a, const uint8_t *occ_a, const double *nsq_b,
+                     const uint8_t *occ_b, int depth, int64_t N, double tau,
+                     int tier_tau_decay, int count_stats, int collect_boxes,
+                     int64_t row_lo, int64_t row_hi, oracle_cull_result *res) {
   memset(res, 0, sizeof *res);
   int64_t cap = 8, n = 1;
   int32_t *cur = (int32_t *)malloc(sizeof(int32_t) * 3 * cap);
@@ -170,12 +190,19 @@ int oracle_cull(const double *nsq_a, const uint8_t *occ_a, const double *nsq_b,
     double *pruned_np = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
     if (!act || !pruned_np) return -1;
     int64_t n_act = 0, n_alive = 0, n_pruned = 0;
+    const int shift = depth - tier;
+    int64_t n_skip_owned = 0;
     for (int64_t c = 0; c < n; ++c) {
       const int32_t i = cur[3 * c], j = cur[3 * c + 1], k = cur[3 * c + 2];
+      const int64_t r0 = (int64_t)i << shift, r1 = (int64_t)(i + 1) << shift;
+      if (!(r1 > row_lo && r0 < row_hi)) continue;  /* another shard's rows */
+      const int owned = r0 >= row_lo && r0 < row_hi;
       const int alive = oa[(int64_t)i * s + k] && ob[(int64_t)k * s + j];
       const double np_ = sqrt(na[(int64_t)i * s + k]) * sqrt(nb_[(int64_t)k * s + j]);
       const int pruned = alive && (np_ < tau_t);
       n_alive += alive;
+      if (!alive && owned) ++n_skip_owned;
+      if (pruned && !owned) continue;  /* counted by the owning shard */
       if (pruned) {
         pruned_np[n_pruned++] = np_;
         if (collect_boxes) {
@@ -194,7 +221,7 @@ int oracle_cull(const double *nsq_a, const uint8_t *occ_a, const double *nsq_b,
       }
     }
     if (count_stats) {
-      const int64_t n_skip = n - n_alive;
+      const int64_t n_skip = n_skip_owned;
       res->pruned_calls += n_skip + n_pruned;
       res->empty_skip_volume += n_skip * vol;
       res->pruned_volume += n_pruned * vol;

@@ -1,0 +1,94 @@
+"""Host-side behaviour of the drop-in API that needs no GPU: validation and
+exception types mirror the reference (quadtree.py:218-251, multiply.py:43-74,
+:77-116), and the compute path refuses to run without the CUDA library/GPU
+instead of falling back to the CPU."""
+
+import dataclasses
+import math
+
+import numpy as np
+import pytest
+
+import paper_1011_3534_b200 as sp
+from paper_1011_3534_b200 import quadtree
+
+
+def test_config_validation():
+    for bad in (-1e-9, float("nan"), float("inf"), -float("inf")):
+        with pytest.raises(ValueError):
+            sp.SpammConfig(tau=bad)
+    cfg = sp.SpammConfig(tau=1e-8)
+    assert cfg.count_stats and cfg.deterministic and not cfg.collect_boxes
+    with pytest.raises(dataclasses.FrozenInstanceError):
+        cfg.tau = 1.0
+
+
+def test_stats_and_boxes():
+    st = sp.ProductStats(leaf_matmuls=3, pruned_volume=10, empty_skip_volume=7)
+    assert st.covered_volume(2) == 3 * 8 + 17
+    assert st.boxes is None
+    bx = sp.PrunedBox(0, 4, 8, 4, 2)
+    assert bx == sp.PrunedBox(0, 4, 8, 4, 2)
+    assert sp.ProductStats() == sp.ProductStats()
+
+
+@pytest.mark.parametrize("leaf", [0, 3, 6, -4])
+def test_bad_leaf_size(leaf):
+    with pytest.raises(ValueError):
+        sp.from_dense(np.eye(4), leaf_size=leaf)
+
+
+def test_bad_dtype():
+    with pytest.raises(ValueError):
+        sp.from_dense(np.eye(4), dtype=np.int32)
+    with pytest.raises(ValueError):
+        sp.from_dense(np.eye(4), dtype=np.float16)
+
+
+def test_non_square_and_empty():
+    with pytest.raises(sp.DimensionMismatchError):
+        sp.from_dense(np.ones((3, 4)))
+    with pytest.raises(sp.DimensionMismatchError):
+        sp.from_dense(np.ones(5))
+    assert issubclass(sp.DimensionMismatchError, ValueError)
+    with pytest.raises(ValueError):
+        sp.from_dense(np.zeros((0, 0)))
+
+
+def test_direct_construction_rejected():
+    with pytest.raises(TypeError):
+        sp.QuadTreeMatrix()
+
+
+def test_conformability_checked_in_python():
+    class Fake:
+        def __init__(self, n, leaf, dtype):
+            self.logical_dim, self.leaf_size, self.dtype = n, leaf, np.dtype(dtype)
+
+    with pytest.raises(sp.DimensionMismatchError):
+        quadtree._require_conformable(Fake(16, 4, np.float64), Fake(32, 4, np.float64))
+    with pytest.raises(sp.DimensionMismatchError):
+        quadtree._require_conformable(Fake(16, 4, np.float64), Fake(16, 2, np.float64))
+    with pytest.raises(sp.DimensionMismatchError):
+        quadtree._require_conformable(Fake(16, 4, np.float64), Fake(16, 4, np.float32))
+
+
+def test_no_cpu_fallback_without_gpu():
+    """On a machine without a CUDA device the product path raises; it never
+    computes on the host."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises((RuntimeError, ValueError)):
+        sp.from_dense(np.eye(8), leaf_size=4)
+
+
+def test_public_surface_matches_reference_names():
+    ref_hot_path = ["EMPTY", "DimensionMismatchError", "EmptyNode", "InteriorNode", "LeafNode",
+                    "QuadTreeMatrix", "from_dense", "identity", "node_norm", "to_dense",
+                    "ProductStats", "PrunedBox", "SpammConfig", "exact_multiply",
+                    "multiply_error", "spamm"]
+    for name in ref_hot_path:
+        assert hasattr(sp, name), name
+    assert sp.EMPTY.kind == "empty" and sp.EMPTY.norm_sq == 0.0
+    assert math.isclose(sp.LeafNode(None, 4.0).norm_sq, 4.0)

@@ -1,0 +1,281 @@
+"""The drop-in API on the B200, exercised like the reference's own tests
+(pkg/tests/test_quadtree.py, test_multiply.py, test_acceptance.py), with the
+CPU oracle or dense numpy as the independent check.  Every multiply runs
+through the C ABI and the CUDA kernels."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1011_3534_b200 as sp
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _exp_pair(n, a1, a2):
+    d = np.abs(np.arange(n)[:, None] - np.arange(n)[None, :]).astype(float)
+    return np.exp(-a1 * d), np.exp(-a2 * d)
+
+
+# ------------------------------------------------------------- quadtree
+def test_identity4_single_leaf():
+    m = sp.from_dense(np.eye(4), leaf_size=4)
+    assert isinstance(m.root, sp.LeafNode)
+    assert m.root.norm_sq == 4.0 and m.padded_dim == 4 and m.depth == 0
+
+
+def test_zero8_empty_root():
+    m = sp.from_dense(np.zeros((8, 8)), leaf_size=4)
+    assert isinstance(m.root, sp.EmptyNode) and m.depth == 1 and m.root.norm_sq == 0.0
+
+
+def test_ones5_padding_and_quadrants():
+    m = sp.from_dense(np.ones((5, 5)), leaf_size=4)
+    assert m.padded_dim == 8 and m.depth == 1 and m.root.norm_sq == 25.0
+    assert m.root.children[3].norm_sq == 1.0
+
+
+def test_roundtrip_exhaustive_small():
+    rng = np.random.default_rng(0)
+    for n in range(1, 66):
+        data = rng.standard_normal((n, n))
+        for leaf in (1, 2, 4):
+            m = sp.from_dense(data, leaf_size=leaf)
+            back = sp.to_dense(m)
+            assert back.shape == (n, n) and np.array_equal(back, data), (n, leaf)
+            pad = m._padded
+            assert not pad[n:, :].any() and not pad[:, n:].any()
+
+
+def test_roundtrip_rebuild_identical_tree():
+    rng = np.random.default_rng(1)
+    data = rng.standard_normal((100, 100))
+    m = sp.from_dense(data)
+    again = sp.from_dense(sp.to_dense(m))
+    assert again.structurally_equal(m)
+    assert again.root.norm_sq == m.root.norm_sq
+
+
+def test_norm_matches_dense():
+    rng = np.random.default_rng(2)
+    for n in (3, 16, 50, 127):
+        data = rng.standard_normal((n, n))
+        ref = float(np.linalg.norm(data))
+        assert abs(sp.node_norm(sp.from_dense(data)) - ref) <= 8 * np.finfo(float).eps * ref
+
+
+@pytest.mark.parametrize("leaf", [1, 2, 4, 8, 16, 32, 64, 128])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_pyramid_bit_exact_vs_oracle(leaf, dtype):
+    rng = np.random.default_rng(leaf)
+    n = 3 * leaf + 5
+    data = (rng.standard_normal((n, n)) * np.exp(-0.3 * np.abs(np.arange(n)[:, None] - np.arange(n)))).astype(dtype)
+    data[: min(n, leaf), : min(n, leaf)] = -0.0  # an all-(-0.0) leaf is canonicalised
+    m = sp.from_dense(data, leaf_size=leaf, dtype=dtype)
+    pa = oracle.pad(data, leaf, dtype)
+    nsq, occ = oracle.build_pyramid(pa, leaf)
+    assert np.array_equal(m._pyramid()[2].view(np.uint64), nsq.view(np.uint64))
+    assert np.array_equal(m._pyramid()[3], occ)
+    assert np.array_equal(m._padded.view(np.uint8), pa.view(np.uint8))  # incl. +0.0 rewrite
+
+
+# ------------------------------------------------------------- multiply
+def test_identity_times_b_exact():
+    bd = np.random.default_rng(0).standard_normal((20, 20))
+    c, stats = sp.spamm(sp.identity(20), sp.from_dense(bd), sp.SpammConfig(tau=0.0))
+    assert np.array_equal(sp.to_dense(c), bd) and stats.omitted_budget == 0.0
+
+
+def test_tau_above_total_norm_prunes_root():
+    rng = np.random.default_rng(1)
+    a = sp.from_dense(rng.standard_normal((16, 16)))
+    b = sp.from_dense(rng.standard_normal((16, 16)))
+    budget = sp.node_norm(a) * sp.node_norm(b)
+    c, st = sp.spamm(a, b, sp.SpammConfig(tau=budget * 1.5, collect_boxes=True))
+    assert isinstance(c.root, sp.EmptyNode) and st.leaf_matmuls == 0
+    assert st.omitted_budget == math.sqrt(a._norm_sq[0][0, 0]) * math.sqrt(b._norm_sq[0][0, 0])
+    assert st.boxes == [sp.PrunedBox(0, 0, 0, a.padded_dim, 0)]
+
+
+def test_full_enumeration_counts():
+    rng = np.random.default_rng(2)
+    for n, leaf in ((8, 4), (64, 8), (256, 32)):
+        a = sp.from_dense(rng.standard_normal((n, n)), leaf_size=leaf)
+        b = sp.from_dense(rng.standard_normal((n, n)), leaf_size=leaf)
+        _, st = sp.spamm(a, b, sp.SpammConfig(tau=0.0))
+        assert st.leaf_matmuls == (n // leaf) ** 3
+
+
+def test_exact_vs_dense_many_leaves():
+    rng = np.random.default_rng(3)
+    for n, leaf in ((64, 4), (100, 8), (128, 16), (300, 32), (256, 64), (512, 128)):
+        ad = rng.standard_normal((n, n))
+        bd = rng.standard_normal((n, n))
+        got = sp.to_dense(sp.exact_multiply(sp.from_dense(ad, leaf_size=leaf),
+                                            sp.from_dense(bd, leaf_size=leaf)))
+        ref = ad @ bd
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-13
+
+
+def test_zero_operand_gives_empty():
+    rng = np.random.default_rng(4)
+    z = sp.from_dense(np.zeros((24, 24)))
+    m = sp.from_dense(rng.standard_normal((24, 24)))
+    assert isinstance(sp.exact_multiply(z, m).root, sp.EmptyNode)
+    c2, st = sp.spamm(m, z, sp.SpammConfig(tau=0.0))
+    assert isinstance(c2.root, sp.EmptyNode)
+    assert st.leaf_matmuls == 0 and st.pruned_calls == 1
+    assert st.empty_skip_volume == m.padded_dim ** 3
+
+
+def test_permutation_times_transpose_is_identity():
+    perm = np.random.default_rng(5).permutation(32)
+    p = np.zeros((32, 32))
+    p[np.arange(32), perm] = 1.0
+    c = sp.exact_multiply(sp.from_dense(p), sp.from_dense(p.T))
+    assert np.array_equal(sp.to_dense(c), np.eye(32))
+
+
+@pytest.mark.parametrize("leaf,tau", [(4, 1e-8), (8, 1e-6), (16, 1e-6), (32, 1e-7), (64, 1e-9),
+                                      (128, 1e-9)])
+def test_matches_oracle_bit_exact(leaf, tau):
+    """Retained triples, boxes, stats and C bit-for-bit vs the oracle across
+    every leaf-kernel path (SIMT <= 16, DMMA 32/64, DMMA sub-tiled 128)."""
+    n = max(512, 8 * leaf)
+    a_d, b_d = _exp_pair(n, 0.05 * 64 / leaf, 0.07 * 64 / leaf)
+    rng = np.random.default_rng(leaf)
+    a_d = a_d * rng.uniform(-1, 1, a_d.shape)
+    b_d = b_d * rng.uniform(-1, 1, b_d.shape)
+    a = sp.from_dense(a_d, leaf_size=leaf)
+    b = sp.from_dense(b_d, leaf_size=leaf)
+    c, st, det = sp.spamm_detailed(a, b, sp.SpammConfig(tau=tau, collect_boxes=True),
+                                   keep_triples=True)
+    ref = oracle.spamm(a_d, b_d, leaf, tau)
+    assert np.array_equal(det.triples, ref["triples"])
+    got_boxes = np.array([[x.i_lo, x.j_lo, x.k_lo, x.edge, x.tier] for x in st.boxes],
+                         np.int64).reshape(-1, 5)
+    assert np.array_equal(got_boxes, ref["boxes"])
+    for k in ("leaf_matmuls", "pruned_calls", "pruned_volume", "empty_skip_volume",
+              "max_depth_reached"):
+        assert getattr(st, k) == ref["stats"][k], k
+    assert st.omitted_budget == ref["stats"]["omitted_budget"]
+    assert np.array_equal(c._padded.view(np.uint64), ref["c_padded"].view(np.uint64))
+    assert np.array_equal(c._pyramid()[2].view(np.uint64), ref["nsq_c"].view(np.uint64))
+
+
+def test_float32_path_matches_oracle():
+    n, leaf, tau = 384, 32, 1e-5
+    a_d, b_d = _exp_pair(n, 0.02, 0.03)
+    rng = np.random.default_rng(7)
+    a_d = (a_d * rng.uniform(-1, 1, a_d.shape)).astype(np.float32)
+    b_d = (b_d * rng.uniform(-1, 1, b_d.shape)).astype(np.float32)
+    a = sp.from_dense(a_d, leaf_size=leaf, dtype=np.float32)
+    b = sp.from_dense(b_d, leaf_size=leaf, dtype=np.float32)
+    c, st, det = sp.spamm_detailed(a, b, sp.SpammConfig(tau=tau), keep_triples=True)
+    ref = oracle.spamm(a_d, b_d, leaf, tau, dtype=np.float32)
+    assert np.array_equal(det.triples, ref["triples"])
+    assert st.omitted_budget == ref["stats"]["omitted_budget"]
+    assert np.array_equal(c._padded.view(np.uint32), ref["c_padded"].view(np.uint32))
+
+
+def test_error_bound_random_decay_pairs():
+    rng = np.random.default_rng(7)
+    taus = [1e-2, 1e-4, 1e-6, 1e-8, 1e-10, 1e-12]
+    for _ in range(20):
+        n = int(rng.integers(8, 49))
+        alpha = float(rng.uniform(0.2, 2.5))
+        idx = np.arange(n)
+        decay = np.exp(-alpha * np.abs(idx[:, None] - idx[None, :]))
+        a = sp.from_dense(decay * rng.standard_normal((n, n)))
+        b = sp.from_dense(decay * rng.standard_normal((n, n)))
+        scale_ab = sp.node_norm(a) * sp.node_norm(b)
+        exact = sp.to_dense(sp.exact_multiply(a, b))
+        for tau in taus:
+            approx, st = sp.spamm(a, b, sp.SpammConfig(tau=tau))
+            err = float(np.linalg.norm(sp.to_dense(approx) - exact))
+            assert err <= st.omitted_budget + 1e-12 * scale_ab
+
+
+def test_multiply_error_matches_dense():
+    a_d, b_d = _exp_pair(512, 1.0, 2.0)
+    a, b = sp.from_dense(a_d), sp.from_dense(b_d)
+    for tau in (1e-2, 1e-6, 1e-10):
+        err, budget = sp.multiply_error(a, b, sp.SpammConfig(tau=tau))
+        approx, st = sp.spamm(a, b, sp.SpammConfig(tau=tau))
+        ref = float(np.linalg.norm(sp.to_dense(approx) - sp.to_dense(sp.exact_multiply(a, b))))
+        assert abs(err - ref) <= 1e-12 * max(ref, 1e-300) + 1e-300
+        assert budget == st.omitted_budget and err <= budget + 1e-12
+
+
+def test_monotone_work_and_tier_decay():
+    a_d, b_d = _exp_pair(256, 0.7, 1.3)
+    a, b = sp.from_dense(a_d), sp.from_dense(b_d)
+    counts = [sp.spamm(a, b, sp.SpammConfig(tau=t))[1].leaf_matmuls
+              for t in (0.0, 1e-12, 1e-9, 1e-6, 1e-3, 1e-1)]
+    assert all(lo <= hi for lo, hi in zip(counts[1:], counts[:-1]))
+    flat = sp.spamm(a, b, sp.SpammConfig(tau=1e-6))[1]
+    dec = sp.spamm(a, b, sp.SpammConfig(tau=1e-6, tier_tau_decay=True))[1]
+    assert dec.leaf_matmuls >= flat.leaf_matmuls
+    assert dec.omitted_budget <= flat.omitted_budget
+    assert dec.covered_volume(4) == a.padded_dim ** 3
+
+
+def test_determinism_bit_identical():
+    a_d, b_d = _exp_pair(256, 0.9, 1.1)
+    a, b = sp.from_dense(a_d), sp.from_dense(b_d)
+    cfg = sp.SpammConfig(tau=1e-7, collect_boxes=True)
+    c1, s1 = sp.spamm(a, b, cfg)
+    c2, s2 = sp.spamm(a, b, cfg)
+    assert sp.to_dense(c1).tobytes() == sp.to_dense(c2).tobytes()
+    assert s1 == s2
+
+
+def test_count_stats_off():
+    a_d, b_d = _exp_pair(128, 0.5, 0.5)
+    a, b = sp.from_dense(a_d), sp.from_dense(b_d)
+    _, st = sp.spamm(a, b, sp.SpammConfig(tau=1e-6, count_stats=False))
+    assert st.leaf_matmuls == 0 and st.pruned_calls == 0 and st.omitted_budget == 0.0
+    assert st.max_depth_reached == a.depth
+
+
+def test_dimension_mismatch_rejected():
+    rng = np.random.default_rng(10)
+    a = sp.from_dense(rng.standard_normal((16, 16)))
+    with pytest.raises(sp.DimensionMismatchError):
+        sp.spamm(a, sp.from_dense(rng.standard_normal((32, 32))), sp.SpammConfig())
+    with pytest.raises(sp.DimensionMismatchError):
+        sp.spamm(a, sp.from_dense(rng.standard_normal((16, 16)), leaf_size=2), sp.SpammConfig())
+    with pytest.raises(sp.DimensionMismatchError):
+        sp.spamm(a, sp.from_dense(rng.standard_normal((16, 16)), dtype=np.float32),
+                 sp.SpammConfig())
+
+
+def test_product_tree_chains():
+    """C feeds the next multiply (the SP2 pattern): C's tree equals a tree
+    rebuilt from its dense form, bit for bit."""
+    a_d, _ = _exp_pair(300, 0.3, 0.3)
+    a = sp.from_dense(a_d, leaf_size=16)
+    c, _ = sp.spamm(a, a, sp.SpammConfig(tau=1e-9))
+    again = sp.from_dense(sp.to_dense(c), leaf_size=16)
+    assert again.structurally_equal(c)
+    assert np.array_equal(again._pyramid()[2].view(np.uint64), c._pyramid()[2].view(np.uint64))
+    c2, _ = sp.spamm(c, c, sp.SpammConfig(tau=1e-9))
+    r2 = oracle.spamm(sp.to_dense(c), sp.to_dense(c), 16, 1e-9)
+    assert np.array_equal(c2._padded.view(np.uint64), r2["c_padded"].view(np.uint64))
+
+
+@pytest.mark.slow
+def test_c5_proxy_n16384_vs_oracle():
+    """The n=65536 config's structure at a size the oracle finishes in
+    seconds: sym(u * 0.98^d), B = A, leaf 64, tau = 1e-8."""
+    from paper_1011_3534_b200 import workloads
+    a_d = workloads.exponential_decay(16384, 0.98, 0, symmetric=True)
+    a = sp.from_dense(a_d, leaf_size=64)
+    c, st, det = sp.spamm_detailed(a, a, sp.SpammConfig(tau=1e-8), keep_triples=True)
+    ref = oracle.spamm(a_d, a_d, 64, 1e-8)
+    assert st.leaf_matmuls == ref["stats"]["leaf_matmuls"] == 186166
+    assert np.array_equal(det.triples, ref["triples"])
+    assert st.omitted_budget == ref["stats"]["omitted_budget"]
+    assert np.array_equal(c._padded.view(np.uint64), ref["c_padded"].view(np.uint64))
