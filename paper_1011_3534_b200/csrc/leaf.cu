@@ -17,6 +17,9 @@
 // consecutive k (32 - clz(k_prev ^ k_next)).  Operand tiles stream through a
 // 3-stage cp.async pipeline with padded shared-memory rows (conflict-free
 // fragment loads); CTAs are persistent and take work items from a ticket.
+#include <cstdio>
+#include <cstdlib>
+
 #include "leaf.cuh"
 
 namespace spamm {
@@ -89,6 +92,58 @@ __device__ __forceinline__ bool fetch_work(const LeafArgs &args, int subs_side, 
   return true;
 }
 
+
+// ---------------------------------------------------------------- TMEM stack
+// The merge stack's deeper entries live in tensor memory (unused by DMMA):
+// each warp owns 32 TMEM lanes (its lane quarter) and NREG columns per stack
+// slot, written with tcgen05.st / read with tcgen05.ld (tens of cycles,
+// instead of local-memory round trips to L2).
+template <int NREG>
+__device__ __forceinline__ void tmem_store(uint32_t taddr, const uint32_t (&r)[NREG]);
+template <int NREG>
+__device__ __forceinline__ void tmem_load(uint32_t taddr, uint32_t (&r)[NREG]);
+
+#define R8(o) "r"(r[o]), "r"(r[o + 1]), "r"(r[o + 2]), "r"(r[o + 3]), "r"(r[o + 4]), "r"(r[o + 5]), "r"(r[o + 6]), "r"(r[o + 7])
+#define W8(o) "=r"(r[o]), "=r"(r[o + 1]), "=r"(r[o + 2]), "=r"(r[o + 3]), "=r"(r[o + 4]), "=r"(r[o + 5]), "=r"(r[o + 6]), "=r"(r[o + 7])
+template <>
+__device__ __forceinline__ void tmem_store<32>(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      R8(0), R8(8), R8(16), R8(24)
+      : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_load<32>(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : W8(0), W8(8), W8(16), W8(24)
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_store<16>(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};\n" ::"r"(taddr),
+      R8(0), R8(8)
+      : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_load<16>(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];\n"
+      : W8(0), W8(8)
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+#undef R8
+#undef W8
+
 // ---------------------------------------------------------------- DMMA path
 constexpr int DMMA_BK = 32;
 constexpr int DMMA_STAGES = 3;
@@ -117,12 +172,19 @@ struct DmmaCfg {
   static constexpr int MT = WTM / 16;     // m16 tiles per warp
   static constexpr int NT = WTN / 8;      // n8 tiles per warp
   static constexpr size_t SMEM = sizeof(double) * DMMA_STAGES * STAGE_ELEMS;
+  static constexpr int NREG = MT * NT * 4 * 2;           // b32 registers per accumulator set
+  static constexpr int TM_SLOTS = 4;                      // merge-stack slots kept in TMEM
+  static constexpr int SLOT_COLS = NREG * ((WM * WN + 3) / 4);
+  static constexpr int TM_COLS_RAW = TM_SLOTS * SLOT_COLS;
+  static constexpr int TM_COLS = TM_COLS_RAW <= 32 ? 32 : TM_COLS_RAW <= 64 ? 64
+                                 : TM_COLS_RAW <= 128 ? 128 : TM_COLS_RAW <= 256 ? 256 : 512;
   static_assert(MT >= 1 && NT >= 1, "warp tile too small");
+  static_assert(NREG == 16 || NREG == 32, "TMEM spill width");
   static_assert((TILE * DMMA_BK / 2) % THREADS == 0 && (DMMA_BK * TILE / 2) % THREADS == 0, "");
 };
 
 template <int TILE, int WM, int WN>
-__global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) {
+__global__ void __launch_bounds__(32 * WM * WN, 2) leaf_dmma_kernel(LeafArgs args) {
   using C = DmmaCfg<TILE, WM, WN>;
   constexpr int QA = (TILE * DMMA_BK / 2) / C::THREADS;  // 16-B copies per thread, A stage
   constexpr int QB = (DMMA_BK * TILE / 2) / C::THREADS;  // 16-B copies per thread, B stage
@@ -174,8 +236,65 @@ __global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) 
   // strictly decreasing from bottom to top, so they form a bit mask whose
   // lowest set bit is the top.  The top value lives in registers; deeper
   // ones in stk[level] (local memory), written back only when dirty.
-  double stk[MAXD][C::MT][C::NT][4];
+  double stk[MAXD][C::MT][C::NT][4];  // only slots >= TM_SLOTS (deep stacks)
   double top[C::MT][C::NT][4];
+  __shared__ uint32_t s_tmem;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&s_tmem)),
+                 "n"(C::TM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t t_my = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * C::NREG);
+  auto spill = [&](int slot) {
+    if (slot < C::TM_SLOTS) {
+      uint32_t r[C::NREG];
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int x = ((mt * C::NT + nt) * 4 + q) * 2;
+            r[x] = (uint32_t)__double2loint(top[mt][nt][q]);
+            r[x + 1] = (uint32_t)__double2hiint(top[mt][nt][q]);
+          }
+      tmem_store<C::NREG>(t_my + slot * C::SLOT_COLS, r);
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) stk[slot][mt][nt][q] = top[mt][nt][q];
+    }
+  };
+  auto reload = [&](int slot) {
+    if (slot < C::TM_SLOTS) {
+      uint32_t r[C::NREG];
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      tmem_load<C::NREG>(t_my + slot * C::SLOT_COLS, r);
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int x = ((mt * C::NT + nt) * 4 + q) * 2;
+            top[mt][nt][q] = __hiloint2double((int)r[x + 1], (int)r[x]);
+          }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) top[mt][nt][q] = stk[slot][mt][nt][q];
+    }
+  };
 
   WorkItem w;
   const unsigned long long t_start = gtimer();
@@ -267,27 +386,13 @@ __global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) 
 #pragma unroll
               for (int q = 0; q < 4; ++q) acc[mt][nt][q] = __dadd_rn(top[mt][nt][q], acc[mt][nt][q]);
           pending &= pending - 1;
-          if (pending) {
-            const int lv = __ffs(pending) - 1;
-#pragma unroll
-            for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-              for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) top[mt][nt][q] = stk[lv][mt][nt][q];
+          if (pending) {  // the new top sits at stack position popcount - 1
+            reload(__popc(pending) - 1);
             top_dirty = false;
           }
         }
         if (s + 1 < nk) {
-          if (pending && top_dirty) {
-            const int lv = __ffs(pending) - 1;
-#pragma unroll
-            for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-              for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) stk[lv][mt][nt][q] = top[mt][nt][q];
-          }
+          if (pending && top_dirty) spill(__popc(pending) - 1);
 #pragma unroll
           for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
@@ -316,6 +421,11 @@ __global__ void __launch_bounds__(32 * WM * WN) leaf_dmma_kernel(LeafArgs args) 
               make_double2(acc[mt][nt][2 * h2], acc[mt][nt][2 * h2 + 1]);
     __syncthreads();
   }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
+                 "n"(C::TM_COLS));
   if (args.timeline && threadIdx.x == 0) {
     args.timeline[3 * blockIdx.x] = t_start;
     args.timeline[3 * blockIdx.x + 1] = gtimer();
@@ -331,7 +441,16 @@ static int launch_dmma(const LeafArgs &args, int num_sms, cudaStream_t st) {
                                       (int)C::SMEM));
   int per_sm = 0;
   SPAMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM));
-  kern<<<num_sms * (per_sm > 0 ? per_sm : 1), C::THREADS, C::SMEM, st>>>(args);
+  if (getenv("SPAMM_GEMM_TIMELINE")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kern);
+    fprintf(stderr, "[gemm launch] per_sm=%d regs=%d static_smem=%zu dyn=%zu maxthreads=%d\n", per_sm,
+            fa.numRegs, fa.sharedSizeBytes, C::SMEM, fa.maxThreadsPerBlock);
+  }
+  // The occupancy query reports 1 CTA/SM for kernels that allocate TMEM; two
+  // fit (registers, shared memory and 2 x TM_COLS <= 512 TMEM columns), and
+  // the persistent ticket loop is correct for any grid size.
+  kern<<<num_sms * (per_sm > 2 ? per_sm : 2), C::THREADS, C::SMEM, st>>>(args);
   return SPAMM_OK;
 }
 

@@ -7,6 +7,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -84,13 +85,13 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed) {
 // rounding).  The parallelism is across leaves only -- a per-leaf shuffle
 // tree would change the bits the strict `< tau` tests compare.
 //
-// Data movement (warp-specialised): a CTA owns K1_LT = 32 leaves.
+// Data movement (warp-specialised): a CTA owns K1_LT (8 or 32) leaves.
 //   warps 2-3  stream the leaves through a K1_STAGES-deep ring of
 //              512-byte-per-leaf stages with cp.async; their copies arrive on
 //              the stage's "full" mbarrier as they land;
-//   warp 1     (f64) squares every element in place, rn(x*x), and ORs the
-//              raw bit patterns for the occupancy / -0.0 tests, then arrives
-//              on "squared";
+//   warps 1-4  (f64) square every element in place, rn(x*x), and OR the
+//              raw bit patterns for the occupancy / -0.0 tests (each warp a
+//              quarter of every leaf's segments), then arrive on "squared";
 //   warp 0     runs the 32 sequential chains acc = rn(acc + sq) -- nothing
 //              else sits on the dependent-add critical path -- and releases
 //              the stage on "empty".
@@ -98,12 +99,11 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed) {
 // fit in place).  Stages carry 16 B of padding per leaf, so the per-lane
 // LDS.128 reads are bank-conflict free while every global read uses whole
 // 128-byte lines.
-constexpr int K1_LT = 32;
+constexpr int K1_SQ_WARPS = 3;                 // squarer warps (f64): SMSPs 1-3, never the chain warp's
 constexpr int K1_PRODUCERS = 64;
-constexpr int K1_THREADS = 64 + K1_PRODUCERS;
+constexpr int K1_THREADS = 32 * (1 + K1_SQ_WARPS) + K1_PRODUCERS;
 constexpr int K1_CHUNK = 512;                  // bytes per leaf per stage
 constexpr int K1_LEAF_STRIDE = K1_CHUNK + 16;  // smem bytes per leaf per stage
-constexpr int K1_STAGE_BYTES = K1_LT * K1_LEAF_STRIDE;
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -167,7 +167,7 @@ __device__ void canonicalise_leaf(T *padded, int64_t N, int32_t b, int64_t bi, i
 }
 
 // Staged kernel: requires b * sizeof(T) >= 16.
-template <typename T, int K1_STAGES>
+template <typename T, int K1_STAGES, int K1_LT>
 __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restrict__ padded,
                                                                       int64_t N, int32_t b,
                                                                       int64_t nb,
@@ -176,10 +176,11 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
                                                                       const uint32_t *__restrict__ list,
                                                                       const unsigned *list_count) {
   using U = typename Bits<T>::U;
-  constexpr bool SQUARER = sizeof(T) == 8;  // warp 1 squares in place (f64 only)
+  constexpr bool SQUARER = sizeof(T) == 8;  // warps 1-4 square in place (f64 only)
+  constexpr int K1_STAGE_BYTES = K1_LT * K1_LEAF_STRIDE;
   extern __shared__ __align__(16) unsigned char k1_smem[];
   __shared__ __align__(8) uint64_t full_bar[K1_STAGES], sq_bar[K1_STAGES], empty_bar[K1_STAGES];
-  __shared__ U s_bits[K1_LT];
+  __shared__ U s_bits[K1_SQ_WARPS][K1_LT];
   // dense mode: every leaf; list mode: only the listed leaves (C blocks that
   // received products -- every other leaf of C is exactly zero)
   const int64_t n_leaves = list ? (int64_t)*list_count : nb * nb;
@@ -194,22 +195,22 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
   const int n_chunks = (b / R) * chunks_per_row;
   const int segs = EPC * (int)sizeof(T) / 16;  // 16-byte segments per leaf chunk
   constexpr int EPS = 16 / (int)sizeof(T);     // elements per segment
-  const bool mine = leaf0 + lane < n_leaves;
+  const bool mine = lane < K1_LT && leaf0 + lane < n_leaves;
 
   if (tid == 0) {
     for (int s = 0; s < K1_STAGES; ++s) {
       mbar_init(&full_bar[s], K1_PRODUCERS);
-      mbar_init(&sq_bar[s], 1);
+      mbar_init(&sq_bar[s], K1_SQ_WARPS);
       mbar_init(&empty_bar[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
   __syncthreads();
 
-  if (warp >= 2) {
+  if (warp > K1_SQ_WARPS) {
     // ------------------------------------------------------------ producers
-    const int p = tid - 64;
-    constexpr int MAX_SLOTS = K1_LT * (K1_CHUNK / 16) / K1_PRODUCERS;
+    const int p = tid - 32 * (1 + K1_SQ_WARPS);
+    constexpr int MAX_SLOTS = (K1_LT * (K1_CHUNK / 16) + K1_PRODUCERS - 1) / K1_PRODUCERS;
     const T *slot_ptr[MAX_SLOTS];
     unsigned slot_dst[MAX_SLOTS];
 #pragma unroll
@@ -246,17 +247,19 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
     return;
   }
 
-  if (warp == 1) {
-    // ------------------------------------------------ squarer (f64 only)
+  if (warp >= 1) {
+    // ------------------------------------------------ squarers (f64 only)
     if (SQUARER) {
+      const int sw = warp - 1;  // segments [sw*segs/4, (sw+1)*segs/4) of every leaf
+      const int v0 = sw * segs / K1_SQ_WARPS, v1 = (sw + 1) * segs / K1_SQ_WARPS;
       U bits = 0;
       for (int chunk = 0; chunk < n_chunks; ++chunk) {
         const int stage = chunk % K1_STAGES;
         mbar_wait(&full_bar[stage], (chunk / K1_STAGES) & 1);
         if (mine) {
           unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + lane * K1_LEAF_STRIDE;
-          int v = 0;
-          for (; v + 8 <= segs; v += 8) {  // batched: loads, then squares, then stores
+          int v = v0;
+          for (; v + 8 <= v1; v += 8) {  // batched: loads, then squares, then stores
             double2 w[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) w[u] = *reinterpret_cast<double2 *>(pp + 16 * (v + u));
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
 #pragma unroll
             for (int u = 0; u < 8; ++u) *reinterpret_cast<double2 *>(pp + 16 * (v + u)) = w[u];
           }
-          for (; v < segs; ++v) {
+          for (; v < v1; ++v) {
             double2 w = *reinterpret_cast<double2 *>(pp + 16 * v);
             bits |= Bits<T>::of((T)w.x) | Bits<T>::of((T)w.y);
             w.x = __dmul_rn(w.x, w.x);
@@ -280,8 +283,9 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
         __syncwarp();
         if (lane == 0) mbar_arrive(&sq_bar[stage]);
       }
-      s_bits[lane] = bits;
-      asm volatile("bar.sync 1, 64;\n" ::: "memory");  // hand the bit ORs to warp 0
+      if (lane < K1_LT) s_bits[sw][lane] = bits;
+      // hand the bit ORs to warp 0
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * (1 + K1_SQ_WARPS)) : "memory");
     }
     return;
   }
@@ -296,41 +300,42 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
       const unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + lane * K1_LEAF_STRIDE;
       int v = 0;
       for (; v + 8 <= segs; v += 8) {
-        uint4 w[8];
+          uint4 w[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) w[u] = *reinterpret_cast<const uint4 *>(pp + 16 * (v + u));
+          for (int u = 0; u < 8; ++u) w[u] = *reinterpret_cast<const uint4 *>(pp + 16 * (v + u));
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < 8; ++u) {
+            if (SQUARER) {
+              const double *q2 = reinterpret_cast<const double *>(&w[u]);
+              acc = __dadd_rn(acc, q2[0]);
+              acc = __dadd_rn(acc, q2[1]);
+            } else {
+              const T *x = reinterpret_cast<const T *>(&w[u]);
+#pragma unroll
+              for (int e = 0; e < EPS; ++e) accum<T>(acc, bits, x[e]);
+            }
+          }
+        }
+        for (; v < segs; ++v) {
+          const uint4 w = *reinterpret_cast<const uint4 *>(pp + 16 * v);
           if (SQUARER) {
-            const double *q2 = reinterpret_cast<const double *>(&w[u]);
+            const double *q2 = reinterpret_cast<const double *>(&w);
             acc = __dadd_rn(acc, q2[0]);
             acc = __dadd_rn(acc, q2[1]);
           } else {
-            const T *x = reinterpret_cast<const T *>(&w[u]);
+            const T *x = reinterpret_cast<const T *>(&w);
 #pragma unroll
             for (int e = 0; e < EPS; ++e) accum<T>(acc, bits, x[e]);
           }
         }
-      }
-      for (; v < segs; ++v) {
-        const uint4 w = *reinterpret_cast<const uint4 *>(pp + 16 * v);
-        if (SQUARER) {
-          const double *q2 = reinterpret_cast<const double *>(&w);
-          acc = __dadd_rn(acc, q2[0]);
-          acc = __dadd_rn(acc, q2[1]);
-        } else {
-          const T *x = reinterpret_cast<const T *>(&w);
-#pragma unroll
-          for (int e = 0; e < EPS; ++e) accum<T>(acc, bits, x[e]);
-        }
-      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[stage]);
   }
   if (SQUARER) {
-    asm volatile("bar.sync 1, 64;\n" ::: "memory");
-    bits = s_bits[lane];
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * (1 + K1_SQ_WARPS)) : "memory");
+#pragma unroll
+    for (int q = 0; q < K1_SQ_WARPS; ++q) bits |= lane < K1_LT ? s_bits[q][lane] : 0;
   }
   if (mine) {
     const int64_t lx = leaf0 + lane;
@@ -434,24 +439,25 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
   double *nsq_leaf = t->nsq + level_offset(t->depth);
   uint8_t *occ_leaf = t->occ + level_offset(t->depth);
   if (t->leaf * sizeof(T) >= 16) {
-    // few CTAs: one per SM with a deep ring (DRAM latency needs ~10 stages
-    // in flight per chain); many CTAs: two per SM with a shallower ring
-    const int64_t grid = (n_leaves + K1_LT - 1) / K1_LT;
+    // The copy rate one SM sustains with cp.async is limited (outstanding
+    // requests), so small trees spread their leaves thinly -- 8 per CTA over
+    // as many SMs as possible with a deep ring -- and large trees use 32
+    // leaves per CTA, two CTAs per SM.
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
-    if (grid <= sms) {
-      constexpr int S = 12;
-      const size_t smem = (size_t)S * K1_STAGE_BYTES;
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_norm_staged_kernel<T, S>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      leaf_norm_staged_kernel<T, S><<<(unsigned)grid, K1_THREADS, smem, st>>>(
+    if (n_leaves >= (int64_t)64 * sms) {
+      constexpr int S = 6, LT = 32;
+      const size_t smem = (size_t)S * LT * K1_LEAF_STRIDE;
+      auto kern = leaf_norm_staged_kernel<T, S, LT>;
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<(unsigned)((n_leaves + LT - 1) / LT), K1_THREADS, smem, st>>>(
           (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count);
     } else {
-      constexpr int S = 6;
-      const size_t smem = (size_t)S * K1_STAGE_BYTES;
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_norm_staged_kernel<T, S>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      leaf_norm_staged_kernel<T, S><<<(unsigned)grid, K1_THREADS, smem, st>>>(
+      constexpr int S = 12, LT = 8;
+      const size_t smem = (size_t)S * LT * K1_LEAF_STRIDE;
+      auto kern = leaf_norm_staged_kernel<T, S, LT>;
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<(unsigned)((n_leaves + LT - 1) / LT), K1_THREADS, smem, st>>>(
           (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count);
     }
   } else {
