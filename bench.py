@@ -259,7 +259,7 @@ def run_b200(args, cfg_name):
     local_gemm = sum(x[3] for step in per_tau_all for x in step)
     achieved = local_f / (local_gemm * 1e-3) / 1e12 if local_gemm > 0 else 0.0
     traffic = k3_traffic()
-    roofline = {"bound": "tensor", "kernel": "leaf_dmma_kernel<64> (K3)", "achieved": achieved,
+    roofline = {"bound": "tensor", "kernel": "leaf_dmma_ws_kernel<64> (K3)", "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": peak_src,
                 "traffic": traffic.get("bytes_per_launch") if traffic else None,

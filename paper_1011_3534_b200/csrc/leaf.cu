@@ -20,6 +20,9 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "leaf.cuh"
 
 namespace spamm {
@@ -34,16 +37,6 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-__device__ __forceinline__ void dmma16816(double (&c)[4], const double (&a)[8],
-                                          const double (&b)[4]) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
-      "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
-      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
-      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
-        "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
 // One DMMA.8x8x4: C(8x8) += A(8x4) B(4x8), f64, inner index ascending.  Not
@@ -93,42 +86,127 @@ __device__ __forceinline__ bool fetch_work(const LeafArgs &args, int subs_side, 
 }
 
 
-// ---------------------------------------------------------------- TMEM stack
-// The merge stack's deeper entries live in tensor memory (unused by DMMA):
-// each warp owns 32 TMEM lanes (its lane quarter) and NREG columns per stack
-// slot, written with tcgen05.st / read with tcgen05.ld (tens of cycles,
-// instead of local-memory round trips to L2).
+
+// ---------------------------------------------------------------- DMMA path
+constexpr int DMMA_BK = 32;
+
+// Shared-memory tiles are dense (rows of 256 B for A, TILE*8 B for B) with the
+// 16-byte chunks of each 128-byte segment XOR-swizzled by (row & 3) << 1.
+// That makes the DMMA fragment loads (4 rows x 2 chunks per half-warp) hit
+// 32 distinct banks, and keeps every 128-byte global line landing in one
+// 128-byte shared segment for the cp.async copies.
+__device__ __forceinline__ int swz(int row, int col) {  // element offset within a row
+  const int chunk = col >> 1;
+  return (((chunk & ~7) | ((chunk & 7) ^ ((row & 3) << 1))) << 1) | (col & 1);
+}
+
+__device__ __forceinline__ void mbar_init_l(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_l(uint64_t *bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared.b64 st, [%0];\n}\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_l(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_l(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx_l(uint64_t *bar, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared.b64 st, [%0], %1;\n}\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// TMA: one 3-D box of the padded operand -> shared memory (128-byte swizzle),
+// completion counted in bytes on `bar`.
+__device__ __forceinline__ void tma_load_3d(void *smem, const CUtensorMap *map, int x, int y, int z,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+      "l"((uint64_t)map), "r"(x), "r"(y), "r"(z), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+// Tiles land in shared memory as TMA boxes of 128-byte lines with the
+// hardware 128-byte swizzle (16-byte chunk ^= line & 7).  A (TILE x 32) is
+// loaded as the box {16, 2, TILE}: line = 2*row + col/16, so the four rows a
+// half-warp's fragment load touches fall on XOR keys 2*(row & 3) + c -- 32
+// distinct banks.  B (32 x TILE) is the box {16, TILE/16, 32}: line =
+// (TILE/16)*k + n/16 (conflict-free for TILE = 32; 2-way for TILE = 64).
+__device__ __forceinline__ int a_off_tma(int r, int c) {  // elements
+  const int L = 2 * r + (c >> 4), ch = (c & 15) >> 1;
+  return L * 16 + ((ch ^ (L & 7)) << 1) + (c & 1);
+}
+template <int TILE>
+__device__ __forceinline__ int b_off_tma(int k, int n) {
+  const int L = (TILE / 16) * k + (n >> 4), ch = (n & 15) >> 1;
+  return L * 16 + ((ch ^ (L & 7)) << 1) + (n & 1);
+}
+
+// Per-stage metadata written by the producer: what the consumers do after
+// the stage's DMMAs (the merge level of the product that just completed and
+// whether the work item -- one C (sub-)tile -- ends here).
+struct StageInfo {
+  int flags;       // STG_MERGE | STG_END | STG_DONE
+  int h;           // merge level with the next k (31 at the item's end)
+  int64_t c_off;   // element offset of the C (sub-)tile's origin
+};
+constexpr int STG_MERGE = 1, STG_END = 2, STG_DONE = 4;
+
+// Warp-specialised persistent leaf-product kernel.
+//   warp 0      producer: takes work items from the ticket, and for every
+//               32-wide k slice of every retained product streams the A and B
+//               tiles into a STAGES-deep ring with cp.async (completion on the
+//               stage's "full" mbarrier), plus the StageInfo.  It runs ahead
+//               across item boundaries, so item starts cost no pipeline bubble.
+//   warps 1-16  consumers: a 4 x 4 grid of warp tiles over the C tile; each
+//               waits "full", runs its DMMAs, releases the stage ("empty"),
+//               then merges / stores as StageInfo says.  No block-wide
+//               barrier in the loop.
+template <int TILE>
+struct WsCfg {
+  static constexpr int CWARPS = 16, WM = 4, WN = 4;
+  static constexpr int THREADS = 32 * (1 + CWARPS);
+  static constexpr int WTM = TILE / WM, WTN = TILE / WN;  // warp tile
+  static constexpr int MT8 = WTM / 8, NT8 = WTN / 8;      // m8 / n8 tiles per warp
+  static constexpr int NACC = MT8 * NT8 * 2;              // accumulator doubles per thread
+  static constexpr int NREG = 2 * NACC;                   // ... as b32 registers
+  static constexpr int A_ELEMS = TILE * DMMA_BK, B_ELEMS = DMMA_BK * TILE;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr int STAGES = TILE == 64 ? 6 : 10;
+  static constexpr size_t SMEM = sizeof(double) * STAGES * STAGE_ELEMS;
+  static constexpr int SLOT_COLS = NREG * (CWARPS / 4);   // TMEM columns per stack slot
+  static constexpr int TM_COLS = 512;
+  static constexpr int TM_SLOTS = TM_COLS / SLOT_COLS;
+  static constexpr int QA = TILE * DMMA_BK / 2 / 32;      // 16-B copies per producer lane
+  static constexpr int QB = DMMA_BK * TILE / 2 / 32;
+};
+
 template <int NREG>
 __device__ __forceinline__ void tmem_store(uint32_t taddr, const uint32_t (&r)[NREG]);
 template <int NREG>
 __device__ __forceinline__ void tmem_load(uint32_t taddr, uint32_t (&r)[NREG]);
-
-#define R8(o) "r"(r[o]), "r"(r[o + 1]), "r"(r[o + 2]), "r"(r[o + 3]), "r"(r[o + 4]), "r"(r[o + 5]), "r"(r[o + 6]), "r"(r[o + 7])
-#define W8(o) "=r"(r[o]), "=r"(r[o + 1]), "=r"(r[o + 2]), "=r"(r[o + 3]), "=r"(r[o + 4]), "=r"(r[o + 5]), "=r"(r[o + 6]), "=r"(r[o + 7])
-template <>
-__device__ __forceinline__ void tmem_store<32>(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
-      R8(0), R8(8), R8(16), R8(24)
-      : "memory");
-}
-template <>
-__device__ __forceinline__ void tmem_load<32>(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-      : W8(0), W8(8), W8(16), W8(24)
-      : "r"(taddr)
-      : "memory");
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-}
+#define R4(o) "r"(r[o]), "r"(r[o + 1]), "r"(r[o + 2]), "r"(r[o + 3])
+#define W4(o) "=r"(r[o]), "=r"(r[o + 1]), "=r"(r[o + 2]), "=r"(r[o + 3])
 template <>
 __device__ __forceinline__ void tmem_store<16>(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
       "%14,%15,%16};\n" ::"r"(taddr),
-      R8(0), R8(8)
+      R4(0), R4(4), R4(8), R4(12)
       : "memory");
 }
 template <>
@@ -136,110 +214,54 @@ __device__ __forceinline__ void tmem_load<16>(uint32_t taddr, uint32_t (&r)[16])
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
       "%15}, [%16];\n"
-      : W8(0), W8(8)
+      : W4(0), W4(4), W4(8), W4(12)
       : "r"(taddr)
       : "memory");
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
-#undef R8
-#undef W8
-
-// ---------------------------------------------------------------- DMMA path
-constexpr int DMMA_BK = 32;
-constexpr int DMMA_STAGES = 3;
-constexpr int KS_SMEM = 1024;  // group k lists up to this length are staged in smem
-
-// Shared-memory tiles are dense (rows of 256 B for A, 512 B for B) with the
-// 16-byte chunks of each 128-byte segment XOR-swizzled by (row & 3) << 1.
-// That makes the m16n8k16 fragment loads (4 rows x 2 chunks per half-warp)
-// hit 32 distinct banks, and keeps every 128-byte global line landing in one
-// 128-byte shared segment for the cp.async copies.
-__device__ __forceinline__ int swz(int row, int col) {  // element offset within a row
-  const int chunk = col >> 1;
-  return (((chunk & ~7) | ((chunk & 7) ^ ((row & 3) << 1))) << 1) | (col & 1);
+template <>
+__device__ __forceinline__ void tmem_store<4>(uint32_t taddr, const uint32_t (&r)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr), R4(0)
+               : "memory");
 }
+template <>
+__device__ __forceinline__ void tmem_load<4>(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : W4(0)
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+#undef R4
+#undef W4
 
-template <int TILE, int WM, int WN>
-struct DmmaCfg {
-  static constexpr int THREADS = 32 * WM * WN;
-  static constexpr int SA = DMMA_BK;      // A row length (doubles)
-  static constexpr int SB = TILE;         // B row length (doubles)
-  static constexpr int A_ELEMS = TILE * SA;
-  static constexpr int B_ELEMS = DMMA_BK * SB;
-  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-  static constexpr int WTM = TILE / WM;   // warp tile rows
-  static constexpr int WTN = TILE / WN;   // warp tile cols
-  static constexpr int MT = WTM / 16;     // m16 tiles per warp
-  static constexpr int NT = WTN / 8;      // n8 tiles per warp
-  static constexpr size_t SMEM = sizeof(double) * DMMA_STAGES * STAGE_ELEMS;
-  static constexpr int NREG = MT * NT * 4 * 2;           // b32 registers per accumulator set
-  static constexpr int TM_SLOTS = 4;                      // merge-stack slots kept in TMEM
-  static constexpr int SLOT_COLS = NREG * ((WM * WN + 3) / 4);
-  static constexpr int TM_COLS_RAW = TM_SLOTS * SLOT_COLS;
-  static constexpr int TM_COLS = TM_COLS_RAW <= 32 ? 32 : TM_COLS_RAW <= 64 ? 64
-                                 : TM_COLS_RAW <= 128 ? 128 : TM_COLS_RAW <= 256 ? 256 : 512;
-  static_assert(MT >= 1 && NT >= 1, "warp tile too small");
-  static_assert(NREG == 16 || NREG == 32, "TMEM spill width");
-  static_assert((TILE * DMMA_BK / 2) % THREADS == 0 && (DMMA_BK * TILE / 2) % THREADS == 0, "");
-};
-
-template <int TILE, int WM, int WN>
-__global__ void __launch_bounds__(32 * WM * WN, 2) leaf_dmma_kernel(LeafArgs args) {
-  using C = DmmaCfg<TILE, WM, WN>;
-  constexpr int QA = (TILE * DMMA_BK / 2) / C::THREADS;  // 16-B copies per thread, A stage
-  constexpr int QB = (DMMA_BK * TILE / 2) / C::THREADS;  // 16-B copies per thread, B stage
-  extern __shared__ __align__(16) double dsm[];
-  __shared__ int s_work;
-  __shared__ uint32_t s_ks[KS_SMEM];
+template <int TILE>
+__global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
+    leaf_dmma_ws_kernel(LeafArgs args, const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB) {
+  using C = WsCfg<TILE>;
+  extern __shared__ __align__(1024) unsigned char dsm_raw[];
+  // TMA 128-byte swizzle needs 1024-byte aligned tiles
+  double *dsm = reinterpret_cast<double *>(
+      (reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[C::STAGES], empty_bar[C::STAGES];
+  __shared__ StageInfo info[C::STAGES];
+  __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / WN, wn = warp % WN, g = lane >> 2, t = lane & 3;
   const int b = args.leaf;
-  const int kchunks = b / DMMA_BK;             // a power of two
-  const int kshift = __ffs(kchunks) - 1;
+  const int kchunks = b / DMMA_BK;
   const int subs_side = b / TILE;
   const int64_t N = args.N;
-  const double *__restrict__ A = (const double *)args.a;
-  const double *__restrict__ B = (const double *)args.b;
-  double *__restrict__ Cm = (double *)args.c;
+  const unsigned long long t_start = gtimer();
 
-  // ---- loop-invariant shared-memory fragment offsets (elements in a stage).
-  // Fragment rows of A are wm*WTM + mt*16 + 8h + g and rows of B are
-  // kk + 4*s4 + t, so the swizzle key (row & 3) is g & 3 for A and t for B.
-  const int a_row0 = (wm * C::WTM + g) * C::SA;
-  int a_col[2][4];
-#pragma unroll
-  for (int kq = 0; kq < 2; ++kq)
-#pragma unroll
-    for (int s4 = 0; s4 < 4; ++s4) a_col[kq][s4] = swz(g, 16 * kq + 4 * s4 + t);
-  int b_col[C::NT];
-#pragma unroll
-  for (int nt = 0; nt < C::NT; ++nt)
-    b_col[nt] = C::A_ELEMS + t * C::SB + swz(t, wn * C::WTN + nt * 8 + g);
-  // ---- loop-invariant copy slots (smem offset, global offset from the tile origin)
-  int sA[QA], sB[QB];
-  int64_t gA[QA], gB[QB];
-#pragma unroll
-  for (int q = 0; q < QA; ++q) {
-    const int e = tid + q * C::THREADS, r = e / (DMMA_BK / 2), c2 = e % (DMMA_BK / 2);
-    sA[q] = r * C::SA + swz(r, 2 * c2);
-    gA[q] = (int64_t)r * N + 2 * c2;
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init_l(&full_bar[s], 1);        // the producer's arrive (+ TMA transaction bytes)
+      mbar_init_l(&empty_bar[s], C::CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
-#pragma unroll
-  for (int q = 0; q < QB; ++q) {
-    const int e = tid + q * C::THREADS, r = e / (TILE / 2), c2 = e % (TILE / 2);
-    sB[q] = C::A_ELEMS + r * C::SB + swz(r, 2 * c2);
-    gB[q] = (int64_t)r * N + 2 * c2;
-  }
-
-  // Merge stack of the reference's tree order (see merge_level): pending
-  // left operands are keyed by tree level; the op levels on the stack are
-  // strictly decreasing from bottom to top, so they form a bit mask whose
-  // lowest set bit is the top.  The top value lives in registers; deeper
-  // ones in stk[level] (local memory), written back only when dirty.
-  double stk[MAXD][C::MT][C::NT][4];  // only slots >= TM_SLOTS (deep stacks)
-  double top[C::MT][C::NT][4];
-  __shared__ uint32_t s_tmem;
-  if (warp == 0) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      (unsigned)__cvta_generic_to_shared(&s_tmem)),
                  "n"(C::TM_COLS));
@@ -248,209 +270,252 @@ __global__ void __launch_bounds__(32 * WM * WN, 2) leaf_dmma_kernel(LeafArgs arg
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
-  const uint32_t t_my = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * C::NREG);
-  auto spill = [&](int slot) {
-    if (slot < C::TM_SLOTS) {
-      uint32_t r[C::NREG];
-#pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int x = ((mt * C::NT + nt) * 4 + q) * 2;
-            r[x] = (uint32_t)__double2loint(top[mt][nt][q]);
-            r[x + 1] = (uint32_t)__double2hiint(top[mt][nt][q]);
-          }
-      tmem_store<C::NREG>(t_my + slot * C::SLOT_COLS, r);
-    } else {
-#pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) stk[slot][mt][nt][q] = top[mt][nt][q];
-    }
-  };
-  auto reload = [&](int slot) {
-    if (slot < C::TM_SLOTS) {
-      uint32_t r[C::NREG];
-      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-      tmem_load<C::NREG>(t_my + slot * C::SLOT_COLS, r);
-#pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int x = ((mt * C::NT + nt) * 4 + q) * 2;
-            top[mt][nt][q] = __hiloint2double((int)r[x + 1], (int)r[x]);
-          }
-    } else {
-#pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) top[mt][nt][q] = stk[slot][mt][nt][q];
-    }
-  };
 
-  WorkItem w;
-  const unsigned long long t_start = gtimer();
   unsigned items = 0;
-  while (fetch_work(args, subs_side, &s_work, w)) {
-    ++items;
-    const int64_t nk = w.end - w.start;
-    const int64_t nsteps = nk * kchunks;
-    const bool ks_in_smem = nk <= KS_SMEM;
-    if (ks_in_smem)
-      for (int e = tid; e < nk; e += C::THREADS) s_ks[e] = args.ks[w.start + e];
-    __syncthreads();
-    const uint32_t *ks = ks_in_smem ? s_ks : args.ks + w.start;
-    const double *a_org = A + (int64_t(w.i) * b + w.si * TILE) * N;
-    const double *b_org = B + int64_t(w.j) * b + w.sj * TILE;
-
-    auto issue = [&](int64_t step) {
-      double *stg = dsm + (int)(step % DMMA_STAGES) * C::STAGE_ELEMS;
-      const int64_t kcol = int64_t(ks[step >> kshift]) * b + (int)(step & (kchunks - 1)) * DMMA_BK;
-      const double *asrc = a_org + kcol;
-      const double *bsrc = b_org + kcol * N;
-#pragma unroll
-      for (int q = 0; q < QA; ++q) cp_async16_l(stg + sA[q], asrc + gA[q]);
-#pragma unroll
-      for (int q = 0; q < QB; ++q) cp_async16_l(stg + sB[q], bsrc + gB[q]);
-    };
-
-#pragma unroll
-    for (int s = 0; s < DMMA_STAGES - 1; ++s) {
-      if (s < nsteps) issue(s);
-      cp_commit();
+  if (warp == 0) {
+    // ============================================================ producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmB) : "memory");
+      unsigned long long m = *args.n_codes;
+      if (m > args.capacity) m = args.capacity;
+      const int ng = (int)args.tc->num_groups;
+      const int subs = subs_side * subs_side;
+      int stage = 0;
+      unsigned phase = 0;
+      long long gstep = 0;  // ring position
+      auto acquire = [&]() {  // wait until the stage is free again
+        if (gstep >= C::STAGES) mbar_wait_l(&empty_bar[stage], phase ^ 1);
+      };
+      auto advance = [&]() {
+        ++gstep;
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      };
+      for (;;) {
+        const int item = (int)atomicAdd(&args.tc->gemm_ticket, 1ull);
+        if (item >= ng * subs) break;
+        ++items;
+        const int grp = item / subs, sub = item - grp * subs;
+        const int si = sub / subs_side, sj = sub - si * subs_side;
+        const int64_t start = args.group_starts[grp];
+        const int64_t end = grp + 1 < ng ? args.group_starts[grp + 1] : (int64_t)m;
+        const uint32_t gid = args.group_ids[grp];
+        const int64_t ci = gid / (uint64_t)args.nb, cj = gid - ci * args.nb;
+        const int arow0 = (int)(ci * b + si * TILE), bcol16 = (int)((cj * b + sj * TILE) >> 4);
+        const int64_t c_off = (int64_t)arow0 * N + cj * b + sj * TILE;
+        uint32_t k = args.ks[start];
+        for (int64_t s = start; s < end; ++s) {
+          const uint32_t knext = s + 1 < end ? args.ks[s + 1] : 0u;
+          for (int kc = 0; kc < kchunks; ++kc) {
+            acquire();
+            double *stg = dsm + stage * C::STAGE_ELEMS;
+            const int kcol = (int)(k * b + kc * DMMA_BK);
+            int flags = 0, h = 31;
+            if (kc == kchunks - 1) {
+              flags = STG_MERGE;
+              if (s + 1 < end) h = merge_level(k, knext);
+              else flags |= STG_END;
+            }
+            info[stage].flags = flags;
+            info[stage].h = h;
+            info[stage].c_off = c_off;
+            mbar_arrive_expect_tx_l(&full_bar[stage], (unsigned)(C::STAGE_ELEMS * sizeof(double)));
+            tma_load_3d(stg, &tmA, 0, kcol >> 4, arow0, &full_bar[stage]);
+            tma_load_3d(stg + C::A_ELEMS, &tmB, 0, bcol16, kcol, &full_bar[stage]);
+            advance();
+          }
+          k = knext;
+        }
+      }
+      // termination marker
+      acquire();
+      info[stage].flags = STG_DONE;
+      info[stage].h = 31;
+      info[stage].c_off = 0;
+      mbar_arrive_l(&full_bar[stage]);
     }
-
-    double acc[C::MT][C::NT][4];
+    __syncwarp();
+  } else {
+    // ============================================================ consumers
+    const int cw = warp - 1;
+    const int wm = cw / C::WN, wn = cw % C::WN, g = lane >> 2, t = lane & 3;
+    double *__restrict__ Cm = (double *)args.c;
+    // loop-invariant fragment offsets (elements) in the swizzled stage
+    int a_o[2][4], b_o[2][4][C::NT8];
 #pragma unroll
-    for (int mt = 0; mt < C::MT; ++mt)
+    for (int kq = 0; kq < 2; ++kq)
 #pragma unroll
-      for (int nt = 0; nt < C::NT; ++nt)
+      for (int s4 = 0; s4 < 4; ++s4) {
+        a_o[kq][s4] = a_off_tma(wm * C::WTM + g, 16 * kq + 4 * s4 + t);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.0;
-    uint32_t pending = 0;    // levels with a pending left operand
-    bool top_dirty = false;  // top[] not yet written to stk[ctz(pending)]
-
-    for (int64_t step = 0; step < nsteps; ++step) {
-      cp_wait<DMMA_STAGES - 2>();
-      __syncthreads();
-      if (step + DMMA_STAGES - 1 < nsteps) issue(step + DMMA_STAGES - 1);
-      cp_commit();
-      const double *stg = dsm + (int)(step % DMMA_STAGES) * C::STAGE_ELEMS;
-      const double *Ab = stg + a_row0;
+        for (int nt = 0; nt < C::NT8; ++nt)
+          b_o[kq][s4][nt] = C::A_ELEMS + b_off_tma<TILE>(16 * kq + 4 * s4 + t, wn * C::WTN + nt * 8 + g);
+      }
+    const uint32_t t_my = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) +
+                          (uint32_t)(((cw >> 2) & 3) * C::NREG);
+    double stk[MAXD][C::NACC];  // only slots >= TM_SLOTS (deep stacks)
+    double acc[C::NACC], top[C::NACC];
+#pragma unroll
+    for (int x = 0; x < C::NACC; ++x) acc[x] = 0.0;
+    uint32_t pending = 0;
+    bool top_dirty = false;
+    auto spill = [&](int slot) {
+      if (slot < C::TM_SLOTS) {
+        uint32_t r[C::NREG];
+#pragma unroll
+        for (int x = 0; x < C::NACC; ++x) {
+          r[2 * x] = (uint32_t)__double2loint(top[x]);
+          r[2 * x + 1] = (uint32_t)__double2hiint(top[x]);
+        }
+        tmem_store<C::NREG>(t_my + slot * C::SLOT_COLS, r);
+      } else {
+#pragma unroll
+        for (int x = 0; x < C::NACC; ++x) stk[slot][x] = top[x];
+      }
+    };
+    auto reload = [&](int slot) {
+      if (slot < C::TM_SLOTS) {
+        uint32_t r[C::NREG];
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tmem_load<C::NREG>(t_my + slot * C::SLOT_COLS, r);
+#pragma unroll
+        for (int x = 0; x < C::NACC; ++x) top[x] = __hiloint2double((int)r[2 * x + 1], (int)r[2 * x]);
+      } else {
+#pragma unroll
+        for (int x = 0; x < C::NACC; ++x) top[x] = stk[slot][x];
+      }
+    };
+    int stage = 0;
+    unsigned phase = 0;
+    for (;;) {
+      mbar_wait_l(&full_bar[stage], phase);
+      const StageInfo si = info[stage];
+      if (si.flags & STG_DONE) break;
+      const double *stg = dsm + stage * C::STAGE_ELEMS;
 #pragma unroll
       for (int kq = 0; kq < 2; ++kq) {
-        // fragments of four k4 steps; every accumulator sees its inner index
-        // in ascending order (k4 steps in order, each DMMA ascending inside)
-        double af[C::MT][2][4], bf[C::NT][4];
+        double af[C::MT8][4], bf[C::NT8][4];
 #pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt)
+        for (int mt = 0; mt < C::MT8; ++mt)
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
+          for (int s4 = 0; s4 < 4; ++s4) af[mt][s4] = stg[mt * 8 * DMMA_BK + a_o[kq][s4]];
 #pragma unroll
-            for (int s4 = 0; s4 < 4; ++s4)
-              af[mt][h][s4] = Ab[(mt * 16 + 8 * h) * C::SA + a_col[kq][s4]];
+        for (int nt = 0; nt < C::NT8; ++nt)
 #pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-          for (int s4 = 0; s4 < 4; ++s4)
-            bf[nt][s4] = stg[(16 * kq + 4 * s4) * C::SB + b_col[nt]];
+          for (int s4 = 0; s4 < 4; ++s4) bf[nt][s4] = stg[b_o[kq][s4][nt]];
 #pragma unroll
         for (int s4 = 0; s4 < 4; ++s4)
 #pragma unroll
-          for (int mt = 0; mt < C::MT; ++mt)
+          for (int mt = 0; mt < C::MT8; ++mt)
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (int nt = 0; nt < C::NT; ++nt)
-                dmma884(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1], af[mt][h][s4], bf[nt][s4]);
+            for (int nt = 0; nt < C::NT8; ++nt)
+              dmma884(acc[(mt * C::NT8 + nt) * 2], acc[(mt * C::NT8 + nt) * 2 + 1], af[mt][s4],
+                      bf[nt][s4]);
       }
-      if ((int)(step & (kchunks - 1)) == kchunks - 1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_l(&empty_bar[stage]);
+      if (++stage == C::STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+      if (si.flags & STG_MERGE) {
         // P_k complete: merge in the reference's tree order
-        const int64_t s = step >> kshift;
-        const uint32_t k = ks[s];
-        int h = 31;
-        if (s + 1 < nk) h = merge_level(k, ks[s + 1]);
+        const int h = si.h;
         while (pending && (__ffs(pending) - 1) < h) {
 #pragma unroll
-          for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) acc[mt][nt][q] = __dadd_rn(top[mt][nt][q], acc[mt][nt][q]);
+          for (int x = 0; x < C::NACC; ++x) acc[x] = __dadd_rn(top[x], acc[x]);
           pending &= pending - 1;
           if (pending) {  // the new top sits at stack position popcount - 1
             reload(__popc(pending) - 1);
             top_dirty = false;
           }
         }
-        if (s + 1 < nk) {
+        if (!(si.flags & STG_END)) {
           if (pending && top_dirty) spill(__popc(pending) - 1);
 #pragma unroll
-          for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                top[mt][nt][q] = acc[mt][nt][q];
-                acc[mt][nt][q] = 0.0;
-              }
+          for (int x = 0; x < C::NACC; ++x) {
+            top[x] = acc[x];
+            acc[x] = 0.0;
+          }
           top_dirty = true;
           pending |= 1u << h;
+        } else {
+          // item complete: the C tile of this warp
+          double *crow = Cm + si.c_off + (int64_t)(wm * C::WTM + g) * N + wn * C::WTN + 2 * t;
+#pragma unroll
+          for (int mt = 0; mt < C::MT8; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < C::NT8; ++nt) {
+              const int x = (mt * C::NT8 + nt) * 2;
+              *reinterpret_cast<double2 *>(crow + (int64_t)(mt * 8) * N + nt * 8) =
+                  make_double2(acc[x], acc[x + 1]);
+            }
+#pragma unroll
+          for (int x = 0; x < C::NACC; ++x) acc[x] = 0.0;
+          pending = 0;
+          top_dirty = false;
         }
       }
     }
-    cp_wait<0>();
-    // epilogue: C block rows/cols of this sub-tile
-    double *crow = Cm + (int64_t(w.i) * b + w.si * TILE + wm * C::WTM + g) * N +
-                   int64_t(w.j) * b + w.sj * TILE + wn * C::WTN + 2 * t;
-#pragma unroll
-    for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2)
-          *reinterpret_cast<double2 *>(crow + (int64_t)(mt * 16 + 8 * h2) * N + nt * 8) =
-              make_double2(acc[mt][nt][2 * h2], acc[mt][nt][2 * h2 + 1]);
-    __syncthreads();
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
-  if (warp == 0)
+  if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
                  "n"(C::TM_COLS));
-  if (args.timeline && threadIdx.x == 0) {
+  if (args.timeline && tid == 0) {
     args.timeline[3 * blockIdx.x] = t_start;
     args.timeline[3 * blockIdx.x + 1] = gtimer();
     args.timeline[3 * blockIdx.x + 2] = items;
   }
 }
 
-template <int TILE, int WM, int WN>
-static int launch_dmma(const LeafArgs &args, int num_sms, cudaStream_t st) {
-  using C = DmmaCfg<TILE, WM, WN>;
-  auto kern = leaf_dmma_kernel<TILE, WM, WN>;
-  SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)C::SMEM));
-  int per_sm = 0;
-  SPAMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM));
-  if (getenv("SPAMM_GEMM_TIMELINE")) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, kern);
-    fprintf(stderr, "[gemm launch] per_sm=%d regs=%d static_smem=%zu dyn=%zu maxthreads=%d\n", per_sm,
-            fa.numRegs, fa.sharedSizeBytes, C::SMEM, fa.maxThreadsPerBlock);
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
   }
-  // The occupancy query reports 1 CTA/SM for kernels that allocate TMEM; two
-  // fit (registers, shared memory and 2 x TM_COLS <= 512 TMEM columns), and
-  // the persistent ticket loop is correct for any grid size.
-  kern<<<num_sms * (per_sm > 2 ? per_sm : 2), C::THREADS, C::SMEM, st>>>(args);
+  return fn;
+}
+
+// 3-D view {16, N/16, N} of a padded N x N f64 operand: box {16, box1, box2}.
+static int make_operand_map(CUtensorMap *map, const void *base, int64_t N, int box1, int box2) {
+  auto enc = tensor_map_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return SPAMM_ERR_CUDA;
+  }
+  cuuint64_t dims[3] = {16, (cuuint64_t)(N / 16), (cuuint64_t)N};
+  cuuint64_t strides[2] = {128, (cuuint64_t)(N * 8)};
+  cuuint32_t box[3] = {16, (cuuint32_t)box1, (cuuint32_t)box2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void *>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return SPAMM_ERR_CUDA;
+  }
+  return SPAMM_OK;
+}
+
+template <int TILE>
+static int launch_dmma_ws(const LeafArgs &args, int num_sms, cudaStream_t st) {
+  using C = WsCfg<TILE>;
+  CUtensorMap ma, mb;
+  SPAMM_TRY(make_operand_map(&ma, args.a, args.N, 2, TILE));             // A: 32 k x TILE rows
+  SPAMM_TRY(make_operand_map(&mb, args.b, args.N, TILE / 16, DMMA_BK));  // B: TILE n x 32 k
+  auto kern = leaf_dmma_ws_kernel<TILE>;
+  SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(C::SMEM + 1024)));
+  kern<<<num_sms, C::THREADS, C::SMEM + 1024, st>>>(args, ma, mb);
   return SPAMM_OK;
 }
 
@@ -524,8 +589,8 @@ __global__ void __launch_bounds__(SIMT_THREADS) leaf_simt_kernel(LeafArgs args) 
 
 int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches) {
   if (dtype == SPAMM_DTYPE_F64 && args.leaf >= 32) {
-    if (args.leaf == 32) SPAMM_TRY((launch_dmma<32, 2, 2>(args, num_sms, st)));
-    else SPAMM_TRY((launch_dmma<64, 2, 4>(args, num_sms, st)));
+    if (args.leaf == 32) SPAMM_TRY((launch_dmma_ws<32>(args, num_sms, st)));
+    else SPAMM_TRY((launch_dmma_ws<64>(args, num_sms, st)));
   } else if (dtype == SPAMM_DTYPE_F64) {
     leaf_simt_kernel<double><<<num_sms * 2, SIMT_THREADS, 0, st>>>(args);
   } else {
