@@ -15,7 +15,8 @@ for r in rows[hi + 1:]:
     if len(r) <= vi:
         continue
     v = float(r[vi].replace(",", ""))
-    v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[ui], 1.0)
+    v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+          "second": 1e6, "s": 1e6}.get(r[ui].strip(), 1.0)
     name = r[ki].split("(")[0][:70]
     a = agg.setdefault(name, [0, 0.0])
     a[0] += 1
