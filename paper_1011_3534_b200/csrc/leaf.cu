@@ -140,6 +140,16 @@ __device__ __forceinline__ void tma_load_3d(void *smem, const CUtensorMap *map, 
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_5d(void *smem, const CUtensorMap *map, int x0, int x1, int x2,
+                                            int x3, int x4, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4, %5, %6}], [%7];\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+      "l"((uint64_t)map), "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(x4),
+      "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
 // Tiles land in shared memory as TMA boxes of 128-byte lines with the
 // hardware 128-byte swizzle (16-byte chunk ^= line & 7).  A (TILE x 32) is
 // loaded as the box {16, 2, TILE}: line = 2*row + col/16, so the four rows a
@@ -153,6 +163,13 @@ __device__ __forceinline__ int a_off_tma(int r, int c) {  // elements
 template <int TILE>
 __device__ __forceinline__ int b_off_tma(int k, int n) {
   const int L = (TILE / 16) * k + (n >> 4), ch = (n & 15) >> 1;
+  return L * 16 + ((ch ^ (L & 7)) << 1) + (n & 1);
+}
+// B for TILE = 64 as the 5-D box {16 n, 2 (n/16 & 1), 4 (k & 3), 2 (n/32), 8 (k/4)}:
+// line = (n/16 & 1) + 2 (k & 3) + 8 (n/32) + 16 (k/4), so the XOR key of the
+// four k rows of a half-warp is c + 2t -- conflict-free like A.
+__device__ __forceinline__ int b_off_tma5(int k, int n) {
+  const int L = ((n >> 4) & 1) + 2 * (k & 3) + 8 * (n >> 5) + 16 * (k >> 2), ch = (n & 15) >> 1;
   return L * 16 + ((ch ^ (L & 7)) << 1) + (n & 1);
 }
 
@@ -324,7 +341,10 @@ __global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
             info[stage].c_off = c_off;
             mbar_arrive_expect_tx_l(&full_bar[stage], (unsigned)(C::STAGE_ELEMS * sizeof(double)));
             tma_load_3d(stg, &tmA, 0, kcol >> 4, arow0, &full_bar[stage]);
-            tma_load_3d(stg + C::A_ELEMS, &tmB, 0, bcol16, kcol, &full_bar[stage]);
+            if (TILE == 64 && args.b_map5)
+              tma_load_5d(stg + C::A_ELEMS, &tmB, 0, 0, 0, bcol16 >> 1, kcol >> 2, &full_bar[stage]);
+            else
+              tma_load_3d(stg + C::A_ELEMS, &tmB, 0, bcol16, kcol, &full_bar[stage]);
             advance();
           }
           k = knext;
@@ -352,7 +372,9 @@ __global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
         a_o[kq][s4] = a_off_tma(wm * C::WTM + g, 16 * kq + 4 * s4 + t);
 #pragma unroll
         for (int nt = 0; nt < C::NT8; ++nt)
-          b_o[kq][s4][nt] = C::A_ELEMS + b_off_tma<TILE>(16 * kq + 4 * s4 + t, wn * C::WTN + nt * 8 + g);
+          b_o[kq][s4][nt] = C::A_ELEMS + (TILE == 64 && args.b_map5
+                                              ? b_off_tma5(16 * kq + 4 * s4 + t, wn * C::WTN + nt * 8 + g)
+                                              : b_off_tma<TILE>(16 * kq + 4 * s4 + t, wn * C::WTN + nt * 8 + g));
       }
     const uint32_t t_my = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) +
                           (uint32_t)(((cw >> 2) & 3) * C::NREG);
@@ -506,12 +528,28 @@ static int make_operand_map(CUtensorMap *map, const void *base, int64_t N, int b
   return SPAMM_OK;
 }
 
+// 5-D view of B for TILE = 64 (see b_off_tma5); its strides are not
+// monotonic, so a driver that rejects the encoding falls back to the 3-D box.
+static bool make_b_map5(CUtensorMap *map, const void *base, int64_t N) {
+  auto enc = tensor_map_encoder();
+  if (!enc || N < 64) return false;
+  cuuint64_t dims[5] = {16, 2, 4, (cuuint64_t)(N / 32), (cuuint64_t)(N / 4)};
+  cuuint64_t strides[4] = {128, (cuuint64_t)(N * 8), 256, (cuuint64_t)(4 * N * 8)};
+  cuuint32_t box[5] = {16, 2, 4, 2, 8};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void *>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int TILE>
-static int launch_dmma_ws(const LeafArgs &args, int num_sms, cudaStream_t st) {
+static int launch_dmma_ws(LeafArgs args, int num_sms, cudaStream_t st) {
   using C = WsCfg<TILE>;
   CUtensorMap ma, mb;
   SPAMM_TRY(make_operand_map(&ma, args.a, args.N, 2, TILE));             // A: 32 k x TILE rows
-  SPAMM_TRY(make_operand_map(&mb, args.b, args.N, TILE / 16, DMMA_BK));  // B: TILE n x 32 k
+  args.b_map5 = TILE == 64 && make_b_map5(&mb, args.b, args.N);
+  if (!args.b_map5)
+    SPAMM_TRY(make_operand_map(&mb, args.b, args.N, TILE / 16, DMMA_BK));  // B: TILE n x 32 k
   auto kern = leaf_dmma_ws_kernel<TILE>;
   SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(C::SMEM + 1024)));

@@ -17,6 +17,7 @@ struct LeafArgs {
   const uint32_t *group_starts;       // first triple of each group
   TraverseCounters *tc;               // num_groups + work ticket
   unsigned long long *timeline;       // optional: per-CTA [start, end, items] (%globaltimer)
+  int b_map5;                         // B streamed as the conflict-free 5-D TMA box
 };
 
 int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches);
