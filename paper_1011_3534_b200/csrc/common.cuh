@@ -51,26 +51,24 @@ inline int depth_for(int64_t n, int32_t leaf) {
   return d;
 }
 
-// ----------------------------------------------------------------- Morton
-// A product-space triple (i, j, k) at tier t is kept as its Morton code:
-// bits (3s+2, 3s+1, 3s) hold bit s of (i, j, k).  Children of code c are
-// 8c + (di<<2 | dj<<1 | dk), which is exactly the reference's (di,dj,dk)
-// expansion order 000..111 (multiply.py:35-37), so a tier's candidate list
-// stays in the reference's order.
-__host__ __device__ inline uint64_t compact3(uint64_t x) {
-  x &= 0x1249249249249249ull;
-  x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ull;
-  x = (x ^ (x >> 4)) & 0x100f00f00f00f00full;
-  x = (x ^ (x >> 8)) & 0x1f0000ff0000ffull;
-  x = (x ^ (x >> 16)) & 0x1f00000000ffffull;
-  x = (x ^ (x >> 32)) & 0x1fffffull;
-  return x;
+// ------------------------------------------------------- triple packing
+// A product-space triple (i, j, k) at any tier is kept packed as
+// i << 42 | j << 21 | k (21 bits each, depth <= 21).  Its children are
+// (2i+di, 2j+dj, 2k+dk) for (di,dj,dk) = 000..111 -- the reference's
+// expansion order (multiply.py:35-37) -- and a tier's candidate list is
+// generated parent by parent, so every list stays in the reference's order.
+constexpr uint64_t TRIPLE_MASK = (uint64_t(1) << 21) - 1;
+__host__ __device__ inline uint64_t pack_triple(uint64_t i, uint64_t j, uint64_t k) {
+  return (i << 42) | (j << 21) | k;
 }
-__host__ __device__ inline void morton_decode(uint64_t code, uint32_t &i, uint32_t &j,
-                                              uint32_t &k) {
-  i = (uint32_t)compact3(code >> 2);
-  j = (uint32_t)compact3(code >> 1);
-  k = (uint32_t)compact3(code);
+__host__ __device__ inline void unpack_triple(uint64_t p, uint32_t &i, uint32_t &j, uint32_t &k) {
+  i = (uint32_t)(p >> 42);
+  j = (uint32_t)((p >> 21) & TRIPLE_MASK);
+  k = (uint32_t)(p & TRIPLE_MASK);
+}
+// child q = di<<2 | dj<<1 | dk of packed parent p
+__host__ __device__ inline uint64_t child_triple(uint64_t p, unsigned q) {
+  return (p << 1) + ((uint64_t)(q >> 2) << 42) + ((uint64_t)((q >> 1) & 1) << 21) + (q & 1);
 }
 
 // ------------------------------------------------------------ device context
@@ -89,7 +87,7 @@ struct DeviceContext {
   cudaEvent_t fork = nullptr, join = nullptr;
   cudaEvent_t ev[8] = {};
   std::mutex mu;
-  Scratch cull_codes[2];  // ping-pong survivor lists (u64 Morton codes)
+  Scratch cull_codes[2];  // ping-pong survivor lists (packed i,j,k)
   Scratch pruned_codes;   // pruned codes, all tiers (u64)
   Scratch pruned_vals;    // pruned norm products, all tiers (f64)
   Scratch tile_status;    // decoupled look-back state

@@ -27,7 +27,7 @@
 
 namespace spamm {
 
-constexpr int MAXD = 22;  // deepest merge stack (depth <= 21 with 63-bit Morton codes)
+constexpr int MAXD = 22;  // deepest merge stack (depth <= 21: 21-bit packed coordinates)
 
 __device__ __forceinline__ void cp_async16_l(void *smem, const void *gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -553,6 +553,7 @@ static int launch_dmma_ws(LeafArgs args, int num_sms, cudaStream_t st) {
   auto kern = leaf_dmma_ws_kernel<TILE>;
   SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(C::SMEM + 1024)));
+  SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   kern<<<num_sms, C::THREADS, C::SMEM + 1024, st>>>(args, ma, mb);
   return SPAMM_OK;
 }

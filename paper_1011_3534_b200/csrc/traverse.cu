@@ -13,8 +13,9 @@
 //   active = alive & ~pruned
 // and active triples expand to their 8 children in (di,dj,dk) = 000..111
 // order (:207-212).  Candidates are never materialised: candidate c of tier
-// t is child (c & 7) of survivor (c >> 3) of tier t-1, every survivor kept
-// as its Morton code, so each tier's list stays in the reference's order and
+// t is child (c & 7) of survivor (c >> 3) of tier t-1 (survivors kept as
+// packed (i, j, k), see common.cuh), so each tier's list stays in the
+// reference's order and
 // the pruned list (budget, boxes) comes out in exactly the reference's order.
 //
 // Phases of the kernel (grid barriers between them):
@@ -30,6 +31,7 @@
 //           scatter of k, and a per-bucket bitonic sort -> the reference's
 //           lexsorted (i, j, k) list, bucket by bucket.
 #include <cuda/atomic>
+#include <cstdlib>
 
 #include "scan.cuh"
 #include "traverse.cuh"
@@ -122,10 +124,10 @@ __device__ void process_tile(const TraverseArgs &a, TvShared &sh, int tier, unsi
     if (c < n_cand) {
       const uint64_t pc = tier == 0 ? 0ull : (!grid_mode ? sh.u.top.list[(tier + 1) & 1][c >> 3]
                                                          : prev[c >> 3]);
-      const uint64_t cd = tier == 0 ? 0ull : pc * 8ull + (c & 7ull);
+      const uint64_t cd = tier == 0 ? 0ull : child_triple(pc, (unsigned)(c & 7ull));
       code[q] = cd;
       uint32_t i, j, k;
-      morton_decode(cd, i, j, k);
+      unpack_triple(cd, i, j, k);
       const int64_t r0 = int64_t(i) << shift, r1 = int64_t(i + 1) << shift;
       const bool intersects = r1 > a.row_lo && r0 < a.row_hi;
       const bool owned = r0 >= a.row_lo && r0 < a.row_hi;
@@ -366,6 +368,13 @@ __device__ void warp_bitonic(uint32_t *x, int n) {
   }
 }
 
+__device__ void clear_status_part(unsigned long long *st, unsigned long long n, unsigned part,
+                                  unsigned parts) {
+  for (unsigned long long i = (unsigned long long)part * TV_THREADS + threadIdx.x; i < n;
+       i += (unsigned long long)parts * TV_THREADS)
+    st[i] = 0ull;
+}
+
 __device__ void clear_status(unsigned long long *st, unsigned long long n) {
   for (unsigned long long i = (unsigned long long)blockIdx.x * TV_THREADS + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * TV_THREADS)
@@ -390,8 +399,11 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
 
   // ---------------- prefix (CTA 0) || clear the buckets (other CTAs)
   if (blockIdx.x == 0) {
+    const unsigned long long t_entry = globaltimer();
     for (int x = threadIdx.x; x < (int)(sizeof(TraverseCounters) / 8); x += TV_THREADS)
       reinterpret_cast<unsigned long long *>(tc)[x] = 0ull;
+    __syncthreads();
+    if (threadIdx.x == 0) tc->phase_ns[15] = t_entry;
     // one parallel load of the pyramid tops; the prefix tiers then hit smem
     const int top_entries = (int)level_offset((depth < PREFIX_LEVELS ? depth : PREFIX_LEVELS) + 1);
     for (int x = threadIdx.x; x < top_entries; x += TV_THREADS) {
@@ -408,7 +420,10 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
     for (; t <= depth; ++t) {
       unsigned long long n_cand = 1;
       if (t > 0) n_cand = 8ull * (sh.prev_active < a.capacity ? sh.prev_active : a.capacity);
-      if (n_cand > PREFIX_MAX_CAND || (t > 0 && sh.prev_active > PREFIX_LIST)) break;
+      // the prefix serialises tiles on one CTA: only worth it while the
+      // pyramid level is cached in shared memory and the tier is small
+      if (t > PREFIX_LEVELS || n_cand > PREFIX_MAX_CAND || (t > 0 && sh.prev_active > PREFIX_LIST))
+        break;
       if (threadIdx.x == 0) {
         sh.run_act = sh.run_prn = 0;
         sh.tier_cnt[0] = sh.tier_cnt[1] = sh.tier_cnt[2] = sh.tier_cnt[3] = 0;
@@ -467,18 +482,56 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && depth >= t0)
     tc->dirty_tiles[depth & 1] = prev_tiles;
 
-  // ---------------- budget (one CTA per tier) + bucket histogram
   unsigned long long m = tc->n_active[depth];
   if (m > a.capacity) m = a.capacity;
   const uint64_t *leaf_codes = a.codes[depth & 1];
-  for (unsigned long long p = (unsigned long long)blockIdx.x * TV_THREADS + threadIdx.x; p < m;
-       p += (unsigned long long)nblocks * TV_THREADS) {
+  const int nbud = depth + 1;  // CTAs 0..depth compute the budget, then leave
+
+  // ---------------- omitted_budget: one CTA per tier, concurrent with the
+  // grouping below (those CTAs never meet the later barriers); the last tier
+  // to finish adds the tier sums in tier order, as the reference's Python
+  // float does.
+  if ((int)blockIdx.x < nbud) {
+    const int t = blockIdx.x;
+    const unsigned long long np_ = tc->n_pruned[t];
+    double s = 0.0;
+    if (np_ && tc->pruned_base[t] + np_ <= a.pruned_capacity) {
+      const double *src = a.pruned_vals + tc->pruned_base[t];
+      if (np_ <= PW_SMEM_VALS) {
+        for (unsigned x = threadIdx.x; x < np_; x += TV_THREADS) sh.u.pw.vals[x] = src[x];
+        __syncthreads();
+        src = sh.u.pw.vals;
+      }
+      s = pairwise_cta(sh, src, (long long)np_);
+    }
+    if (threadIdx.x == 0) {
+      tc->tier_budget[t] = s;
+      __threadfence();
+      if (atomicAdd(&tc->budgets_done, 1u) == (unsigned)depth) {
+        __threadfence();
+        tc->phase_ns[12] = globaltimer();
+        double b = 0.0;
+        for (int u = 0; u <= depth; ++u)
+          if (tc->n_pruned[u]) b = __dadd_rn(b, ((volatile double *)tc->tier_budget)[u]);
+        tc->budget = b;
+      }
+      atomicMax(&tc->phase_ns[13], globaltimer());
+    }
+    return;
+  }
+  const unsigned gi = blockIdx.x - nbud, gn = nblocks - nbud;  // grouping CTAs
+#define GPHASE(ix) \
+  if (gi == 0 && threadIdx.x == 0) tc->phase_ns[ix] = globaltimer();
+
+  // ---------------- bucket histogram
+  for (unsigned long long p = (unsigned long long)gi * TV_THREADS + threadIdx.x; p < m;
+       p += (unsigned long long)gn * TV_THREADS) {
     uint32_t i, j, k;
-    morton_decode(leaf_codes[p], i, j, k);
+    unpack_triple(leaf_codes[p], i, j, k);
     atomicAdd(&a.counts[int64_t(i) * a.nb + j], 1u);
   }
-  grid_sync(a.barrier, nblocks);
-  PHASE(8)
+  grid_sync(a.barrier, gn);
+  GPHASE(8)
 
   // ---------------- bucket scan: offsets + non-empty block list
   {
@@ -524,56 +577,23 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
       __syncthreads();
     }
   }
-  grid_sync(a.barrier, nblocks);
-  PHASE(9)
+  grid_sync(a.barrier, gn);
+  GPHASE(9)
 
   // ---------------- scatter k into the buckets; clear look-back state
-  for (unsigned long long p = (unsigned long long)blockIdx.x * TV_THREADS + threadIdx.x; p < m;
-       p += (unsigned long long)nblocks * TV_THREADS) {
+  for (unsigned long long p = (unsigned long long)gi * TV_THREADS + threadIdx.x; p < m;
+       p += (unsigned long long)gn * TV_THREADS) {
     uint32_t i, j, k;
-    morton_decode(leaf_codes[p], i, j, k);
+    unpack_triple(leaf_codes[p], i, j, k);
     const int64_t gid = int64_t(i) * a.nb + j;
     const unsigned slot = atomicSub(&a.counts[gid], 1u) - 1u;
     a.ks[a.offsets[gid] + slot] = k;
   }
-  if (depth >= t0) {
-    clear_status(a.status[depth & 1], tc->dirty_tiles[depth & 1]);
-    if (depth > t0) {
-      // tier depth-1's array was cleared during tier depth
-    }
-  }
-  clear_status(a.status[2], (G + TV_TILE - 1) / TV_TILE);
-  grid_sync(a.barrier, nblocks);
-  PHASE(10)
-
-  // ---------------- omitted_budget: one CTA per tier, off the critical path
-  // (nothing after it waits at a barrier); the last tier to finish adds the
-  // tier sums in tier order, as the reference's Python float does.
-  for (int t = blockIdx.x; t <= depth; t += nblocks) {
-    const unsigned long long np_ = tc->n_pruned[t];
-    double s = 0.0;
-    if (np_ && tc->pruned_base[t] + np_ <= a.pruned_capacity) {
-      const double *src = a.pruned_vals + tc->pruned_base[t];
-      if (np_ <= PW_SMEM_VALS) {
-        for (unsigned x = threadIdx.x; x < np_; x += TV_THREADS) sh.u.pw.vals[x] = src[x];
-        __syncthreads();
-        src = sh.u.pw.vals;
-      }
-      s = pairwise_cta(sh, src, (long long)np_);
-    }
-    if (threadIdx.x == 0) {
-      tc->tier_budget[t] = s;
-      __threadfence();
-      if (atomicAdd(&tc->budgets_done, 1u) == (unsigned)depth) {
-        __threadfence();
-        double b = 0.0;
-        for (int u = 0; u <= depth; ++u)
-          if (tc->n_pruned[u]) b = __dadd_rn(b, ((volatile double *)tc->tier_budget)[u]);
-        tc->budget = b;
-      }
-    }
-    __syncthreads();
-  }
+  // (tier depth-1's status array was already cleared during tier depth)
+  if (depth >= t0) clear_status_part(a.status[depth & 1], tc->dirty_tiles[depth & 1], gi, gn);
+  clear_status_part(a.status[2], (G + TV_TILE - 1) / TV_TILE, gi, gn);
+  grid_sync(a.barrier, gn);
+  GPHASE(10)
 
   // ---------------- sort every bucket's k list ascending (one warp per bucket)
   {
@@ -604,12 +624,18 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
       }
     }
   }
-  PHASE(11)
+  GPHASE(11)
+  if (threadIdx.x == 0) atomicMax(&tc->phase_ns[13], globaltimer());  // last CTA out
+#undef GPHASE
 }
 
 int launch_traverse(const TraverseArgs &args, int num_sms, cudaStream_t st) {
   static int per_sm = 0;
   if (per_sm == 0) {
+    // every library kernel asks for the maximum shared-memory carveout, so
+    // consecutive launches never pay for an L1/shared reconfiguration
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(traverse_kernel,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     SPAMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel,
                                                                  TV_THREADS, 0));
     if (per_sm < 1) {

@@ -32,7 +32,7 @@ struct TraverseArgs {
   double tau_tier[MAX_TIERS];
   const double *nrm_a, *nrm_b;      // rn(sqrt(norm_sq)) pyramids (concatenated levels)
   const uint8_t *occ_a, *occ_b;
-  uint64_t *codes[2];               // ping-pong survivor lists (Morton codes)
+  uint64_t *codes[2];               // ping-pong survivor lists (packed i,j,k)
   unsigned long long capacity;      // items per survivor list
   double *pruned_vals;              // all tiers, reference order
   uint64_t *pruned_codes;

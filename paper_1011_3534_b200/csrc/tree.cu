@@ -450,6 +450,7 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
       const size_t smem = (size_t)S * LT * K1_LEAF_STRIDE;
       auto kern = leaf_norm_staged_kernel<T, S, LT>;
       SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       kern<<<(unsigned)((n_leaves + LT - 1) / LT), K1_THREADS, smem, st>>>(
           (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count);
     } else {
@@ -457,6 +458,7 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
       const size_t smem = (size_t)S * LT * K1_LEAF_STRIDE;
       auto kern = leaf_norm_staged_kernel<T, S, LT>;
       SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       kern<<<(unsigned)((n_leaves + LT - 1) / LT), K1_THREADS, smem, st>>>(
           (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count);
     }
@@ -476,6 +478,12 @@ int build_pyramid_async(spamm_tree *t, cudaStream_t st, int *launches, const uin
   if (t->dtype == SPAMM_DTYPE_F64) SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap));
   else SPAMM_TRY(launch_leaf_norms<float>(t, st, list, list_count, list_cap));
   if (launches) ++*launches;
+  static bool carve = false;
+  if (!carve) {
+    cudaFuncSetAttribute(pyramid_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(norm_sqrt_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    carve = true;
+  }
   int from = t->depth;
   while (from > 0) {
     const int L = from < 5 ? from : 5;
