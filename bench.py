@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu/context")
+    p.add_argument("--dist", action="store_true",
+                   help="use the torch.distributed (NCCL) path even at world size 1")
     return p.parse_args()
 
 
@@ -190,14 +192,15 @@ def run_b200(args, cfg_name):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     sp.set_device(local)
-    if world > 1:
+    use_dist = world > 1 or args.dist
+    if use_dist:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     a_host, _, leaf, taus = workloads.make_config(cfg_name)
     n = a_host.shape[0]
     from paper_1011_3534_b200 import distributed as spd
 
-    shard = spd.row_shard(rank, world, n, leaf) if world > 1 else None
+    shard = spd.row_shard(rank, world, n, leaf) if use_dist else None
     a = sp.from_dense(a_host, leaf_size=leaf)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -219,7 +222,7 @@ def run_b200(args, cfg_name):
 
     for _ in range(args.warmup):
         one_step()
-    if world > 1:
+    if use_dist:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     tot_f = tot_ms = tot_gemm = 0.0
@@ -228,7 +231,7 @@ def run_b200(args, cfg_name):
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             f, ms, gemm, la, per_tau = one_step()
-            if world > 1:
+            if use_dist:
                 t = torch.tensor([ms], dtype=torch.float64, device="cuda")
                 torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
                 ms = float(t.item())
@@ -241,7 +244,7 @@ def run_b200(args, cfg_name):
             launches += la
             per_tau_all.append(per_tau)
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         torch.distributed.barrier()
     clocks = clk.summary()
     value = tot_f / (tot_ms * 1e-3) / 1e12
@@ -273,7 +276,8 @@ def run_b200(args, cfg_name):
         "config": {"workload": f"{cfg_name}: n={n} leaf={leaf} A=B=sym(u*0.95^|i-j|), "
                                f"tau sweep {list(taus)}, one spamm per tau per step",
                    "l2": "flushed (256 MiB write) before every multiply",
-                   "parallelism": f"C block-row shards x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"C block-row shards x{world} (no data-path collective)"
+                                   if use_dist else "single GPU"),
                    "per_tau": table},
         "roofline": roofline,
         "clocks": clocks,
@@ -296,32 +300,8 @@ def run_b200(args, cfg_name):
             "ms": dg, "tflops": 2.0 * n ** 3 / (dg * 1e-3) / 1e12}
         del at
 
-    if not args.no_e2e and not args.profile and world == 1:
-        pin_a = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
-        pin_a[...] = a_host
-        pin_c = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
-        for it in range(args.warmup + args.steps):
-            if it == args.warmup:
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                e_f = 0.0
-            at = sp.from_dense(pin_a, leaf_size=leaf)
-            f = 0.0
-            for tau in taus:
-                c, st = sp.spamm(at, at, sp.SpammConfig(tau=tau))
-                c.to_dense(out=pin_c)
-                f += leaf_flops(leaf, st.leaf_matmuls)
-                del c
-            del at
-            if it >= args.warmup:
-                e_f += f
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        line["e2e"] = {"value": e_f / el / 1e12, "unit": "TFLOP/s",
-                       "h2d_bytes_per_step": n * n * 8,
-                       "d2h_bytes_per_step": len(taus) * n * n * 8,
-                       "ms_per_step": el / args.steps * 1e3,
-                       "timing": "host wall clock around synchronous public-API calls"}
+    if not args.no_e2e and not args.profile:
+        line["e2e"] = e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist)
 
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
         cv, sec, cores = cpu_reference(a_host, leaf, taus, 1, 1)
@@ -331,8 +311,71 @@ def run_b200(args, cfg_name):
                                 "ms_per_step": sec * 1e3}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         torch.distributed.destroy_process_group()
+
+
+def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist):
+    """The same metric through the public API with host buffers.
+
+    Every step: pinned host A -> from_dense (H2D + K1 pyramid), one spamm per
+    tau, and the product back to pinned host memory.  With row shards each
+    rank multiplies its C block rows and reads back only its own row band
+    (bands partition C); wall time is the max over ranks."""
+    import torch
+
+    n = a_host.shape[0]
+    pin_a = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+    pin_a[...] = a_host
+    if shard is None:
+        r0, r1 = 0, n
+    else:
+        r0, r1 = min(shard[0] * leaf, n), min(shard[1] * leaf, n)
+    pin_c = torch.empty((max(r1 - r0, 1), n), dtype=torch.float64, pin_memory=True)
+    t0 = None
+    e_f = 0.0
+    for it in range(args.warmup + args.steps):
+        if it == args.warmup:
+            torch.cuda.synchronize()
+            if use_dist:
+                torch.distributed.barrier()
+            t0 = time.perf_counter()
+        at = sp.from_dense(pin_a, leaf_size=leaf)
+        f = 0.0
+        for tau in taus:
+            if shard is None:
+                c, st = sp.spamm(at, at, sp.SpammConfig(tau=tau))
+                c.to_dense(out=pin_c.numpy())
+            else:
+                from paper_1011_3534_b200 import distributed as spd
+                c, st, _ = sp.spamm_detailed(at, at, sp.SpammConfig(tau=tau), rows=shard)
+                if r1 > r0:
+                    pin_c[: r1 - r0].copy_(spd.tree_storage(c)[r0:r1, :n])
+            f += leaf_flops(leaf, st.leaf_matmuls)
+            del c
+        del at
+        if it >= args.warmup:
+            e_f += f
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    d2h = len(taus) * (r1 - r0) * n * 8
+    if use_dist:
+        t = torch.tensor([el, e_f], dtype=torch.float64, device="cuda")
+        mx = t[:1].clone()
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(t[1:])
+        el, e_f = float(mx.item()), float(t[1].item())
+        d2h = len(taus) * n * n * 8  # all bands together
+    return {"value": e_f / el / 1e12, "unit": "TFLOP/s",
+            "h2d_bytes_per_step": n * n * 8 * (dist_world() if use_dist else 1),
+            "d2h_bytes_per_step": d2h,
+            "ms_per_step": el / args.steps * 1e3,
+            "timing": "host wall clock around synchronous public-API calls (max over ranks)"}
+
+
+def dist_world():
+    import torch.distributed as dist
+    return dist.get_world_size()
 
 
 def main():

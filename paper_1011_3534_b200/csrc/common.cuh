@@ -95,6 +95,7 @@ struct DeviceContext {
   Scratch keys[2];        // bucket counts/offsets, grouped inner indices
   Scratch group_starts;   // non-empty C blocks and their first triple
   Scratch reduce_tmp;     // misc reduction scratch
+  Scratch pyr_tickets;    // pyramid hand-off counters (self-resetting, zero at rest)
   size_t cull_capacity = 0;   // survivor capacity per ping-pong buffer (items)
   size_t pruned_capacity = 0; // pruned capacity (items, all tiers)
   void *host_pinned = nullptr;  // small pinned staging for counters

@@ -27,8 +27,8 @@ namespace spamm {
 
 int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out);
 void free_tree_async(spamm_tree *t, cudaStream_t st);
-int build_pyramid_async(spamm_tree *t, cudaStream_t st, int *launches, const uint32_t *list,
-                        const unsigned *list_count, int64_t list_cap);
+int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
+                        const uint32_t *list, const unsigned *list_count, int64_t list_cap);
 int finish_tree(DeviceContext *ctx, spamm_tree *t);
 
 static int check_conformable(const spamm_tree *a, const spamm_tree *b) {
@@ -188,7 +188,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[3], st));
 
     // ------------------------------------------- C's tree (multiply.py:220)
-    if ((rc = build_pyramid_async(c, st, &launches, ta.group_ids, &dtc->num_groups, (int64_t)gcap)))
+    if ((rc = build_pyramid_async(ctx, c, st, &launches, ta.group_ids, &dtc->num_groups, (int64_t)gcap)))
       break;
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
     SPAMM_CUDA_BREAK(cudaMemcpyAsync(hc, dtc, sizeof(TraverseCounters), cudaMemcpyDeviceToHost, st));

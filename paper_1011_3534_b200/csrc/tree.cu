@@ -374,62 +374,122 @@ __global__ void leaf_norm_direct_kernel(T *__restrict__ padded, int64_t N, int32
   if (!nz && bits) canonicalise_leaf<T>(padded, N, b, bi, bj);
 }
 
-// Pyramid: each CTA reduces a 2^L x 2^L tile of level `from` through L levels,
-// parent = ((c11 + c12) + c21) + c22 (quadtree.py:90-92), occupancy OR
-// (quadtree.py:137-138).  Launched in passes of L <= 5 levels.
+// Pyramid (one launch for every level): the levels are cut into passes of
+// L <= 5 levels; a pass-p CTA reduces one 2^L x 2^L tile of its input level
+// through L levels, parent = ((c11 + c12) + c21) + c22 (quadtree.py:90-92),
+// occupancy OR (quadtree.py:137-138), and writes nrm = rn(sqrt(nsq)) of every
+// node it produces (the factors of the reference's norm product,
+// multiply.py:185, rounded exactly like np.sqrt).  The last of the 4^L'
+// children of a pass-(p+1) tile to finish goes on to reduce that tile
+// (ticket counters that reset themselves), so the whole pyramid is one
+// launch whatever the depth.  Pass-0 CTAs also take the sqrt of the leaf
+// level.
 constexpr int PYR_THREADS = 256;
-__global__ void __launch_bounds__(PYR_THREADS) pyramid_kernel(double *__restrict__ nsq,
-                                                              uint8_t *__restrict__ occ, int from,
-                                                              int L) {
-  __shared__ double s_n[1024];
-  __shared__ uint8_t s_o[1024];
-  const int tiles_per_side = 1 << (from - L);
-  const int ti = blockIdx.x / tiles_per_side, tj = blockIdx.x % tiles_per_side;
-  int side = 1 << L;
-  const int64_t fine_side = int64_t(1) << from;
-  const double *lvl = nsq + level_offset(from);
-  const uint8_t *olvl = occ + level_offset(from);
-  for (int e = threadIdx.x; e < side * side; e += PYR_THREADS) {
-    const int r = e / side, c = e % side;
-    const int64_t g = (int64_t(ti) * side + r) * fine_side + int64_t(tj) * side + c;
-    s_n[e] = lvl[g];
-    s_o[e] = olvl[g];
+constexpr int PYR_MAX_PASSES = 6;
+
+struct PyrPlan {
+  int passes;
+  int from[PYR_MAX_PASSES], L[PYR_MAX_PASSES];
+  int64_t cnt_off[PYR_MAX_PASSES];  // ticket counters of pass p's tiles (p >= 1)
+  int64_t n_counters;
+};
+
+static PyrPlan pyramid_plan(int depth) {
+  PyrPlan pl{};
+  int from = depth;
+  int64_t off = 0;
+  while (from > 0) {
+    const int L = from < 5 ? from : 5;
+    pl.from[pl.passes] = from;
+    pl.L[pl.passes] = L;
+    pl.cnt_off[pl.passes] = off;
+    if (pl.passes > 0) off += int64_t(1) << (2 * (from - L));
+    ++pl.passes;
+    from -= L;
   }
-  __syncthreads();
-  for (int k = from - 1; k >= from - L; --k) {
-    const int ps = side >> 1;
-    const int64_t coarse_side = int64_t(1) << k;
-    double *clvl = nsq + level_offset(k);
-    uint8_t *oclvl = occ + level_offset(k);
-    double v[4];
-    uint8_t o[4];
-    int cnt = 0;
-    for (int e = threadIdx.x; e < ps * ps; e += PYR_THREADS, ++cnt) {
-      const int r = e / ps, c = e % ps;
-      const int f0 = (2 * r) * side + 2 * c, f1 = f0 + side;
-      v[cnt] = __dadd_rn(__dadd_rn(__dadd_rn(s_n[f0], s_n[f0 + 1]), s_n[f1]), s_n[f1 + 1]);
-      o[cnt] = s_o[f0] | s_o[f0 + 1] | s_o[f1] | s_o[f1 + 1];
-      const int64_t g = (int64_t(ti) * ps + r) * coarse_side + int64_t(tj) * ps + c;
-      clvl[g] = v[cnt];
-      oclvl[g] = o[cnt];
-    }
-    __syncthreads();
-    cnt = 0;
-    for (int e = threadIdx.x; e < ps * ps; e += PYR_THREADS, ++cnt) {
-      s_n[e] = v[cnt];
-      s_o[e] = o[cnt];
-    }
-    __syncthreads();
-    side = ps;
-  }
+  pl.n_counters = off;
+  return pl;
 }
 
-// rn(sqrt(norm_sq)) of every node: the factors of the reference's norm
-// product (multiply.py:185), correctly rounded exactly like np.sqrt.
-__global__ void norm_sqrt_kernel(const double *__restrict__ nsq, double *__restrict__ nrm, int64_t P) {
-  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < P;
-       x += (int64_t)gridDim.x * blockDim.x)
-    nrm[x] = __dsqrt_rn(nsq[x]);
+__global__ void __launch_bounds__(PYR_THREADS) pyramid_fused_kernel(double *__restrict__ nsq,
+                                                                    uint8_t *__restrict__ occ,
+                                                                    double *__restrict__ nrm,
+                                                                    PyrPlan pl,
+                                                                    unsigned *__restrict__ tickets) {
+  __shared__ double s_n[1024];
+  __shared__ uint8_t s_o[1024];
+  __shared__ int s_last;
+  if (pl.passes == 0) {  // depth 0: the single leaf is the root
+    if (threadIdx.x == 0) nrm[0] = __dsqrt_rn(nsq[0]);
+    return;
+  }
+  int64_t tile = blockIdx.x;
+  for (int p = 0; p < pl.passes; ++p) {
+    const int from = pl.from[p], L = pl.L[p];
+    const int tiles_per_side = 1 << (from - L);
+    const int ti = (int)(tile / tiles_per_side), tj = (int)(tile % tiles_per_side);
+    int side = 1 << L;
+    const int64_t fine_side = int64_t(1) << from;
+    const double *lvl = nsq + level_offset(from);
+    const uint8_t *olvl = occ + level_offset(from);
+    double *nlvl = nrm + level_offset(from);
+    for (int e = threadIdx.x; e < side * side; e += PYR_THREADS) {
+      const int r = e / side, c = e % side;
+      const int64_t g = (int64_t(ti) * side + r) * fine_side + int64_t(tj) * side + c;
+      // L1-bypassing loads: later passes read what other CTAs wrote
+      const double x = __ldcg(lvl + g);
+      s_n[e] = x;
+      s_o[e] = __ldcg(olvl + g);
+      if (p == 0) nlvl[g] = __dsqrt_rn(x);
+    }
+    __syncthreads();
+    for (int k = from - 1; k >= from - L; --k) {
+      const int ps = side >> 1;
+      const int64_t coarse_side = int64_t(1) << k;
+      double *clvl = nsq + level_offset(k);
+      uint8_t *oclvl = occ + level_offset(k);
+      double *nclvl = nrm + level_offset(k);
+      double v[4];
+      uint8_t o[4];
+      int cnt = 0;
+      for (int e = threadIdx.x; e < ps * ps; e += PYR_THREADS, ++cnt) {
+        const int r = e / ps, c = e % ps;
+        const int f0 = (2 * r) * side + 2 * c, f1 = f0 + side;
+        v[cnt] = __dadd_rn(__dadd_rn(__dadd_rn(s_n[f0], s_n[f0 + 1]), s_n[f1]), s_n[f1 + 1]);
+        o[cnt] = s_o[f0] | s_o[f0 + 1] | s_o[f1] | s_o[f1 + 1];
+        const int64_t g = (int64_t(ti) * ps + r) * coarse_side + int64_t(tj) * ps + c;
+        clvl[g] = v[cnt];
+        oclvl[g] = o[cnt];
+        nclvl[g] = __dsqrt_rn(v[cnt]);
+      }
+      __syncthreads();
+      cnt = 0;
+      for (int e = threadIdx.x; e < ps * ps; e += PYR_THREADS, ++cnt) {
+        s_n[e] = v[cnt];
+        s_o[e] = o[cnt];
+      }
+      __syncthreads();
+      side = ps;
+    }
+    if (p + 1 == pl.passes) break;
+    // hand the parent tile to the last of its children
+    const int Ln = pl.L[p + 1];
+    const int parent_side = 1 << (pl.from[p + 1] - Ln);
+    const int64_t parent = int64_t(ti >> Ln) * parent_side + (tj >> Ln);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned *tk = tickets + pl.cnt_off[p + 1] + parent;
+      const unsigned children = 1u << (2 * Ln);
+      const unsigned old = atomicAdd(tk, 1u);
+      s_last = old == children - 1;
+      if (s_last) *tk = 0;  // ready for the next build
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    tile = parent;
+  }
 }
 
 template <typename T>
@@ -472,29 +532,27 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
 }
 
 // Rebuild the whole pyramid of `t` from its padded storage (canonicalising
-// all-zero leaves in place).  Stream-ordered; no host sync.
-int build_pyramid_async(spamm_tree *t, cudaStream_t st, int *launches, const uint32_t *list,
-                        const unsigned *list_count, int64_t list_cap) {
+// all-zero leaves in place).  Stream-ordered; no host sync; two launches.
+int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
+                        const uint32_t *list, const unsigned *list_count, int64_t list_cap) {
   if (t->dtype == SPAMM_DTYPE_F64) SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap));
   else SPAMM_TRY(launch_leaf_norms<float>(t, st, list, list_count, list_cap));
   if (launches) ++*launches;
   static bool carve = false;
   if (!carve) {
-    cudaFuncSetAttribute(pyramid_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(norm_sqrt_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(pyramid_fused_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     carve = true;
   }
-  int from = t->depth;
-  while (from > 0) {
-    const int L = from < 5 ? from : 5;
-    const int64_t tiles = int64_t(1) << (2 * (from - L));
-    pyramid_kernel<<<(unsigned)tiles, PYR_THREADS, 0, st>>>(t->nsq, t->occ, from, L);
-    SPAMM_CUDA_TRY(cudaGetLastError());
-    if (launches) ++*launches;
-    from -= L;
+  const PyrPlan pl = pyramid_plan(t->depth);
+  if (pl.passes == 0) {
+    pyramid_fused_kernel<<<1, 32, 0, st>>>(t->nsq, t->occ, t->nrm, pl, nullptr);
+  } else {
+    // tickets start (and are left) at zero
+    const size_t need = sizeof(unsigned) * (size_t)std::max<int64_t>(pl.n_counters, 1);
+    SPAMM_TRY(ensure_scratch(ctx->pyr_tickets, need, st, /*zeroed=*/true));
+    pyramid_fused_kernel<<<(unsigned)(int64_t(1) << (2 * (pl.from[0] - pl.L[0]))), PYR_THREADS, 0,
+                           st>>>(t->nsq, t->occ, t->nrm, pl, (unsigned *)ctx->pyr_tickets.ptr);
   }
-  const int64_t P = pyramid_size(t->depth);
-  norm_sqrt_kernel<<<(unsigned)std::min<int64_t>((P + 255) / 256, 4096), 256, 0, st>>>(t->nsq, t->nrm, P);
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (launches) ++*launches;
   return SPAMM_OK;
@@ -577,7 +635,7 @@ static int tree_from(const void *src, bool src_on_host, int64_t n, int64_t ld, i
                           src_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                           ctx->stream);
     if (e != cudaSuccess) { set_error("copy: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-    rc = build_pyramid_async(t, ctx->stream, nullptr, nullptr, nullptr, 0);
+    rc = build_pyramid_async(ctx, t, ctx->stream, nullptr, nullptr, nullptr, 0);
     if (rc) break;
     rc = finish_tree(ctx, t);
   } while (0);
