@@ -57,6 +57,10 @@ extern "C" {
 #define SPAMM_COUNT_STATS 0x2u    /* maintain the ProductStats counters       */
 #define SPAMM_TIER_TAU_DECAY 0x4u /* prune tier t against tau / 8**t          */
 #define SPAMM_KEEP_TRIPLES 0x8u   /* keep the retained leaf (i,j,k) list      */
+/* Traversal kernel selection (results are identical either way): shallow
+ * trees (depth <= 7) default to the dense single-pass kernel; this flag
+ * forces the tiered breadth-first kernel (testing / comparison). */
+#define SPAMM_TIERED_TRAVERSAL 0x10u
 
 typedef struct spamm_tree spamm_tree;
 typedef struct spamm_product spamm_product;

@@ -27,6 +27,7 @@ COLLECT_BOXES = 0x1
 COUNT_STATS = 0x2
 TIER_TAU_DECAY = 0x4
 KEEP_TRIPLES = 0x8
+TIERED_TRAVERSAL = 0x10
 
 # every symbol include/spamm_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (

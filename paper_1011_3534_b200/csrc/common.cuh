@@ -91,11 +91,16 @@ struct DeviceContext {
   Scratch pruned_codes;   // pruned codes, all tiers (u64)
   Scratch pruned_vals;    // pruned norm products, all tiers (f64)
   Scratch tile_status;    // decoupled look-back state
-  Scratch counters;       // device counters (TraverseCounters) + grid barrier
+  Scratch counters;       // two alternating TraverseCounters sets
   Scratch keys[2];        // bucket counts/offsets, grouped inner indices
   Scratch group_starts;   // non-empty C blocks and their first triple
   Scratch reduce_tmp;     // misc reduction scratch
   Scratch pyr_tickets;    // pyramid hand-off counters (self-resetting, zero at rest)
+  Scratch dn_masks;       // dense traversal: pruned bitmasks (zero at rest)
+  Scratch dn_retained;    // dense traversal: retained leaf bitmask
+  Scratch dn_np;          // dense traversal: leaf-tier pruned products
+  Scratch dn_status;      // dense traversal: look-back state (zero at rest)
+  int counter_parity = 0; // which traversal counter set the next call uses
   size_t cull_capacity = 0;   // survivor capacity per ping-pong buffer (items)
   size_t pruned_capacity = 0; // pruned capacity (items, all tiers)
   void *host_pinned = nullptr;  // small pinned staging for counters

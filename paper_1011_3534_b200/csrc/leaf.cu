@@ -69,7 +69,7 @@ __device__ __forceinline__ bool fetch_work(const LeafArgs &args, int subs_side, 
   if (threadIdx.x == 0) *s_work = (int)atomicAdd(&args.tc->gemm_ticket, 1ull);
   __syncthreads();
   const int item = *s_work;
-  const int ng = (int)args.tc->num_groups;
+  const int ng = args.tc->overflow ? 0 : (int)args.tc->num_groups;  // overflow: result discarded, re-run
   const int subs = subs_side * subs_side;
   if (item >= ng * subs) return false;
   const int grp = item / subs, sub = item - grp * subs;
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
       asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmB) : "memory");
       unsigned long long m = *args.n_codes;
       if (m > args.capacity) m = args.capacity;
-      const int ng = (int)args.tc->num_groups;
+      const int ng = args.tc->overflow ? 0 : (int)args.tc->num_groups;  // overflow: result discarded, re-run
       const int subs = subs_side * subs_side;
       int stage = 0;
       unsigned phase = 0;

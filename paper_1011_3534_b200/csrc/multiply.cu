@@ -111,11 +111,24 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     if ((rc = ensure_scratch(ctx->tile_status,
                              sizeof(unsigned long long) * (2 * st_tier + st_grp), st, true)))
       break;
-    if ((rc = ensure_scratch(ctx->counters, sizeof(TraverseCounters) + 64, st, true))) break;
+    // two counter sets, alternating between calls (see TraverseCounters)
+    if ((rc = ensure_scratch(ctx->counters, 2 * sizeof(TraverseCounters), st, true))) break;
+    const bool dense = dense_traversal_ok(depth) && !(flags & SPAMM_TIERED_TRAVERSAL);
+    if (dense) {
+      if ((rc = ensure_scratch(ctx->dn_masks, sizeof(uint32_t) * dense_mask_words(depth), st, true)))
+        break;
+      if ((rc = ensure_scratch(ctx->dn_retained, sizeof(uint32_t) * dense_retained_words(depth), st)))
+        break;
+      if ((rc = ensure_scratch(ctx->dn_np, sizeof(double) * dense_np_entries(depth), st))) break;
+      if ((rc = ensure_scratch(ctx->dn_status,
+                               sizeof(unsigned long long) * dense_status_entries(depth, nb), st, true)))
+        break;
+    }
     if ((rc = ensure_scratch(ctx->keys[0], 2 * sizeof(uint32_t) * G, st))) break;  // counts, offsets
     if ((rc = ensure_scratch(ctx->group_starts, 2 * sizeof(uint32_t) * gcap, st))) break;
     if ((rc = ensure_scratch(ctx->keys[1], sizeof(uint32_t) * cap, st))) break;  // ks
-    TraverseCounters *dtc = (TraverseCounters *)ctx->counters.ptr;
+    TraverseCounters *tcs = (TraverseCounters *)ctx->counters.ptr;
+    TraverseCounters *dtc = tcs + ctx->counter_parity;
 
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->fork, st));
     // ------------------------------------------- K2 traversal + grouping
@@ -146,10 +159,27 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     ta.group_ids = (uint32_t *)ctx->group_starts.ptr;
     ta.group_starts = ta.group_ids + gcap;
     ta.ks = (uint32_t *)ctx->keys[1].ptr;
-    ta.barrier = (unsigned *)((char *)ctx->counters.ptr + sizeof(TraverseCounters));
+    ta.tc_clear = tcs + (ctx->counter_parity ^ 1);
+    if (dense) {
+      ta.dn_masks = (uint32_t *)ctx->dn_masks.ptr;
+      ta.dn_retained = (uint32_t *)ctx->dn_retained.ptr;
+      ta.dn_np = (double *)ctx->dn_np.ptr;
+      ta.dn_status = (unsigned long long *)ctx->dn_status.ptr;
+      ta.dn_status_q = dense_pruned_tiles(depth);
+    }
+    static const bool tv_timeline = getenv("SPAMM_TRAVERSE_TIMELINE") != nullptr;
+    static unsigned long long *tv_tl = nullptr;
+    if (tv_timeline) {
+      if (!tv_tl) SPAMM_CUDA_BREAK(cudaMalloc(&tv_tl, sizeof(unsigned long long) * 4 * 4096));
+      SPAMM_CUDA_BREAK(cudaMemsetAsync(tv_tl, 0, sizeof(unsigned long long) * 4 * 4096, st));
+      ta.timeline = tv_tl;
+    }
     // device timing starts at the first kernel (host-side setup excluded)
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[0], st));
-    if ((rc = launch_traverse(ta, ctx->num_sms, st))) break;
+    if ((rc = dense ? launch_traverse_dense(ta, ctx->num_sms, st)
+                    : launch_traverse(ta, ctx->num_sms, st)))
+      break;
+    ctx->counter_parity ^= 1;
     ++launches;
     // C's zero fill runs on the side stream, under the traversal (issued
     // after the cooperative launch so it cannot delay its residency)
@@ -194,6 +224,27 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     SPAMM_CUDA_BREAK(cudaMemcpyAsync(hc, dtc, sizeof(TraverseCounters), cudaMemcpyDeviceToHost, st));
     SPAMM_CUDA_BREAK(cudaMemcpyAsync(&c->root_norm_sq, c->nsq, sizeof(double), cudaMemcpyDeviceToHost, st));
     SPAMM_CUDA_BREAK(cudaStreamSynchronize(st));
+    if (tv_timeline && ta.timeline) {
+      std::vector<unsigned long long> tl(4 * 4096);
+      cudaMemcpy(tl.data(), tv_tl, sizeof(unsigned long long) * 4 * 4096, cudaMemcpyDeviceToHost);
+      unsigned long long t0 = ~0ull;
+      int n = 0;
+      for (int q = 0; q < 4096; ++q)
+        if (tl[4 * q]) { t0 = std::min(t0, tl[4 * q]); ++n; }
+      fprintf(stderr, "[traverse timeline] ctas=%d", n);
+      for (int half = 0; half < 2; ++half) {
+        fprintf(stderr, half ? "\n   Q:" : "\n   P:");
+        for (int f = 0; f < 4; ++f) {
+          std::vector<double> v;
+          for (int q = half ? n / 2 : 0; q < (half ? n : n / 2); ++q)
+            if (tl[4 * q] && tl[4 * q + f]) v.push_back((tl[4 * q + f] - t0) * 1e-3);
+          std::sort(v.begin(), v.end());
+          if (!v.empty())
+            fprintf(stderr, " | s%d %.1f/%.1f/%.1f", f, v[0], v[v.size() / 2], v.back());
+        }
+      }
+      fprintf(stderr, "\n");
+    }
     if (!hc->overflow) break;
     unsigned long long need = 0, pneed = 0;
     for (int t = 0; t <= depth; ++t) {

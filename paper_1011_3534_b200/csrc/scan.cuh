@@ -25,6 +25,9 @@ __device__ __forceinline__ unsigned unpack_b(unsigned long long v) { return (uns
 // Called by all 32 lanes of one warp.  Publishes the tile's aggregate,
 // resolves its exclusive prefix from predecessors and publishes the
 // inclusive prefix.  Returns the exclusive prefix (packed) on every lane.
+// The status words carry their own values, so relaxed (L1-bypassing) loads
+// and stores suffice: no fence, and no acquire -- which on sm_100 invalidates
+// the SM's whole L1 on every poll and stalls co-resident CTAs.
 __device__ __forceinline__ unsigned long long lookback_exclusive(unsigned long long *status,
                                                                  unsigned long long tile,
                                                                  unsigned long long tile_total) {
@@ -33,13 +36,13 @@ __device__ __forceinline__ unsigned long long lookback_exclusive(unsigned long l
   if (tile == 0) {
     if (lane == 0) {
       cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[0]);
-      st.store(ST_PREFIX | tile_total, cuda::memory_order_release);
+      st.store(ST_PREFIX | tile_total, cuda::memory_order_relaxed);
     }
     return 0;
   }
   if (lane == 0) {
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[tile]);
-    st.store(ST_AGG | tile_total, cuda::memory_order_release);
+    st.store(ST_AGG | tile_total, cuda::memory_order_relaxed);
   }
   long long pred = (long long)tile - 1;
   for (;;) {
@@ -47,9 +50,11 @@ __device__ __forceinline__ unsigned long long lookback_exclusive(unsigned long l
     unsigned long long s = ST_PREFIX;  // virtual zero prefix before tile 0
     if (idx >= 0) {
       cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[idx]);
-      do {
-        s = st.load(cuda::memory_order_acquire);
-      } while ((s & ST_FLAGS) == 0);
+      for (;;) {
+        s = st.load(cuda::memory_order_relaxed);
+        if (s & ST_FLAGS) break;
+        __nanosleep(20);
+      }
     }
     const unsigned pmask = __ballot_sync(0xffffffffu, (s & ST_FLAGS) == ST_PREFIX);
     const int stop = pmask ? __ffs(pmask) - 1 : 31;
@@ -62,7 +67,7 @@ __device__ __forceinline__ unsigned long long lookback_exclusive(unsigned long l
   }
   if (lane == 0) {
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[tile]);
-    st.store(ST_PREFIX | (excl + tile_total), cuda::memory_order_release);
+    st.store(ST_PREFIX | (excl + tile_total), cuda::memory_order_relaxed);
   }
   return excl;
 }

@@ -58,38 +58,43 @@ struct TvShared {
   unsigned long long tier_cnt[4];       // prefix: active, pruned, skip, alive of the tier
   unsigned long long prev_active;       // prefix: survivors of the previous tier
   unsigned warp_item[TV_THREADS / 32];
-  int pw_lvl[24];
-  int pw_nlevels, pw_count;
   union {
     struct {  // prefix: the top of both pyramids + the small survivor lists
       double nrm_a[PREFIX_ENTRIES], nrm_b[PREFIX_ENTRIES];
       uint64_t list[2][PREFIX_LIST];
       uint8_t occ_a[PREFIX_ENTRIES], occ_b[PREFIX_ENTRIES];
     } top;
-    struct {  // budget
-      long long start[PW_NODES], len[PW_NODES];
-      int left[PW_NODES];
-      double val[PW_NODES];
+    struct {  // budget: the values, then numpy's recursion tree (heap order)
       double vals[PW_SMEM_VALS];
+      double val[2 * PW_NODES];
+      uint8_t split[2 * PW_NODES];
     } pw;
     uint32_t keys[TV_THREADS / 32][SORT_WARP_KEYS];  // sort
+    uint16_t qks[16384];                              // dense grouping: a tile's k lists
   } u;
 };
 
 // ------------------------------------------------------------- grid barrier
-__device__ void grid_sync(unsigned *bar, unsigned nblocks) {
+// One arrival counter per barrier group, zero at the start of the call (it
+// lives in the call's counter set, cleared by the previous call) and never
+// reset: the k-th barrier of a group of n CTAs completes when the counter
+// reaches k*n.  One release-add per CTA, relaxed polling of the same word
+// and one acquire fence (measured ~1.2 us on B200 for 296 CTAs vs 2.5 us for
+// a count + generation pair with full fences; tools/gridsync_probe.cu).
+__device__ void grid_sync(unsigned *ctr, unsigned nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    cuda::atomic_ref<unsigned, cuda::thread_scope_device> cnt(bar[0]), gen(bar[1]);
-    const unsigned g = gen.load(cuda::memory_order_acquire);
-    __threadfence();
-    if (cnt.fetch_add(1u, cuda::memory_order_acq_rel) == nblocks - 1) {
-      cnt.store(0u, cuda::memory_order_relaxed);
-      gen.fetch_add(1u, cuda::memory_order_release);
-    } else {
-      while (gen.load(cuda::memory_order_acquire) == g) __nanosleep(32);
+    unsigned old;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+    const unsigned target = (old / nblocks + 1) * nblocks;
+    unsigned cur;
+    for (;;) {  // relaxed polling (an acquire per poll would invalidate L1 each time),
+                // backed off so waiting CTAs do not flood the counter's L2 slice
+      asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
+      if (cur >= target) break;
+      __nanosleep(100);
     }
-    __threadfence();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }
@@ -284,45 +289,65 @@ __device__ double pw_serial(const double *a, long long n) {
   return ret;
 }
 
-// One CTA: the recursion expanded breadth-first to <= PW_NODES nodes, the
-// frontier summed in parallel, the tree folded back level by level.
-__device__ double pairwise_cta(TvShared &sh, const double *a, long long n) {
-  if (threadIdx.x == 0) {
-    sh.u.pw.start[0] = 0;
-    sh.u.pw.len[0] = n;
-    sh.u.pw.left[0] = -1;
-    int count = 1, lb = 0, le = 1, nl = 0;
-    sh.pw_lvl[nl++] = 0;
-    for (;;) {
-      int add = 0;
-      for (int x = lb; x < le; ++x) add += sh.u.pw.len[x] > 128 ? 2 : 0;
-      if (add == 0 || count + add > PW_NODES || nl >= 22) break;
-      for (int x = lb; x < le; ++x) {
-        if (sh.u.pw.len[x] > 128) {
-          long long n2 = sh.u.pw.len[x] / 2;
-          n2 -= n2 % 8;
-          sh.u.pw.left[x] = count;
-          sh.u.pw.start[count] = sh.u.pw.start[x]; sh.u.pw.len[count] = n2; sh.u.pw.left[count] = -1; ++count;
-          sh.u.pw.start[count] = sh.u.pw.start[x] + n2; sh.u.pw.len[count] = sh.u.pw.len[x] - n2;
-          sh.u.pw.left[count] = -1; ++count;
-        }
-      }
-      lb = le;
-      le = count;
-      sh.pw_lvl[nl++] = lb;
+// Copy n doubles global -> shared, eight loads in flight per thread.
+template <int NT>
+__device__ __forceinline__ void stage_values(double *dst, const double *__restrict__ src,
+                                             unsigned long long n) {
+  for (unsigned long long x0 = threadIdx.x; x0 < n; x0 += 8ull * NT) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const unsigned long long x = x0 + (unsigned long long)u * NT;
+      v[u] = x < n ? __ldcg(src + x) : 0.0;
     }
-    sh.pw_lvl[nl] = count;
-    sh.pw_nlevels = nl;
-    sh.pw_count = count;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const unsigned long long x = x0 + (unsigned long long)u * NT;
+      if (x < n) dst[x] = v[u];
+    }
+  }
+}
+
+// One CTA: numpy's recursion tree, PW_LOG levels deep at most, built in
+// parallel -- thread p follows the left/right path spelled by its bits, the
+// first thread under each node records whether the node splits (n > 128)
+// and the leaves are summed serially (numpy's 8-accumulator blocks) -- then
+// folded back level by level, left + right, exactly as the recursion adds.
+constexpr int PW_LOG = 9;  // 2^PW_LOG = PW_NODES leaves at most
+__device__ double pairwise_cta(TvShared &sh, const double *a, long long n) {
+  int L = 0;
+  for (long long m = n; m > 128 && L < PW_LOG; m = (m + 1) / 2) ++L;
+  const int paths = 1 << L;
+  for (int p = threadIdx.x; p < paths; p += TV_THREADS) {
+    long long st = 0, len = n;
+    int d = 0;
+    for (; d < L && len > 128; ++d) {
+      sh.u.pw.split[(1 << d) - 1 + (p >> (L - d))] = 1;  // every thread below writes the same 1
+      long long n2 = len / 2;
+      n2 -= n2 % 8;
+      if ((p >> (L - 1 - d)) & 1) {
+        st += n2;
+        len -= n2;
+      } else {
+        len = n2;
+      }
+    }
+    if ((p & ((1 << (L - d)) - 1)) == 0) {  // first path through this leaf
+      const int node = (1 << d) - 1 + (p >> (L - d));
+      sh.u.pw.split[node] = 0;
+      sh.u.pw.val[node] = len <= 128 ? pw_block(a + st, len) : pw_serial(a + st, len);
+    }
   }
   __syncthreads();
-  const int count = sh.pw_count;
-  for (int x = threadIdx.x; x < count; x += TV_THREADS)
-    if (sh.u.pw.left[x] < 0) sh.u.pw.val[x] = pw_serial(a + sh.u.pw.start[x], sh.u.pw.len[x]);
-  __syncthreads();
-  for (int l = sh.pw_nlevels - 1; l >= 0; --l) {
-    for (int x = sh.pw_lvl[l] + threadIdx.x; x < sh.pw_lvl[l + 1]; x += TV_THREADS)
-      if (sh.u.pw.left[x] >= 0) sh.u.pw.val[x] = __dadd_rn(sh.u.pw.val[sh.u.pw.left[x]], sh.u.pw.val[sh.u.pw.left[x] + 1]);
+  for (int d = L - 1; d >= 0; --d) {
+    for (int id = threadIdx.x; id < (1 << d); id += TV_THREADS) {
+      const int node = (1 << d) - 1 + id;
+      // nodes under a leaf hold stale flags but are never read
+      if (sh.u.pw.split[node]) {
+        const int c0 = (1 << (d + 1)) - 1 + 2 * id;
+        sh.u.pw.val[node] = __dadd_rn(sh.u.pw.val[c0], sh.u.pw.val[c0 + 1]);
+      }
+    }
     __syncthreads();
   }
   const double r = sh.u.pw.val[0];
@@ -398,11 +423,12 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
   const int64_t G = a.nb * a.nb;
 
   // ---------------- prefix (CTA 0) || clear the buckets (other CTAs)
+  // this call's counters were zeroed by the previous call; clear that one's
+  for (int x = blockIdx.x * TV_THREADS + threadIdx.x; x < (int)(sizeof(TraverseCounters) / 8);
+       x += nblocks * TV_THREADS)
+    reinterpret_cast<unsigned long long *>(a.tc_clear)[x] = 0ull;
   if (blockIdx.x == 0) {
     const unsigned long long t_entry = globaltimer();
-    for (int x = threadIdx.x; x < (int)(sizeof(TraverseCounters) / 8); x += TV_THREADS)
-      reinterpret_cast<unsigned long long *>(tc)[x] = 0ull;
-    __syncthreads();
     if (threadIdx.x == 0) tc->phase_ns[15] = t_entry;
     // one parallel load of the pyramid tops; the prefix tiers then hit smem
     const int top_entries = (int)level_offset((depth < PREFIX_LEVELS ? depth : PREFIX_LEVELS) + 1);
@@ -451,7 +477,7 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
          x += (int64_t)(nblocks - 1) * TV_THREADS)
       a.counts[x] = 0u;
   }
-  grid_sync(a.barrier, nblocks);
+  grid_sync(&tc->bar_grid, nblocks);
   PHASE(2)
 
   // ---------------- grid-wide tiers
@@ -476,7 +502,7 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
       process_tile(a, sh, t, tile, n_cand, pbase, true, a.status[t & 1]);
     }
     prev_tiles = tiles;
-    grid_sync(a.barrier, nblocks);
+    grid_sync(&tc->bar_grid, nblocks);
     PHASE(3 + (t - t0 < 5 ? t - t0 : 4))
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && depth >= t0)
@@ -498,7 +524,7 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
     if (np_ && tc->pruned_base[t] + np_ <= a.pruned_capacity) {
       const double *src = a.pruned_vals + tc->pruned_base[t];
       if (np_ <= PW_SMEM_VALS) {
-        for (unsigned x = threadIdx.x; x < np_; x += TV_THREADS) sh.u.pw.vals[x] = src[x];
+        stage_values<TV_THREADS>(sh.u.pw.vals, src, np_);
         __syncthreads();
         src = sh.u.pw.vals;
       }
@@ -512,7 +538,7 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
         tc->phase_ns[12] = globaltimer();
         double b = 0.0;
         for (int u = 0; u <= depth; ++u)
-          if (tc->n_pruned[u]) b = __dadd_rn(b, ((volatile double *)tc->tier_budget)[u]);
+          if (tc->n_pruned[u]) b = __dadd_rn(b, __ldcg(&tc->tier_budget[u]));
         tc->budget = b;
       }
       atomicMax(&tc->phase_ns[13], globaltimer());
@@ -530,7 +556,7 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
     unpack_triple(leaf_codes[p], i, j, k);
     atomicAdd(&a.counts[int64_t(i) * a.nb + j], 1u);
   }
-  grid_sync(a.barrier, gn);
+  grid_sync(&tc->bar_sub, gn);
   GPHASE(8)
 
   // ---------------- bucket scan: offsets + non-empty block list
@@ -577,7 +603,7 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
       __syncthreads();
     }
   }
-  grid_sync(a.barrier, gn);
+  grid_sync(&tc->bar_sub, gn);
   GPHASE(9)
 
   // ---------------- scatter k into the buckets; clear look-back state
@@ -592,7 +618,7 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
   // (tier depth-1's status array was already cleared during tier depth)
   if (depth >= t0) clear_status_part(a.status[depth & 1], tc->dirty_tiles[depth & 1], gi, gn);
   clear_status_part(a.status[2], (G + TV_TILE - 1) / TV_TILE, gi, gn);
-  grid_sync(a.barrier, gn);
+  grid_sync(&tc->bar_sub, gn);
   GPHASE(10)
 
   // ---------------- sort every bucket's k list ascending (one warp per bucket)
@@ -627,6 +653,518 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
   GPHASE(11)
   if (threadIdx.x == 0) atomicMax(&tc->phase_ns[13], globaltimer());  // last CTA out
 #undef GPHASE
+}
+
+// ======================================================= dense traversal
+//
+// For shallow trees (8^depth leaf triples fit comfortably) the tier-by-tier
+// compaction is replaced by one dense pass.  Thread x owns the leaf-level
+// triple whose Morton code is x -- the 3-bit digits (di,dj,dk) of every
+// level, the root's first -- so thread order IS the reference's
+// breadth-first order at every tier: a tier-t triple sits at x >> 3(depth-t)
+// and its candidates appear in the order survivors expand (multiply.py:
+// 207-212).  Each thread re-derives its ancestors' verdicts top-down
+// (candidate = parent active; the same alive / strict `< tau` tests as the
+// tiered kernel), so no survivor list is ever materialised:
+//   * tier-t counters come from the representative threads (low 3(depth-t)
+//     bits zero), CTA-reduced;
+//   * pruned calls owned by the shard set bits in per-tier Morton bitmasks
+//     (tier depth: one ballot per warp; shallower tiers: atomicOr);
+//   * retained leaf triples set bits in the leaf tier's Morton bitmask.
+// After one grid barrier, half the CTAs scan the pruned bitmasks (tier-major,
+// so the scan position IS the reference's pruned-list position), rebuild
+// each record and then run the per-tier pairwise budgets; the other half
+// walk every C block (i, j) over k ascending through the retained bitmask:
+// the block's k list comes out already sorted, so there is no histogram,
+// scatter or sort.  Both scans are single-pass decoupled look-backs whose
+// last tile clears the look-back state.
+constexpr int DN_THREADS = 256;
+constexpr int DN_MAX_DEPTH = 7;
+static_assert(DN_PARTS_H == 16 && DN_MAXT_H == DN_MAX_DEPTH + 1, "TraverseCounters::dn_part layout");
+constexpr int DN_PARTS = DN_PARTS_H;
+constexpr int DN_PW = 64;   // pruned-bitmask words per scan tile
+
+__host__ __device__ __forceinline__ uint32_t compact3(uint32_t x) {
+  x &= 0x09249249u;
+  x = (x ^ (x >> 2)) & 0x030c30c3u;
+  x = (x ^ (x >> 4)) & 0x0300f00fu;
+  x = (x ^ (x >> 8)) & 0xff0000ffu;
+  x = (x ^ (x >> 16)) & 0x000003ffu;
+  return x;
+}
+__host__ __device__ __forceinline__ uint32_t spread3(uint32_t x) {
+  x &= 0x3ffu;
+  x = (x | (x << 16)) & 0xff0000ffu;
+  x = (x | (x << 8)) & 0x0300f00fu;
+  x = (x | (x << 4)) & 0x030c30c3u;
+  x = (x | (x << 2)) & 0x09249249u;
+  return x;
+}
+
+__host__ __device__ constexpr uint64_t dn_words(int t) {  // bitmask words of tier t
+  return ((uint64_t(1) << (3 * t)) + 31) >> 5;
+}
+__host__ __device__ constexpr uint64_t dn_base(int t) {  // first word of tier t
+  uint64_t b = 0;
+  for (int s = 0; s < t; ++s) b += dn_words(s);
+  return b;
+}
+
+// Per-tier counters are accumulated per warp in registers (ballot + popc over
+// the representatives), then per CTA in shared memory, then once per CTA in
+// global memory.
+template <int D>
+__global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs a) {
+  __shared__ TvShared sh;
+  __shared__ unsigned s_cnt[D + 1][4];  // alive, active, pruned(owned), skip(owned)
+  static_assert(D + 1 <= DN_MAX_DEPTH + 1, "depth");
+  TraverseCounters *tc = a.tc;
+  const unsigned nblocks = gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long t_entry = globaltimer();
+  uint32_t *pm = a.dn_masks;                     // pruned, all tiers (tier-major)
+  constexpr uint64_t TOTAL_WORDS = dn_base(D + 1);
+  uint32_t *am = a.dn_retained;                  // retained leaf triples (rewritten every call)
+  double *npd = a.dn_np;                         // leaf-tier pruned products by Morton code
+  constexpr uint64_t N_X = uint64_t(1) << (3 * D);
+  constexpr uint64_t N_X32 = (N_X + 31) & ~uint64_t(31);
+  const double *__restrict__ nrm_a = a.nrm_a;
+  const double *__restrict__ nrm_b = a.nrm_b;
+  const uint8_t *__restrict__ occ_a = a.occ_a;
+  const uint8_t *__restrict__ occ_b = a.occ_b;
+
+  // the previous call's counters were read back already: leave them zero
+  for (int x = blockIdx.x * DN_THREADS + threadIdx.x; x < (int)(sizeof(TraverseCounters) / 8);
+       x += nblocks * DN_THREADS)
+    reinterpret_cast<unsigned long long *>(a.tc_clear)[x] = 0ull;
+  for (int x = threadIdx.x; x < (D + 1) * 4; x += DN_THREADS) (&s_cnt[0][0])[x] = 0u;
+  __syncthreads();
+
+  // ---------------- phase 1: classify every leaf triple and its ancestors
+  // Tiers t <= U have one ancestor per 64 consecutive x, so a warp's 32
+  // lanes share it: those verdicts are warp-uniform and a warp whose tier-U
+  // ancestor is not active leaves after them.
+  constexpr int U = D >= 2 ? D - 2 : -1;
+  unsigned wc[D + 1][4];
+#pragma unroll
+  for (int t = 0; t <= D; ++t) wc[t][0] = wc[t][1] = wc[t][2] = wc[t][3] = 0u;
+  for (uint64_t x = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x; x < N_X32;
+       x += (uint64_t)nblocks * DN_THREADS) {
+    const bool valid = x < N_X;
+    const uint32_t xe = valid ? (uint32_t)x : 0u;  // lanes past the end read triple 0
+    const uint32_t ix = compact3(xe >> 2), jx = compact3(xe >> 1), kx = compact3(xe);
+    const uint64_t xw = x - lane;  // the warp's first x
+    bool cand = valid;
+#pragma unroll
+    for (int t = 0; t <= U; ++t) {  // warp-uniform tiers
+      const int sh_t = D - t;
+      const uint32_t I = ix >> sh_t, J = jx >> sh_t, K = kx >> sh_t;
+      const int64_t ik = level_offset(t) + (int64_t(I) << t) + K;
+      const int64_t kj = level_offset(t) + (int64_t(K) << t) + J;
+      const int64_t r0 = int64_t(I) << sh_t, r1 = int64_t(I + 1) << sh_t;
+      const bool intersects = r1 > a.row_lo && r0 < a.row_hi;
+      const bool owned = r0 >= a.row_lo && r0 < a.row_hi;
+      const bool oc = occ_a[ik] & occ_b[kj];
+      const double np_ = __dmul_rn(nrm_a[ik], nrm_b[kj]);
+      const bool alive = cand && intersects && oc;
+      const bool pruned = alive && np_ < a.tau_tier[t];
+      const bool active = alive && !pruned;
+      // the tier-t representative is lane 0 of the warp starting its block
+      if (lane == 0 && (xw & ((uint64_t(1) << (3 * sh_t)) - 1)) == 0) {
+        wc[t][0] += alive;
+        wc[t][1] += active;
+        wc[t][2] += pruned && owned;
+        wc[t][3] += cand && intersects && !oc && owned;
+        if (pruned && owned) {
+          const uint64_t m = x >> (3 * sh_t);
+          atomicOr(&pm[dn_base(t) + (m >> 5)], 1u << (m & 31));
+        }
+      }
+      cand = active;
+    }
+    if (U >= 0 && !__any_sync(0xffffffffu, cand)) {  // nothing below survives
+      if (lane == 0) {
+        pm[dn_base(D) + (x >> 5)] = 0u;
+        am[x >> 5] = 0u;
+      }
+      continue;
+    }
+    // per-lane tiers: operands of both loaded at once
+    constexpr int T0 = U + 1;
+    double na[D + 1 - T0], nbv[D + 1 - T0];
+    bool oc[D + 1 - T0];
+#pragma unroll
+    for (int t = T0; t <= D; ++t) {
+      const uint32_t I = ix >> (D - t), J = jx >> (D - t), K = kx >> (D - t);
+      const int64_t ik = level_offset(t) + (int64_t(I) << t) + K;
+      const int64_t kj = level_offset(t) + (int64_t(K) << t) + J;
+      oc[t - T0] = occ_a[ik] & occ_b[kj];
+      na[t - T0] = nrm_a[ik];
+      nbv[t - T0] = nrm_b[kj];
+    }
+    bool pruned_leaf = false, active_leaf = false;
+    double np_leaf = 0.0;
+#pragma unroll
+    for (int t = T0; t <= D; ++t) {
+      const int sh_t = D - t;
+      const uint32_t I = ix >> sh_t;
+      const bool rep = valid && (x & ((uint64_t(1) << (3 * sh_t)) - 1)) == 0;
+      const int64_t r0 = int64_t(I) << sh_t, r1 = int64_t(I + 1) << sh_t;
+      const bool intersects = r1 > a.row_lo && r0 < a.row_hi;
+      const bool owned = r0 >= a.row_lo && r0 < a.row_hi;
+      const double np_ = __dmul_rn(na[t - T0], nbv[t - T0]);
+      const bool alive = cand && intersects && oc[t - T0];
+      const bool pruned = alive && np_ < a.tau_tier[t];
+      const bool active = alive && !pruned;
+      const bool p_own = pruned && owned;
+      const bool skip = cand && intersects && !oc[t - T0] && owned;
+      wc[t][0] += __popc(__ballot_sync(0xffffffffu, rep && alive));
+      wc[t][1] += __popc(__ballot_sync(0xffffffffu, rep && active));
+      wc[t][2] += __popc(__ballot_sync(0xffffffffu, rep && p_own));
+      wc[t][3] += __popc(__ballot_sync(0xffffffffu, rep && skip));
+      if (t < D) {
+        if (rep && p_own) {
+          const uint64_t m = x >> (3 * sh_t);
+          atomicOr(&pm[dn_base(t) + (m >> 5)], 1u << (m & 31));
+        }
+      } else {
+        pruned_leaf = p_own;
+        active_leaf = active;
+        np_leaf = np_;
+      }
+      cand = active;
+    }
+    const unsigned bp = __ballot_sync(0xffffffffu, pruned_leaf);
+    const unsigned bv = __ballot_sync(0xffffffffu, active_leaf);
+    if (pruned_leaf) npd[x] = np_leaf;
+    if (lane == 0) {
+      pm[dn_base(D) + (x >> 5)] = bp;
+      am[x >> 5] = bv;
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int t = 0; t <= D; ++t)
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+        if (wc[t][f]) atomicAdd(&s_cnt[t][f], wc[t][f]);
+  }
+  __syncthreads();
+  // CTA totals into one of DN_PARTS copies (spreads the global atomics)
+  for (int x = threadIdx.x; x < (D + 1) * 4; x += DN_THREADS) {
+    const unsigned v = (&s_cnt[0][0])[x];
+    if (v) atomicAdd(&tc->dn_part[blockIdx.x % DN_PARTS][x / 4][x % 4], (unsigned long long)v);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    tc->phase_ns[15] = t_entry;
+    tc->phase_ns[0] = globaltimer();
+  }
+  if (a.timeline && threadIdx.x == 0) {
+    a.timeline[4 * blockIdx.x] = t_entry;
+    a.timeline[4 * blockIdx.x + 1] = globaltimer();
+  }
+  grid_sync(&tc->bar_grid, nblocks);
+  if (blockIdx.x == 0 && threadIdx.x == 0) tc->phase_ns[1] = globaltimer();
+
+  const unsigned n_p = nblocks / 2 > (unsigned)(D + 1) ? nblocks / 2 : (unsigned)(D + 1);
+
+  if (blockIdx.x < n_p) {
+    // ---------------- phase 2P: pruned records, tier-major Morton order
+    // Tiles of DN_PW words; the scan position of a set bit IS its place in
+    // the reference's pruned list.  The tile's B records are then dealt out
+    // one per thread (word found by binary search over the word prefixes,
+    // bit by __fns), so the work follows the records, not the words, and the
+    // stores are coalesced.
+    constexpr unsigned long long tiles = (TOTAL_WORDS + DN_PW - 1) / DN_PW;
+    unsigned long long *status = a.dn_status;
+    __shared__ unsigned s_wpre[DN_PW + 1], s_bits[DN_PW];
+    // static round-robin tiles: every CTA is resident, so a tile's
+    // predecessors are always in progress (no ticket round trip)
+    for (unsigned long long tile = blockIdx.x; tile < tiles; tile += n_p) {
+      const uint64_t w = tile * DN_PW + threadIdx.x;
+      uint32_t bits = 0;
+      if (threadIdx.x < DN_PW && w < TOTAL_WORDS) {
+        bits = pm[w];
+        if (bits) pm[w] = 0u;  // zero at rest for the next call's atomicOr
+      }
+      unsigned long long tile_total;
+      const unsigned long long in_tile =
+          block_exclusive<DN_THREADS>(pack2(0u, (unsigned)__popc(bits)), sh.warp, &tile_total);
+      if (threadIdx.x < DN_PW) {
+        s_wpre[threadIdx.x] = unpack_b(in_tile);
+        s_bits[threadIdx.x] = bits;
+      }
+      if (warp == 0) {
+        const unsigned long long excl = lookback_exclusive(status, tile, tile_total);
+        if (lane == 0) sh.excl = excl;
+      }
+      __syncthreads();
+      const unsigned long long base = unpack_b(sh.excl);
+      const unsigned B = unpack_b(tile_total);
+#pragma unroll 4
+      for (unsigned e = threadIdx.x; e < B; e += DN_THREADS) {
+        int lo = 0, hi = DN_PW - 1;  // last word whose prefix <= e
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_wpre[mid] <= e) lo = mid; else hi = mid - 1;
+        }
+        const unsigned bit = __fns(s_bits[lo], 0, (int)(e - s_wpre[lo]) + 1);
+        const uint64_t wq = tile * DN_PW + lo;
+        int t = D;
+        uint32_t m;
+        if (wq >= dn_base(D)) {
+          m = (uint32_t)(((wq - dn_base(D)) << 5) + bit);
+        } else {
+          t = 0;
+#pragma unroll
+          for (int s2 = 1; s2 < D; ++s2) t += wq >= dn_base(s2);
+          m = (uint32_t)(((wq - dn_base(t)) << 5) + bit);
+        }
+        const uint32_t I = compact3(m >> 2), J = compact3(m >> 1), K = compact3(m);
+        double v;
+        if (t == D) {
+          v = npd[m];  // leaf tier: product saved by phase 1
+        } else {
+          const int64_t ik = level_offset(t) + (int64_t(I) << t) + K;
+          const int64_t kj = level_offset(t) + (int64_t(K) << t) + J;
+          v = __dmul_rn(nrm_a[ik], nrm_b[kj]);
+        }
+        const unsigned long long pos = base + e;
+        if (pos < a.pruned_capacity) {
+          a.pruned_vals[pos] = v;
+          a.pruned_codes[pos] = pack_triple(I, J, K);
+        } else {
+          tc->overflow = 1;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&tc->budgets_done, 1u) == tiles - 1) {  // last tile: clear look-back state
+          for (unsigned long long q = 0; q < tiles; ++q) status[q] = 0ull;
+          __threadfence();
+        }
+      }
+    }
+    if (a.timeline && threadIdx.x == 0) a.timeline[4 * blockIdx.x + 2] = globaltimer();
+    grid_sync(&tc->bar_sub, n_p);
+    if (blockIdx.x == 0 && threadIdx.x == 0) tc->phase_ns[2] = globaltimer();
+    if ((int)blockIdx.x > D) return;
+    // tier totals from the counter copies; CTA 0 publishes them
+    __shared__ unsigned long long s_tot[D + 1][4];
+    for (int x = threadIdx.x; x < (D + 1) * 4; x += DN_THREADS) (&s_tot[0][0])[x] = 0ull;
+    __syncthreads();
+    for (int x = threadIdx.x; x < DN_PARTS * (D + 1) * 4; x += DN_THREADS) {
+      const int q = x / ((D + 1) * 4), f = x - q * ((D + 1) * 4);
+      const unsigned long long v = __ldcg(&tc->dn_part[q][0][0] + f);
+      if (v) atomicAdd(&(&s_tot[0][0])[f], v);
+    }
+    __syncthreads();
+    unsigned long long pbase[D + 2];
+    pbase[0] = 0;
+#pragma unroll
+    for (int t = 0; t <= D; ++t) pbase[t + 1] = pbase[t] + s_tot[t][2];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      for (int t = 0; t <= D; ++t) {
+        tc->n_alive[t] = s_tot[t][0];
+        tc->n_active[t] = s_tot[t][1];
+        tc->n_pruned[t] = s_tot[t][2];
+        tc->n_skip[t] = s_tot[t][3];
+        tc->pruned_base[t] = pbase[t];
+      }
+      tc->n_cand[0] = 1;
+      for (int t = 1; t <= D; ++t) tc->n_cand[t] = 8ull * s_tot[t - 1][1];
+      tc->first_grid_tier = D + 1;
+      if (pbase[D + 1] > a.pruned_capacity) tc->overflow = 1;
+    }
+    // ---------------- phase 3: per-tier pairwise budget, summed in tier order
+    const int t = blockIdx.x;
+    const unsigned long long np_ = pbase[t + 1] - pbase[t];
+    double s = 0.0;
+    if (np_ && pbase[t + 1] <= a.pruned_capacity) {
+      const double *src = a.pruned_vals + pbase[t];
+      if (np_ <= PW_SMEM_VALS) {
+        stage_values<DN_THREADS>(sh.u.pw.vals, src, np_);
+        __syncthreads();
+        src = sh.u.pw.vals;
+      }
+      s = pairwise_cta(sh, src, (long long)np_);
+    }
+    if (threadIdx.x == 0) {
+      tc->tier_budget[t] = s;
+      __threadfence();
+      if (atomicAdd(&tc->sort_ticket, 1ull) == (unsigned long long)D) {
+        __threadfence();
+        double tb[D + 1];
+#pragma unroll
+        for (int u = 0; u <= D; ++u) tb[u] = __ldcg(&tc->tier_budget[u]);
+        double b = 0.0;
+#pragma unroll
+        for (int u = 0; u <= D; ++u)
+          if (pbase[u + 1] > pbase[u]) b = __dadd_rn(b, tb[u]);
+        tc->budget = b;
+        tc->phase_ns[12] = globaltimer();
+      }
+      atomicMax(&tc->phase_ns[13], globaltimer());
+    }
+    if (a.timeline && threadIdx.x == 0) a.timeline[4 * blockIdx.x + 3] = globaltimer();
+    return;
+  }
+
+  // ---------------- phase 2Q: C blocks in order, k lists ascending
+  {
+    constexpr int NB = 1 << D;
+    constexpr int64_t G = int64_t(NB) * NB;
+    constexpr unsigned long long tiles = (G + DN_THREADS - 1) / DN_THREADS;
+    unsigned long long *status = a.dn_status + a.dn_status_q;
+    for (unsigned long long tile = blockIdx.x - n_p; tile < tiles; tile += nblocks - n_p) {
+      const int64_t g = (int64_t)tile * DN_THREADS + threadIdx.x;
+      const uint32_t i = (uint32_t)(g >> D), j = (uint32_t)(g & (NB - 1));
+      const uint32_t base = (spread3(i) << 2) | (spread3(j) << 1);
+      // the block's retained bits: 4 k per word (k bits sit at x bits 0 and 3)
+      constexpr int NW = NB >= 4 ? NB / 4 : 1;
+      uint32_t wv[NW];
+      unsigned cnt = 0;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        wv[q] = 0u;
+        if (g < G) {
+          if constexpr (NB >= 4) {
+            const uint32_t x0 = base | spread3((uint32_t)(4 * q));
+            wv[q] = (am[x0 >> 5] >> (x0 & 31)) & 0x303u;
+          } else {
+            for (int k = 0; k < NB; ++k) {
+              const uint32_t x0 = base | spread3((uint32_t)k);
+              wv[q] |= ((am[x0 >> 5] >> (x0 & 31)) & 1u) << k;
+            }
+          }
+        }
+        cnt += __popc(wv[q]);
+      }
+      unsigned long long tile_total;
+      const unsigned long long in_tile =
+          block_exclusive<DN_THREADS>(pack2(cnt, cnt != 0), sh.warp, &tile_total);
+      if (warp == 0) {
+        const unsigned long long excl = lookback_exclusive(status, tile, tile_total);
+        if (lane == 0) {
+          sh.excl = excl;
+          atomicAdd(&tc->num_groups, unpack_b(tile_total));
+        }
+      }
+      __syncthreads();
+      if (a.timeline && threadIdx.x == 0) a.timeline[4 * blockIdx.x + 2] = globaltimer();
+      const unsigned long long pre = sh.excl + in_tile;
+      const unsigned tile_off = unpack_a(sh.excl), tile_cnt = unpack_a(tile_total);
+      const bool fits = tile_off + tile_cnt <= a.capacity;
+      const bool staged = tile_cnt <= 16384u;  // always for depth <= 6
+      if (cnt) {  // group records are always written; k lists only within capacity
+        const unsigned off = unpack_a(pre);
+        a.group_ids[unpack_b(pre)] = (uint32_t)g;
+        a.group_starts[unpack_b(pre)] = off;
+        if (!fits) {
+          tc->overflow = 1;
+        } else if (staged) {
+          unsigned o = off - tile_off;
+#pragma unroll
+          for (int q = 0; q < NW; ++q) {
+            if constexpr (NB >= 4) {
+              if (wv[q] & 0x001u) sh.u.qks[o++] = (uint16_t)(4 * q);
+              if (wv[q] & 0x002u) sh.u.qks[o++] = (uint16_t)(4 * q + 1);
+              if (wv[q] & 0x100u) sh.u.qks[o++] = (uint16_t)(4 * q + 2);
+              if (wv[q] & 0x200u) sh.u.qks[o++] = (uint16_t)(4 * q + 3);
+            } else {
+              for (int k = 0; k < NB; ++k)
+                if ((wv[q] >> k) & 1u) sh.u.qks[o++] = (uint16_t)k;
+            }
+          }
+        } else {
+          unsigned o = off;
+#pragma unroll
+          for (int q = 0; q < NW; ++q) {
+            if constexpr (NB >= 4) {
+              if (wv[q] & 0x001u) a.ks[o++] = 4 * q;
+              if (wv[q] & 0x002u) a.ks[o++] = 4 * q + 1;
+              if (wv[q] & 0x100u) a.ks[o++] = 4 * q + 2;
+              if (wv[q] & 0x200u) a.ks[o++] = 4 * q + 3;
+            } else {
+              for (int k = 0; k < NB; ++k)
+                if ((wv[q] >> k) & 1u) a.ks[o++] = k;
+            }
+          }
+        }
+      }
+      if (fits && staged) {  // the tile's k lists are one contiguous range of ks
+        __syncthreads();
+        for (unsigned e = threadIdx.x; e < tile_cnt; e += DN_THREADS)
+          a.ks[tile_off + e] = sh.u.qks[e];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&tc->groups_done, 1u) == tiles - 1) {
+          for (unsigned long long q = 0; q < tiles; ++q) status[q] = 0ull;
+          __threadfence();
+          tc->phase_ns[11] = globaltimer();
+        }
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    atomicMax(&tc->phase_ns[13], globaltimer());
+    if (a.timeline) a.timeline[4 * blockIdx.x + 3] = globaltimer();
+  }
+}
+
+bool dense_traversal_ok(int depth) { return depth <= DN_MAX_DEPTH; }
+size_t dense_mask_words(int depth) { return (size_t)dn_base(depth + 1); }
+size_t dense_retained_words(int depth) { return (size_t)dn_words(depth); }
+size_t dense_np_entries(int depth) { return (size_t)1 << (3 * depth); }
+size_t dense_pruned_tiles(int depth) { return (size_t)((dn_base(depth + 1) + DN_PW - 1) / DN_PW); }
+size_t dense_status_entries(int depth, int64_t nb) {
+  return dense_pruned_tiles(depth) + (size_t)((nb * nb + DN_THREADS - 1) / DN_THREADS) + 4;
+}
+
+template <int D>
+static int launch_dense_d(const TraverseArgs &args, int num_sms, cudaStream_t st) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(traverse_dense_kernel<D>,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    SPAMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_dense_kernel<D>,
+                                                                 DN_THREADS, 0));
+    if (per_sm < 1) {
+      set_error("dense traverse kernel cannot be resident");
+      return SPAMM_ERR_INTERNAL;
+    }
+  }
+  const int grid = num_sms * (per_sm < 2 ? per_sm : 2);
+  void *kargs[] = {(void *)&args};
+  // profiling aid: a plain launch (the grid still fits in one wave) so that
+  // tools which skip cooperative launches can capture the kernel
+  static const bool plain = getenv("SPAMM_TRAVERSE_PLAIN_LAUNCH") != nullptr;
+  if (plain)
+    SPAMM_CUDA_TRY(cudaLaunchKernel((const void *)traverse_dense_kernel<D>, grid, DN_THREADS,
+                                    kargs, 0, st));
+  else
+    SPAMM_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)traverse_dense_kernel<D>, grid,
+                                               DN_THREADS, kargs, 0, st));
+  return SPAMM_OK;
+}
+
+int launch_traverse_dense(const TraverseArgs &args, int num_sms, cudaStream_t st) {
+  switch (args.depth) {
+    case 0: return launch_dense_d<0>(args, num_sms, st);
+    case 1: return launch_dense_d<1>(args, num_sms, st);
+    case 2: return launch_dense_d<2>(args, num_sms, st);
+    case 3: return launch_dense_d<3>(args, num_sms, st);
+    case 4: return launch_dense_d<4>(args, num_sms, st);
+    case 5: return launch_dense_d<5>(args, num_sms, st);
+    case 6: return launch_dense_d<6>(args, num_sms, st);
+    case 7: return launch_dense_d<7>(args, num_sms, st);
+    default:
+      set_error("dense traversal supports depth <= %d", DN_MAX_DEPTH);
+      return SPAMM_ERR_INTERNAL;
+  }
 }
 
 int launch_traverse(const TraverseArgs &args, int num_sms, cudaStream_t st) {

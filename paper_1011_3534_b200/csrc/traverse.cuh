@@ -5,8 +5,11 @@
 namespace spamm {
 
 constexpr int MAX_TIERS = 32;
+constexpr int DN_PARTS_H = 16, DN_MAXT_H = 8;  // dn_part dimensions
 
-// Device-resident counters of one multiply (zeroed by the kernel itself).
+// Device-resident counters of one multiply.  Two sets alternate between
+// calls: a call finds its set zero and clears the other (the previous call's,
+// already read back by the host).
 struct TraverseCounters {
   unsigned long long ticket[MAX_TIERS];      // tile tickets of the grid-wide tiers
   unsigned long long n_cand[MAX_TIERS];      // candidates generated
@@ -21,9 +24,16 @@ struct TraverseCounters {
   int first_grid_tier;                       // tiers below ran in the single-CTA prefix
   unsigned num_groups;                       // non-empty C blocks
   unsigned budgets_done;                     // tiers whose pruned sum is final
-  unsigned long long scan_ticket, sort_ticket, gemm_ticket;
+  unsigned long long scan_ticket, sort_ticket, gemm_ticket, gemm_ticket2;
+  unsigned groups_done, pad0;
+  // grid barrier arrival counters (whole grid, subset), each on its own
+  // 128-byte line so polling CTAs never contend with the counters above
+  alignas(128) unsigned bar_grid;
+  alignas(128) unsigned bar_sub;
+  alignas(128) unsigned bar_pad;
   unsigned long long dirty_tiles[3];         // status entries to clear before the next call
   unsigned long long phase_ns[16];           // %globaltimer at phase boundaries (CTA 0)
+  unsigned long long dn_part[16][8][4];      // dense traversal: per-CTA-group tier counters
 };
 
 struct TraverseArgs {
@@ -46,11 +56,26 @@ struct TraverseArgs {
   uint32_t *group_ids;              // non-empty buckets, ascending i*nb + j
   uint32_t *group_starts;           // their offsets into ks
   uint32_t *ks;                     // inner indices, bucket-major, ascending per bucket
-  unsigned *barrier;                // [0] arrival count, [1] generation
+  // dense traversal (depth <= 7)
+  uint32_t *dn_masks;               // pruned bitmasks, all tiers (zero at rest)
+  uint32_t *dn_retained;            // retained leaf-triple bitmask
+  double *dn_np;                    // leaf-tier pruned norm products, by Morton code
+  unsigned long long *dn_status;    // look-back state: pruned scan, then (+dn_status_q) groups
+  unsigned long long dn_status_q;
+  TraverseCounters *tc_clear;       // the previous call's counter set, zeroed by this call
+  unsigned long long *timeline;     // optional per-CTA %globaltimer stamps (4 per CTA)
 };
 
 // Launch the cooperative traversal kernel (one launch per multiply).
 int launch_traverse(const TraverseArgs &args, int num_sms, cudaStream_t st);
+// Dense single-pass variant for shallow trees (see traverse.cu).
+bool dense_traversal_ok(int depth);
+size_t dense_mask_words(int depth);
+size_t dense_retained_words(int depth);
+size_t dense_pruned_tiles(int depth);
+size_t dense_np_entries(int depth);
+size_t dense_status_entries(int depth, int64_t nb);
+int launch_traverse_dense(const TraverseArgs &args, int num_sms, cudaStream_t st);
 size_t traverse_status_entries(size_t capacity);
 size_t group_status_entries(int64_t nb);
 

@@ -94,8 +94,10 @@ class MultiplyDetail:
     traverse_phase_us: list = field(default_factory=list)
 
 
-def _flags(config, keep_triples):
-    f = 0
+def _flags(config, keep_triples, traversal="auto"):
+    if traversal not in ("auto", "tiered"):
+        raise ValueError(f"traversal must be 'auto' or 'tiered', got {traversal!r}")
+    f = _lib.TIERED_TRAVERSAL if traversal == "tiered" else 0
     if config.collect_boxes:
         f |= _lib.COLLECT_BOXES
     if config.count_stats:
@@ -107,10 +109,12 @@ def _flags(config, keep_triples):
     return f
 
 
-def spamm_detailed(a, b, config=None, keep_triples=False, rows=None):
+def spamm_detailed(a, b, config=None, keep_triples=False, rows=None, traversal="auto"):
     """spamm() plus a MultiplyDetail (retained triples, per-tier counts,
     device timings).  ``rows=(lo, hi)`` restricts the product to C leaf block
-    rows [lo, hi) -- the shard of one rank in the multi-GPU layout."""
+    rows [lo, hi) -- the shard of one rank in the multi-GPU layout.
+    ``traversal="tiered"`` forces the breadth-first tier kernel even where
+    the dense single-pass kernel applies (depth <= 7); results are identical."""
     _require_conformable(a, b)
     if config is None:
         config = SpammConfig()
@@ -118,7 +122,7 @@ def spamm_detailed(a, b, config=None, keep_triples=False, rows=None):
     c = ctypes.c_void_p()
     prod = ctypes.c_void_p()
     st = _lib.Stats()
-    flags = _flags(config, keep_triples)
+    flags = _flags(config, keep_triples, traversal)
     if rows is None:
         _lib.check(L.spamm_multiply(a._handle, b._handle, float(config.tau), flags,
                                     ctypes.byref(c), ctypes.byref(st), ctypes.byref(prod)))

@@ -21,14 +21,14 @@ SMALL = gc.case_names(max_n=1024)
 LARGE = [n for n in gc.case_names() if n not in SMALL]
 
 
-def _run(name):
+def _run(name, traversal="auto"):
     meta, z, a_d, b_d = gc.load(name)
     leaf = meta["leaf"]
     a = sp.from_dense(a_d, leaf_size=leaf, dtype=a_d.dtype)
     b = a if meta["same_operand"] else sp.from_dense(b_d, leaf_size=leaf, dtype=b_d.dtype)
     cfg = sp.SpammConfig(tau=meta["tau"], collect_boxes=True,
                          tier_tau_decay=meta["tier_tau_decay"])
-    c, st, det = sp.spamm_detailed(a, b, cfg, keep_triples=True)
+    c, st, det = sp.spamm_detailed(a, b, cfg, keep_triples=True, traversal=traversal)
     return meta, z, a, b, c, st, det
 
 
@@ -36,8 +36,8 @@ def _pyr(t):
     return t._pyramid()[2], t._pyramid()[3]
 
 
-def _check(name):
-    meta, z, a, b, c, st, det = _run(name)
+def _check(name, traversal="auto"):
+    meta, z, a, b, c, st, det = _run(name, traversal)
     na, oa = _pyr(a)
     assert np.array_equal(na.view(np.uint64), z["nsq_a"].view(np.uint64)), "A norms"
     assert np.array_equal(oa, z["occ_a"]), "A occupancy"
@@ -74,14 +74,18 @@ def _check(name):
     return meta, a, b, c
 
 
+# "auto" takes the dense single-pass traversal for depth <= 7 (every golden
+# case), "tiered" the breadth-first tier kernel: both must match.
+@pytest.mark.parametrize("traversal", ["auto", "tiered"])
 @pytest.mark.parametrize("name", SMALL)
-def test_golden_small(name):
-    _check(name)
+def test_golden_small(name, traversal):
+    _check(name, traversal)
 
 
+@pytest.mark.parametrize("traversal", ["auto", "tiered"])
 @pytest.mark.parametrize("name", LARGE)
-def test_golden_large(name):
-    meta, a, b, c = _check(name)
+def test_golden_large(name, traversal):
+    meta, a, b, c = _check(name, traversal)
     # SpAMM-vs-exact error equals the reference's (multiply_error)
     err, budget = sp.multiply_error(a, b, sp.SpammConfig(tau=meta["tau"]))
     assert abs(err - meta["abs_err"]) <= 1e-9 * max(meta["abs_err"], 1e-300) + 1e-15 * meta["norm_a"] * meta["norm_b"]
