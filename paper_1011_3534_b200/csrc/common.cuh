@@ -96,6 +96,7 @@ struct DeviceContext {
   Scratch group_starts;   // non-empty C blocks and their first triple
   Scratch reduce_tmp;     // misc reduction scratch
   Scratch pyr_tickets;    // pyramid hand-off counters (self-resetting, zero at rest)
+  Scratch k1_ticket;      // K1's last-CTA ticket for the fused pyramid (zero at rest)
   Scratch dn_masks;       // dense traversal: pruned bitmasks (zero at rest)
   Scratch dn_retained;    // dense traversal: retained leaf bitmask
   Scratch dn_np;          // dense traversal: leaf-tier pruned products

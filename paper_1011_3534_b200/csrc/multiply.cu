@@ -30,6 +30,8 @@ void free_tree_async(spamm_tree *t, cudaStream_t st);
 int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap);
 int finish_tree(DeviceContext *ctx, spamm_tree *t);
+void k1_timeline_enable(cudaStream_t st);
+void k1_timeline_dump();
 
 static int check_conformable(const spamm_tree *a, const spamm_tree *b) {
   // quadtree.py:209-215
@@ -188,6 +190,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     // C's leaf level: only blocks that receive products are recomputed below
     SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nsq + level_offset(depth), 0, sizeof(double) * G, ctx->side));
     SPAMM_CUDA_BREAK(cudaMemsetAsync(c->occ + level_offset(depth), 0, G, ctx->side));
+    SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nrm + level_offset(depth), 0, sizeof(double) * G, ctx->side));
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
 
@@ -218,6 +221,8 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[3], st));
 
     // ------------------------------------------- C's tree (multiply.py:220)
+    static const bool k1tl = getenv("SPAMM_K1_TIMELINE") != nullptr;
+    if (k1tl) k1_timeline_enable(st);
     if ((rc = build_pyramid_async(ctx, c, st, &launches, ta.group_ids, &dtc->num_groups, (int64_t)gcap)))
       break;
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
@@ -245,6 +250,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       }
       fprintf(stderr, "\n");
     }
+    if (k1tl) k1_timeline_dump();
     if (!hc->overflow) break;
     unsigned long long need = 0, pneed = 0;
     for (int t = 0; t <= depth; ++t) {

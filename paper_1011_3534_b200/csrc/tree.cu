@@ -135,6 +135,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
       "r"(parity));
 }
 
+// Waits of the helper warps back off, so a helper that is far ahead never
+// competes for issue slots with the chain warp on its SMSP.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  for (;;) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    if (ok) return;
+    __nanosleep(64);
+  }
+}
+
 template <typename T>
 struct Bits;
 template <>
@@ -167,6 +182,84 @@ __device__ void canonicalise_leaf(T *padded, int64_t N, int32_t b, int64_t bi, i
 }
 
 // Staged kernel: requires b * sizeof(T) >= 16.
+// Fused pyramid tail of K1 (small trees): the last CTA of the leaf-norm
+// launch to finish reduces the whole pyramid in its shared memory, so C's
+// tree costs one launch.  ticket == nullptr disables it.
+struct PyrTail {
+  unsigned *ticket;  // zero at rest; the last CTA resets it
+  double *nsq;
+  uint8_t *occ;
+  double *nrm;
+  int depth;
+};
+
+// Whole pyramid above the leaves in one CTA: parent = ((c11 + c12) + c21) +
+// c22 (quadtree.py:90-92), occupancy OR, nrm = rn(sqrt(nsq)) for every
+// interior node.  Needs 1.25 * 9 * 4^depth bytes of shared memory.
+__device__ void pyramid_cta(const PyrTail &pt, unsigned char *smem) {
+  const int side0 = 1 << pt.depth;
+  const int n0 = side0 * side0;
+  double *bufA = reinterpret_cast<double *>(smem);
+  double *bufB = bufA + n0;
+  uint8_t *oA = reinterpret_cast<uint8_t *>(bufB + (n0 >> 2) + 1);
+  uint8_t *oB = oA + n0;
+  {
+    // eight elements per thread in flight: the loads come from L2, and a
+    // one-at-a-time loop would pay its latency 4^depth / blockDim times
+    const int64_t lo = level_offset(pt.depth);
+    for (int e0 = threadIdx.x; e0 < n0; e0 += 8 * blockDim.x) {
+      double x[8];
+      uint8_t o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        x[u] = e < n0 ? __ldcg(pt.nsq + lo + e) : 0.0;
+        o[u] = e < n0 ? __ldcg(pt.occ + lo + e) : (uint8_t)0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        if (e < n0) {  // (the leaves' nrm was written by their chains)
+          bufA[e] = x[u];
+          oA[e] = o[u];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  int side = side0;
+  for (int k = pt.depth - 1; k >= 0; --k) {
+    const int ps = side >> 1;
+    const int64_t lo = level_offset(k);
+    for (int e = threadIdx.x; e < ps * ps; e += blockDim.x) {
+      const int r = e / ps, c = e - r * ps;
+      const int f0 = (2 * r) * side + 2 * c, f1 = f0 + side;
+      const double v = __dadd_rn(__dadd_rn(__dadd_rn(bufA[f0], bufA[f0 + 1]), bufA[f1]), bufA[f1 + 1]);
+      const uint8_t o = oA[f0] | oA[f0 + 1] | oA[f1] | oA[f1 + 1];
+      bufB[e] = v;
+      oB[e] = o;
+      pt.nsq[lo + e] = v;
+      pt.occ[lo + e] = o;
+      pt.nrm[lo + e] = __dsqrt_rn(v);
+    }
+    __syncthreads();
+    double *td = bufA; bufA = bufB; bufB = td;
+    uint8_t *to = oA; oA = oB; oB = to;
+    side = ps;
+  }
+}
+
+static size_t pyramid_cta_smem(int depth) {
+  const size_t n0 = size_t(1) << (2 * depth);
+  return n0 * 8 + ((n0 >> 2) + 1) * 8 + 2 * n0;
+}
+
+__device__ unsigned long long *g_k1_tl = nullptr;
+__device__ __forceinline__ unsigned long long k1_gt() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 template <typename T, int K1_STAGES, int K1_LT>
 __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restrict__ padded,
                                                                       int64_t N, int32_t b,
@@ -174,7 +267,8 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
                                                                       double *__restrict__ nsq_leaf,
                                                                       uint8_t *__restrict__ occ_leaf,
                                                                       const uint32_t *__restrict__ list,
-                                                                      const unsigned *list_count) {
+                                                                      const unsigned *list_count,
+                                                                      PyrTail tail) {
   using U = typename Bits<T>::U;
   constexpr bool SQUARER = sizeof(T) == 8;  // warps 1-4 square in place (f64 only)
   constexpr int K1_STAGE_BYTES = K1_LT * K1_LEAF_STRIDE;
@@ -185,7 +279,9 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
   // received products -- every other leaf of C is exactly zero)
   const int64_t n_leaves = list ? (int64_t)*list_count : nb * nb;
   const int64_t leaf0 = (int64_t)blockIdx.x * K1_LT;
-  if (leaf0 >= n_leaves) return;
+  if (leaf0 < n_leaves) {
+  unsigned long long *const k1_tl = g_k1_tl;  // optional timeline (SPAMM_K1_TIMELINE)
+  if (k1_tl && threadIdx.x == 0) k1_tl[4 * blockIdx.x] = k1_gt();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t bb = (int64_t)b * b;
   const int EPC = (int)(bb < K1_CHUNK / (int)sizeof(T) ? bb : K1_CHUNK / (int)sizeof(T));
@@ -234,7 +330,7 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
     const int shift_cpr = __ffs(chunks_per_row) - 1;
     for (int chunk = 0; chunk < n_chunks; ++chunk) {
       const int stage = chunk % K1_STAGES;
-      if (chunk >= K1_STAGES) mbar_wait(&empty_bar[stage], ((chunk / K1_STAGES) - 1) & 1);
+      if (chunk >= K1_STAGES) mbar_wait_backoff(&empty_bar[stage], ((chunk / K1_STAGES) - 1) & 1);
       const int64_t off =
           (int64_t)((chunk >> shift_cpr) * R) * N + (chunk & (chunks_per_row - 1)) * CW;
       unsigned char *base = k1_smem + stage * K1_STAGE_BYTES;
@@ -244,10 +340,7 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
       cp_async_mbar_arrive(&full_bar[stage]);
     }
     cp_async_wait<0>();
-    return;
-  }
-
-  if (warp >= 1) {
+  } else if (warp >= 1) {
     // ------------------------------------------------ squarers (f64 only)
     if (SQUARER) {
       const int sw = warp - 1;  // segments [sw*segs/4, (sw+1)*segs/4) of every leaf
@@ -255,7 +348,7 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
       U bits = 0;
       for (int chunk = 0; chunk < n_chunks; ++chunk) {
         const int stage = chunk % K1_STAGES;
-        mbar_wait(&full_bar[stage], (chunk / K1_STAGES) & 1);
+        mbar_wait_backoff(&full_bar[stage], (chunk / K1_STAGES) & 1);
         if (mine) {
           unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + lane * K1_LEAF_STRIDE;
           int v = v0;
@@ -287,16 +380,35 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
       // hand the bit ORs to warp 0
       asm volatile("bar.sync 1, %0;\n" ::"n"(32 * (1 + K1_SQ_WARPS)) : "memory");
     }
-    return;
-  }
-
+  } else {
   // --------------------------------------------------------------- warp 0
   double acc = 0.0;
   U bits = 0;
   for (int chunk = 0; chunk < n_chunks; ++chunk) {
     const int stage = chunk % K1_STAGES;
     mbar_wait(SQUARER ? &sq_bar[stage] : &full_bar[stage], (chunk / K1_STAGES) & 1);
-    if (mine) {
+    if (k1_tl && lane == 0 && chunk == 0) k1_tl[4 * blockIdx.x + 1] = k1_gt();
+    if (mine && SQUARER && segs == 32) {
+      // the common case (every leaf of >= 64 elements): 4 batches of 8
+      // segments, fully unrolled so the next batch's shared loads are in
+      // flight under the current batch's 16 dependent adds
+      const unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + lane * K1_LEAF_STRIDE;
+      double2 w[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) w[u] = *reinterpret_cast<const double2 *>(pp + 16 * u);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        acc = __dadd_rn(acc, w[u].x);
+        acc = __dadd_rn(acc, w[u].y);
+      }
+    } else if (mine && SQUARER) {
+      const unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + lane * K1_LEAF_STRIDE;
+      for (int v = 0; v < segs; ++v) {
+        const double2 w = *reinterpret_cast<const double2 *>(pp + 16 * v);
+        acc = __dadd_rn(acc, w.x);
+        acc = __dadd_rn(acc, w.y);
+      }
+    } else if (mine) {
       const unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + lane * K1_LEAF_STRIDE;
       int v = 0;
       for (; v + 8 <= segs; v += 8) {
@@ -337,15 +449,33 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
 #pragma unroll
     for (int q = 0; q < K1_SQ_WARPS; ++q) bits |= lane < K1_LT ? s_bits[q][lane] : 0;
   }
+  if (k1_tl && lane == 0) k1_tl[4 * blockIdx.x + 3] = k1_gt();
   if (mine) {
     const int64_t lx = leaf0 + lane;
     const int64_t leaf = list ? (int64_t)list[lx] : lx;
     const bool nz = (U)(bits << 1) != 0;
     nsq_leaf[leaf] = acc;
     occ_leaf[leaf] = (uint8_t)nz;
+    tail.nrm[level_offset(tail.depth) + leaf] = __dsqrt_rn(acc);
     if (!nz && bits) {
       const int64_t bi = leaf / nb;
       canonicalise_leaf<T>(padded, N, b, bi, leaf - bi * nb);
+    }
+  }
+  }  // warp 0
+  }  // leaf0 < n_leaves
+  if (tail.ticket) {  // the last CTA builds the pyramid
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(tail.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      pyramid_cta(tail, k1_smem);
+      if (threadIdx.x == 0) *tail.ticket = 0u;
     }
   }
 }
@@ -494,7 +624,9 @@ __global__ void __launch_bounds__(PYR_THREADS) pyramid_fused_kernel(double *__re
 
 template <typename T>
 static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *list,
-                             const unsigned *list_count, int64_t list_cap) {
+                             const unsigned *list_count, int64_t list_cap, unsigned *ticket,
+                             bool *fused) {
+  *fused = false;
   const int64_t n_leaves = list ? std::min<int64_t>(list_cap, t->nb * t->nb) : t->nb * t->nb;
   double *nsq_leaf = t->nsq + level_offset(t->depth);
   uint8_t *occ_leaf = t->occ + level_offset(t->depth);
@@ -511,16 +643,26 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
       auto kern = leaf_norm_staged_kernel<T, S, LT>;
       SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      PyrTail tail{nullptr, t->nsq, t->occ, t->nrm, t->depth};
+      if (ticket && pyramid_cta_smem(t->depth) <= smem) {
+        tail.ticket = ticket;
+        *fused = true;
+      }
       kern<<<(unsigned)((n_leaves + LT - 1) / LT), K1_THREADS, smem, st>>>(
-          (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count);
+          (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count, tail);
     } else {
       constexpr int S = 12, LT = 8;
       const size_t smem = (size_t)S * LT * K1_LEAF_STRIDE;
       auto kern = leaf_norm_staged_kernel<T, S, LT>;
       SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      PyrTail tail{nullptr, t->nsq, t->occ, t->nrm, t->depth};
+      if (ticket && pyramid_cta_smem(t->depth) <= smem) {
+        tail.ticket = ticket;
+        *fused = true;
+      }
       kern<<<(unsigned)((n_leaves + LT - 1) / LT), K1_THREADS, smem, st>>>(
-          (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count);
+          (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count, tail);
     }
   } else {
     const int64_t grid = (n_leaves + 127) / 128;
@@ -531,13 +673,45 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
   return SPAMM_OK;
 }
 
+static unsigned long long *h_k1_tl_dev = nullptr;
+void k1_timeline_enable(cudaStream_t st) {
+  if (!h_k1_tl_dev) {
+    cudaMalloc(&h_k1_tl_dev, sizeof(unsigned long long) * 4 * 8192);
+    cudaMemcpyToSymbol(g_k1_tl, &h_k1_tl_dev, sizeof(void *));
+  }
+  cudaMemsetAsync(h_k1_tl_dev, 0, sizeof(unsigned long long) * 4 * 8192, st);
+}
+void k1_timeline_dump() {
+  std::vector<unsigned long long> tl(4 * 8192);
+  cudaMemcpy(tl.data(), h_k1_tl_dev, tl.size() * 8, cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull;
+  int n = 0;
+  for (int q = 0; q < 8192; ++q)
+    if (tl[4 * q]) { t0 = std::min(t0, tl[4 * q]); ++n; }
+  fprintf(stderr, "[k1 timeline] ctas=%d", n);
+  for (int f = 0; f < 4; ++f) {
+    std::vector<double> v;
+    for (int q = 0; q < 8192; ++q)
+      if (tl[4 * q] && tl[4 * q + f]) v.push_back((tl[4 * q + f] - t0) * 1e-3);
+    std::sort(v.begin(), v.end());
+    if (!v.empty()) fprintf(stderr, " | s%d %.1f/%.1f/%.1f", f, v[0], v[v.size() / 2], v.back());
+  }
+  fprintf(stderr, "\n");
+}
+
 // Rebuild the whole pyramid of `t` from its padded storage (canonicalising
 // all-zero leaves in place).  Stream-ordered; no host sync; two launches.
 int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap) {
-  if (t->dtype == SPAMM_DTYPE_F64) SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap));
-  else SPAMM_TRY(launch_leaf_norms<float>(t, st, list, list_count, list_cap));
+  SPAMM_TRY(ensure_scratch(ctx->k1_ticket, sizeof(unsigned), st, /*zeroed=*/true));
+  unsigned *ticket = (unsigned *)ctx->k1_ticket.ptr;
+  bool fused = false;
+  if (t->dtype == SPAMM_DTYPE_F64)
+    SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap, ticket, &fused));
+  else
+    SPAMM_TRY(launch_leaf_norms<float>(t, st, list, list_count, list_cap, ticket, &fused));
   if (launches) ++*launches;
+  if (fused) return SPAMM_OK;  // the last K1 CTA built the pyramid
   static bool carve = false;
   if (!carve) {
     cudaFuncSetAttribute(pyramid_fused_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
