@@ -101,7 +101,12 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed) {
 // 128-byte lines.
 constexpr int K1_SQ_WARPS = 3;                 // squarer warps (f64): SMSPs 1-3, never the chain warp's
 constexpr int K1_PRODUCERS = 64;
-constexpr int K1_THREADS = 32 * (1 + K1_SQ_WARPS) + K1_PRODUCERS;
+// warp 4 is a spacer that leaves at once: warps land on SMSP (warp % 4), and
+// a producer warp issuing cp.async on the chain warp's SMSP slows the chain
+// from 8.2 to 13 cycles per add (tools/chain_probe3.cu, mode 11); the
+// producers are warps 5-6 (SMSPs 1-2)
+constexpr int K1_SPACER = 32;
+constexpr int K1_THREADS = 32 * (1 + K1_SQ_WARPS) + K1_SPACER + K1_PRODUCERS;
 constexpr int K1_CHUNK = 512;                  // bytes per leaf per stage
 constexpr int K1_LEAF_STRIDE = K1_CHUNK + 16;  // smem bytes per leaf per stage
 
@@ -303,9 +308,11 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
   }
   __syncthreads();
 
-  if (warp > K1_SQ_WARPS) {
+  if (warp == 1 + K1_SQ_WARPS) {
+    // spacer: nothing to do
+  } else if (warp > 1 + K1_SQ_WARPS) {
     // ------------------------------------------------------------ producers
-    const int p = tid - 32 * (1 + K1_SQ_WARPS);
+    const int p = tid - 32 * (1 + K1_SQ_WARPS) - K1_SPACER;
     constexpr int MAX_SLOTS = (K1_LT * (K1_CHUNK / 16) + K1_PRODUCERS - 1) / K1_PRODUCERS;
     const T *slot_ptr[MAX_SLOTS];
     unsigned slot_dst[MAX_SLOTS];

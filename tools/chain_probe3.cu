@@ -150,7 +150,7 @@ int main() {
   cudaMalloc(&o, 8 * 4096 * 64);
   cudaMallocManaged(&c, 8);
   const int reps = 64;  // x 64 elements per lane
-  for (int warps : {1, 4}) {
+  for (int warps : {6, 8}) {
     for (int mode = 0; mode < 14; ++mode) {
       const int smem = warps * 32 * STRIDE;
       cudaFuncSetAttribute(chain, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
