@@ -102,6 +102,8 @@ struct DeviceContext {
   Scratch dn_np;          // dense traversal: leaf-tier pruned products
   Scratch dn_status;      // dense traversal: look-back state (zero at rest)
   int counter_parity = 0; // which traversal counter set the next call uses
+  bool last_overlapped = false;  // the last product's C tree overlapped K3
+  Scratch grp_done;       // per-group finished-tile counters (zero at rest)
   size_t cull_capacity = 0;   // survivor capacity per ping-pong buffer (items)
   size_t pruned_capacity = 0; // pruned capacity (items, all tiers)
   void *host_pinned = nullptr;  // small pinned staging for counters

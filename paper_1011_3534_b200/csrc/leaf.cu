@@ -180,6 +180,8 @@ struct StageInfo {
   int flags;       // STG_MERGE | STG_END | STG_DONE
   int h;           // merge level with the next k (31 at the item's end)
   int64_t c_off;   // element offset of the C (sub-)tile's origin
+  int grp;         // group (C block) of the item
+  int pad;
 };
 constexpr int STG_MERGE = 1, STG_END = 2, STG_DONE = 4;
 
@@ -287,6 +289,12 @@ __global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
+  // every CTA is resident: a programmatic dependent (C's norm kernel, which
+  // waits on args.grp_done) may start now and overlap this kernel
+  if (tid == 0) {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    atomicMax(&args.tc->k3_t0n, ~t_start);
+  }
 
   unsigned items = 0;
   if (warp == 0) {
@@ -339,6 +347,7 @@ __global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
             info[stage].flags = flags;
             info[stage].h = h;
             info[stage].c_off = c_off;
+            info[stage].grp = grp;
             mbar_arrive_expect_tx_l(&full_bar[stage], (unsigned)(C::STAGE_ELEMS * sizeof(double)));
             tma_load_3d(stg, &tmA, 0, kcol >> 4, arow0, &full_bar[stage]);
             if (TILE == 64 && args.b_map5)
@@ -479,6 +488,13 @@ __global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
           for (int x = 0; x < C::NACC; ++x) acc[x] = 0.0;
           pending = 0;
           top_dirty = false;
+          if (args.grp_done) {  // this warp's part of the group is in C
+            __syncwarp();
+            if (lane == 0) {
+              __threadfence();
+              atomicAdd(&args.grp_done[si.grp], 1u);
+            }
+          }
         }
       }
     }
@@ -488,6 +504,7 @@ __global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
                  "n"(C::TM_COLS));
+  if (tid == 0) atomicMax(&args.tc->k3_t1, gtimer());
   if (args.timeline && tid == 0) {
     args.timeline[3 * blockIdx.x] = t_start;
     args.timeline[3 * blockIdx.x + 1] = gtimer();
@@ -626,14 +643,18 @@ __global__ void __launch_bounds__(SIMT_THREADS) leaf_simt_kernel(LeafArgs args) 
   }
 }
 
-int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches) {
+int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches,
+                bool *signals) {
+  if (signals) *signals = false;
   if (dtype == SPAMM_DTYPE_F64 && args.leaf >= 32) {
     if (args.leaf == 32) SPAMM_TRY((launch_dmma_ws<32>(args, num_sms, st)));
     else SPAMM_TRY((launch_dmma_ws<64>(args, num_sms, st)));
-  } else if (dtype == SPAMM_DTYPE_F64) {
-    leaf_simt_kernel<double><<<num_sms * 2, SIMT_THREADS, 0, st>>>(args);
+    if (signals) *signals = args.grp_done != nullptr;
   } else {
-    leaf_simt_kernel<float><<<num_sms * 2, SIMT_THREADS, 0, st>>>(args);
+    LeafArgs a2 = args;
+    a2.grp_done = nullptr;
+    if (dtype == SPAMM_DTYPE_F64) leaf_simt_kernel<double><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
+    else leaf_simt_kernel<float><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
   }
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (launches) ++*launches;

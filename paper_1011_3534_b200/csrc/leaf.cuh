@@ -18,8 +18,13 @@ struct LeafArgs {
   TraverseCounters *tc;               // num_groups + work ticket
   unsigned long long *timeline;       // optional: per-CTA [start, end, items] (%globaltimer)
   int b_map5;                         // B streamed as the conflict-free 5-D TMA box
+  unsigned *grp_done;                 // optional: per-group count of finished warp tiles
 };
 
-int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches);
+// Returns through *signals whether the launched kernel reports finished groups
+// in args.grp_done (CWARPS per (sub-)tile) and lets dependents launch early.
+int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches,
+                bool *signals = nullptr);
+constexpr unsigned LEAF_SIGNALS_PER_TILE = 16;  // consumer warps of the warp-specialised kernel
 
 }  // namespace spamm

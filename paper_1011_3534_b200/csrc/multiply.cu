@@ -28,10 +28,12 @@ namespace spamm {
 int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out);
 void free_tree_async(spamm_tree *t, cudaStream_t st);
 int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
-                        const uint32_t *list, const unsigned *list_count, int64_t list_cap);
+                        const uint32_t *list, const unsigned *list_count, int64_t list_cap,
+                        unsigned *grp_done, unsigned grp_target, const int *overflow,
+                        unsigned long long *t_end);
 int finish_tree(DeviceContext *ctx, spamm_tree *t);
 void k1_timeline_enable(cudaStream_t st);
-void k1_timeline_dump();
+void k1_timeline_dump(unsigned long long k3_end, unsigned long long k3_start);
 
 static int check_conformable(const spamm_tree *a, const spamm_tree *b) {
   // quadtree.py:209-215
@@ -217,14 +219,33 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       SPAMM_CUDA_BREAK(cudaMemsetAsync(ctx->reduce_tmp.ptr, 0, sizeof(unsigned long long) * 3 * 4096, st));
       la.timeline = (unsigned long long *)ctx->reduce_tmp.ptr;
     }
-    if ((rc = launch_leaf(la, a->dtype, ctx->num_sms, st, &launches))) break;
-    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[3], st));
-
-    // ------------------------------------------- C's tree (multiply.py:220)
+    // per-group completion counters let C's norm kernel overlap K3
+    if ((rc = ensure_scratch(ctx->grp_done, sizeof(unsigned) * G, st, /*zeroed=*/true))) break;
+    la.grp_done = (unsigned *)ctx->grp_done.ptr;
+    // The overlapped C tree (programmatic dependent launch of K1 beside K3)
+    // is opt-in: measured on B200, K1 CTAs cannot co-reside with K3 CTAs
+    // (per-SMSP register budget of K3's 17 warps x 96 registers), so they
+    // only start as K3 CTAs retire and the overlap does not pay.
+    static const bool overlap = getenv("SPAMM_CTREE_OVERLAP") != nullptr;
+    if (!overlap) la.grp_done = nullptr;
     static const bool k1tl = getenv("SPAMM_K1_TIMELINE") != nullptr;
     if (k1tl) k1_timeline_enable(st);
-    if ((rc = build_pyramid_async(ctx, c, st, &launches, ta.group_ids, &dtc->num_groups, (int64_t)gcap)))
-      break;
+    bool overlapped = false;
+    if ((rc = launch_leaf(la, a->dtype, ctx->num_sms, st, &launches, &overlapped))) break;
+    if (!overlapped) SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[3], st));
+
+    // ------------------------------------------- C's tree (multiply.py:220)
+    // Overlapped: a programmatic dependent launch that starts once every K3
+    // CTA is resident and reads each C block as soon as K3 has stored it.
+    {
+      const int tile = a->leaf < 64 ? a->leaf : 64;
+      const unsigned subs = (unsigned)((a->leaf / tile) * (a->leaf / tile));
+      if ((rc = build_pyramid_async(ctx, c, st, &launches, ta.group_ids, &dtc->num_groups,
+                                    (int64_t)gcap, overlapped ? la.grp_done : nullptr,
+                                    LEAF_SIGNALS_PER_TILE * subs, &dtc->overflow, &dtc->k1_t1)))
+        break;
+    }
+    ctx->last_overlapped = overlapped;
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
     SPAMM_CUDA_BREAK(cudaMemcpyAsync(hc, dtc, sizeof(TraverseCounters), cudaMemcpyDeviceToHost, st));
     SPAMM_CUDA_BREAK(cudaMemcpyAsync(&c->root_norm_sq, c->nsq, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -250,7 +271,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       }
       fprintf(stderr, "\n");
     }
-    if (k1tl) k1_timeline_dump();
+    if (k1tl) k1_timeline_dump(hc->k3_t1, ~hc->k3_t0n);
     if (!hc->overflow) break;
     unsigned long long need = 0, pneed = 0;
     for (int t = 0; t <= depth; ++t) {
@@ -325,10 +346,18 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   // slot 0: kernel entry -> phase 0 (negative offset of the prologue)
   s.traverse_phase_us[0] = cc.phase_ns[15] ? (float)((double)(cc.phase_ns[0] - cc.phase_ns[15]) * 1e-3) : 0.f;
   cudaEventElapsedTime(&s.ms_cull, ctx->ev[0], ctx->ev[1]);
-  cudaEventElapsedTime(&s.ms_leaf, ctx->ev[1], ctx->ev[3]);
-  cudaEventElapsedTime(&s.ms_gemm, ctx->ev[2], ctx->ev[3]);
-  cudaEventElapsedTime(&s.ms_ctree, ctx->ev[3], ctx->ev[4]);
   cudaEventElapsedTime(&s.ms_total, ctx->ev[0], ctx->ev[4]);
+  if (ctx->last_overlapped && cc.k3_t0n && cc.k3_t1 && cc.k1_t1 > cc.k3_t1) {
+    // K3 and the C tree overlap (no event can sit between them): K3's span
+    // and the C tree's tail after it from the kernels' own %globaltimer stamps
+    s.ms_gemm = (float)((double)(cc.k3_t1 - ~cc.k3_t0n) * 1e-6);
+    s.ms_leaf = s.ms_gemm;
+    s.ms_ctree = (float)((double)(cc.k1_t1 - cc.k3_t1) * 1e-6);
+  } else {
+    cudaEventElapsedTime(&s.ms_leaf, ctx->ev[1], ctx->ev[3]);
+    cudaEventElapsedTime(&s.ms_gemm, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&s.ms_ctree, ctx->ev[3], ctx->ev[4]);
+  }
 
   // ------------------------------------------------------- product records
   if (product) {

@@ -34,6 +34,7 @@ struct TraverseCounters {
   unsigned long long dirty_tiles[3];         // status entries to clear before the next call
   unsigned long long phase_ns[16];           // %globaltimer at phase boundaries (CTA 0)
   unsigned long long dn_part[16][8][4];      // dense traversal: per-CTA-group tier counters
+  unsigned long long k3_t0n, k3_t1, k1_t1;   // %globaltimer: ~(K3 first start), K3 last end, C tree end
 };
 
 struct TraverseArgs {

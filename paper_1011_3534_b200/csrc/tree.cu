@@ -101,11 +101,9 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed) {
 // 128-byte lines.
 constexpr int K1_SQ_WARPS = 3;                 // squarer warps (f64): SMSPs 1-3, never the chain warp's
 constexpr int K1_PRODUCERS = 64;
-// warp 4 is a spacer that leaves at once: warps land on SMSP (warp % 4), and
-// a producer warp issuing cp.async on the chain warp's SMSP slows the chain
-// from 8.2 to 13 cycles per add (tools/chain_probe3.cu, mode 11); the
-// producers are warps 5-6 (SMSPs 1-2)
-constexpr int K1_SPACER = 32;
+// (A spacer warp that keeps the producers off the chain warp's SMSP was
+// measured not to matter here; K1_SPACER = 32 re-enables it.)
+constexpr int K1_SPACER = 0;
 constexpr int K1_THREADS = 32 * (1 + K1_SQ_WARPS) + K1_SPACER + K1_PRODUCERS;
 constexpr int K1_CHUNK = 512;                  // bytes per leaf per stage
 constexpr int K1_LEAF_STRIDE = K1_CHUNK + 16;  // smem bytes per leaf per stage
@@ -196,44 +194,80 @@ struct PyrTail {
   uint8_t *occ;
   double *nrm;
   int depth;
+  // Overlap with the leaf-product kernel (list mode, programmatic dependent
+  // launch): a leaf is read only once grp_done[slot] reaches grp_target
+  // (every warp tile of that C block stored); its chain lane then resets the
+  // counter.  Skipped when *overflow (the product is discarded and re-run).
+  unsigned *grp_done;
+  unsigned grp_target;
+  const int *overflow;
+  unsigned long long *t_end;  // %globaltimer when the C tree is complete
 };
 
 // Whole pyramid above the leaves in one CTA: parent = ((c11 + c12) + c21) +
 // c22 (quadtree.py:90-92), occupancy OR, nrm = rn(sqrt(nsq)) for every
-// interior node.  Needs 1.25 * 9 * 4^depth bytes of shared memory.
-__device__ void pyramid_cta(const PyrTail &pt, unsigned char *smem) {
-  const int side0 = 1 << pt.depth;
-  const int n0 = side0 * side0;
+// interior node.  Levels too large for the CTA's shared memory are reduced
+// straight from global memory (L2), the rest in shared memory.
+// Level k nodes [e0, e0 + 4 * blockDim) of this thread from their children in
+// global memory: all 16 child loads in flight before any store.
+__device__ __forceinline__ void pyr_nodes_from_global(const PyrTail &pt, int k, int e0, int n,
+                                                      double *sv, uint8_t *so) {
+  const int ps = 1 << k, side = 2 * ps;
+  const int64_t lc = level_offset(k + 1), lo = level_offset(k);
+  double cn[4][4];
+  uint8_t co[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = e0 + u * (int)blockDim.x;
+    const int ee = e < n ? e : 0;
+    const int r = ee >> k, c = ee & (ps - 1);
+    const int64_t f0 = lc + (int64_t)(2 * r) * side + 2 * c, f1 = f0 + side;
+    cn[u][0] = __ldcg(pt.nsq + f0);
+    cn[u][1] = __ldcg(pt.nsq + f0 + 1);
+    cn[u][2] = __ldcg(pt.nsq + f1);
+    cn[u][3] = __ldcg(pt.nsq + f1 + 1);
+    co[u][0] = __ldcg(pt.occ + f0);
+    co[u][1] = __ldcg(pt.occ + f0 + 1);
+    co[u][2] = __ldcg(pt.occ + f1);
+    co[u][3] = __ldcg(pt.occ + f1 + 1);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = e0 + u * (int)blockDim.x;
+    if (e < n) {
+      const double v = __dadd_rn(__dadd_rn(__dadd_rn(cn[u][0], cn[u][1]), cn[u][2]), cn[u][3]);
+      const uint8_t o = co[u][0] | co[u][1] | co[u][2] | co[u][3];
+      pt.nsq[lo + e] = v;
+      pt.occ[lo + e] = o;
+      pt.nrm[lo + e] = __dsqrt_rn(v);
+      if (sv) {
+        sv[e] = v;
+        so[e] = o;
+      }
+    }
+  }
+}
+
+__device__ void pyramid_cta(const PyrTail &pt, unsigned char *smem, size_t smem_bytes) {
+  int k = pt.depth - 1;
+  if (k < 0) return;
+  // global-memory levels until one fits (with the next) in shared memory
+  auto fits = [&](int kk) { return (size_t)(1u << (2 * kk)) * 9 * 5 / 4 + 16 <= smem_bytes; };
+  for (; k > 0 && !fits(k); --k) {
+    const int n = 1 << (2 * k);
+    for (int e0 = threadIdx.x; e0 < n; e0 += 4 * blockDim.x)
+      pyr_nodes_from_global(pt, k, e0, n, nullptr, nullptr);
+    __syncthreads();
+  }
+  const int n0 = 1 << (2 * k);
   double *bufA = reinterpret_cast<double *>(smem);
   double *bufB = bufA + n0;
   uint8_t *oA = reinterpret_cast<uint8_t *>(bufB + (n0 >> 2) + 1);
   uint8_t *oB = oA + n0;
-  {
-    // eight elements per thread in flight: the loads come from L2, and a
-    // one-at-a-time loop would pay its latency 4^depth / blockDim times
-    const int64_t lo = level_offset(pt.depth);
-    for (int e0 = threadIdx.x; e0 < n0; e0 += 8 * blockDim.x) {
-      double x[8];
-      uint8_t o[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * blockDim.x;
-        x[u] = e < n0 ? __ldcg(pt.nsq + lo + e) : 0.0;
-        o[u] = e < n0 ? __ldcg(pt.occ + lo + e) : (uint8_t)0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * blockDim.x;
-        if (e < n0) {  // (the leaves' nrm was written by their chains)
-          bufA[e] = x[u];
-          oA[e] = o[u];
-        }
-      }
-    }
-  }
+  for (int e0 = threadIdx.x; e0 < n0; e0 += 4 * blockDim.x) pyr_nodes_from_global(pt, k, e0, n0, bufA, oA);
   __syncthreads();
-  int side = side0;
-  for (int k = pt.depth - 1; k >= 0; --k) {
+  int side = 1 << k;
+  for (--k; k >= 0; --k) {
     const int ps = side >> 1;
     const int64_t lo = level_offset(k);
     for (int e = threadIdx.x; e < ps * ps; e += blockDim.x) {
@@ -254,10 +288,8 @@ __device__ void pyramid_cta(const PyrTail &pt, unsigned char *smem) {
   }
 }
 
-static size_t pyramid_cta_smem(int depth) {
-  const size_t n0 = size_t(1) << (2 * depth);
-  return n0 * 8 + ((n0 >> 2) + 1) * 8 + 2 * n0;
-}
+// whole-pyramid tails are used up to this depth (one CTA: 4^depth leaves)
+constexpr int PYR_TAIL_MAX_DEPTH = 6;
 
 __device__ unsigned long long *g_k1_tl = nullptr;
 __device__ __forceinline__ unsigned long long k1_gt() {
@@ -308,9 +340,9 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
   }
   __syncthreads();
 
-  if (warp == 1 + K1_SQ_WARPS) {
+  if (K1_SPACER && warp == 1 + K1_SQ_WARPS) {
     // spacer: nothing to do
-  } else if (warp > 1 + K1_SQ_WARPS) {
+  } else if (warp >= 1 + K1_SQ_WARPS + K1_SPACER / 32) {
     // ------------------------------------------------------------ producers
     const int p = tid - 32 * (1 + K1_SQ_WARPS) - K1_SPACER;
     constexpr int MAX_SLOTS = (K1_LT * (K1_CHUNK / 16) + K1_PRODUCERS - 1) / K1_PRODUCERS;
@@ -335,6 +367,22 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
       }
     }
     const int shift_cpr = __ffs(chunks_per_row) - 1;
+    if (tail.grp_done && !*(volatile const int *)tail.overflow) {
+      // wait until the leaf-product kernel has stored each of this thread's leaves
+#pragma unroll
+      for (int q = 0; q < MAX_SLOTS; ++q) {
+        const int sidx = p + q * K1_PRODUCERS;
+        if (slot_ptr[q] && (q == 0 || sidx / segs != (sidx - K1_PRODUCERS) / segs)) {
+          const unsigned *flag = tail.grp_done + leaf0 + sidx / segs;
+          for (;;) {
+            unsigned v;
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+            if (v >= tail.grp_target) break;
+            __nanosleep(256);
+          }
+        }
+      }
+    }
     for (int chunk = 0; chunk < n_chunks; ++chunk) {
       const int stage = chunk % K1_STAGES;
       if (chunk >= K1_STAGES) mbar_wait_backoff(&empty_bar[stage], ((chunk / K1_STAGES) - 1) & 1);
@@ -464,6 +512,7 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
     nsq_leaf[leaf] = acc;
     occ_leaf[leaf] = (uint8_t)nz;
     tail.nrm[level_offset(tail.depth) + leaf] = __dsqrt_rn(acc);
+    if (tail.grp_done) tail.grp_done[lx] = 0u;  // zero at rest for the next product
     if (!nz && bits) {
       const int64_t bi = leaf / nb;
       canonicalise_leaf<T>(padded, N, b, bi, leaf - bi * nb);
@@ -481,8 +530,11 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
     __syncthreads();
     if (s_last) {
       __threadfence();
-      pyramid_cta(tail, k1_smem);
-      if (threadIdx.x == 0) *tail.ticket = 0u;
+      pyramid_cta(tail, k1_smem, (size_t)K1_STAGES * K1_LT * K1_LEAF_STRIDE);
+      if (threadIdx.x == 0) {
+        *tail.ticket = 0u;
+        if (tail.t_end) *tail.t_end = k1_gt();
+      }
     }
   }
 }
@@ -629,10 +681,63 @@ __global__ void __launch_bounds__(PYR_THREADS) pyramid_fused_kernel(double *__re
   }
 }
 
+// Launch of the staged K1.  `ov` (list mode, after the warp-specialised leaf
+// kernel) makes it a programmatic dependent launch that overlaps that kernel
+// and waits per C block; its ring is then only 4 stages deep so one K1 CTA
+// fits beside the leaf kernel on every SM.
+struct K1Overlap {
+  unsigned *grp_done;
+  unsigned grp_target;
+  const int *overflow;
+  unsigned long long *t_end;
+};
+
+template <typename T, int S, int LT>
+static int launch_staged(spamm_tree *t, cudaStream_t st, const uint32_t *list,
+                         const unsigned *list_count, int64_t n_leaves, unsigned *ticket,
+                         const K1Overlap *ov, bool *fused) {
+  const size_t smem = (size_t)S * LT * K1_LEAF_STRIDE;
+  auto kern = leaf_norm_staged_kernel<T, S, LT>;
+  SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  PyrTail tail{};
+  tail.nsq = t->nsq;
+  tail.occ = t->occ;
+  tail.nrm = t->nrm;
+  tail.depth = t->depth;
+  if (ticket && t->depth <= PYR_TAIL_MAX_DEPTH) {
+    tail.ticket = ticket;
+    *fused = true;
+  }
+  if (ov) {
+    tail.grp_done = ov->grp_done;
+    tail.grp_target = ov->grp_target;
+    tail.overflow = ov->overflow;
+    tail.t_end = ov->t_end;
+  }
+  double *nsq_leaf = t->nsq + level_offset(t->depth);
+  uint8_t *occ_leaf = t->occ + level_offset(t->depth);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)((n_leaves + LT - 1) / LT));
+  cfg.blockDim = dim3(K1_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (ov) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  SPAMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, (T *)t->padded, t->N, (int32_t)t->leaf, t->nb,
+                                    nsq_leaf, occ_leaf, list, list_count, tail));
+  return SPAMM_OK;
+}
+
 template <typename T>
 static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *list,
                              const unsigned *list_count, int64_t list_cap, unsigned *ticket,
-                             bool *fused) {
+                             const K1Overlap *ov, bool *fused) {
   *fused = false;
   const int64_t n_leaves = list ? std::min<int64_t>(list_cap, t->nb * t->nb) : t->nb * t->nb;
   double *nsq_leaf = t->nsq + level_offset(t->depth);
@@ -644,33 +749,12 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
     // leaves per CTA, two CTAs per SM.
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
-    if (n_leaves >= (int64_t)64 * sms) {
-      constexpr int S = 6, LT = 32;
-      const size_t smem = (size_t)S * LT * K1_LEAF_STRIDE;
-      auto kern = leaf_norm_staged_kernel<T, S, LT>;
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      PyrTail tail{nullptr, t->nsq, t->occ, t->nrm, t->depth};
-      if (ticket && pyramid_cta_smem(t->depth) <= smem) {
-        tail.ticket = ticket;
-        *fused = true;
-      }
-      kern<<<(unsigned)((n_leaves + LT - 1) / LT), K1_THREADS, smem, st>>>(
-          (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count, tail);
-    } else {
-      constexpr int S = 12, LT = 8;
-      const size_t smem = (size_t)S * LT * K1_LEAF_STRIDE;
-      auto kern = leaf_norm_staged_kernel<T, S, LT>;
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      PyrTail tail{nullptr, t->nsq, t->occ, t->nrm, t->depth};
-      if (ticket && pyramid_cta_smem(t->depth) <= smem) {
-        tail.ticket = ticket;
-        *fused = true;
-      }
-      kern<<<(unsigned)((n_leaves + LT - 1) / LT), K1_THREADS, smem, st>>>(
-          (T *)t->padded, t->N, t->leaf, t->nb, nsq_leaf, occ_leaf, list, list_count, tail);
-    }
+    if (ov)
+      SPAMM_TRY((launch_staged<T, 4, 8>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
+    else if (n_leaves >= (int64_t)64 * sms)
+      SPAMM_TRY((launch_staged<T, 6, 32>(t, st, list, list_count, n_leaves, ticket, nullptr, fused)));
+    else
+      SPAMM_TRY((launch_staged<T, 12, 8>(t, st, list, list_count, n_leaves, ticket, nullptr, fused)));
   } else {
     const int64_t grid = (n_leaves + 127) / 128;
     leaf_norm_direct_kernel<T><<<(unsigned)grid, 128, 0, st>>>(
@@ -688,14 +772,15 @@ void k1_timeline_enable(cudaStream_t st) {
   }
   cudaMemsetAsync(h_k1_tl_dev, 0, sizeof(unsigned long long) * 4 * 8192, st);
 }
-void k1_timeline_dump() {
+void k1_timeline_dump(unsigned long long k3_end, unsigned long long k3_start) {
   std::vector<unsigned long long> tl(4 * 8192);
   cudaMemcpy(tl.data(), h_k1_tl_dev, tl.size() * 8, cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull;
   int n = 0;
   for (int q = 0; q < 8192; ++q)
     if (tl[4 * q]) { t0 = std::min(t0, tl[4 * q]); ++n; }
-  fprintf(stderr, "[k1 timeline] ctas=%d", n);
+  fprintf(stderr, "[k1 timeline] ctas=%d k3 start %.1f end %.1f", n, ((double)k3_start - (double)t0) * 1e-3,
+          ((double)k3_end - (double)t0) * 1e-3);
   for (int f = 0; f < 4; ++f) {
     std::vector<double> v;
     for (int q = 0; q < 8192; ++q)
@@ -709,14 +794,18 @@ void k1_timeline_dump() {
 // Rebuild the whole pyramid of `t` from its padded storage (canonicalising
 // all-zero leaves in place).  Stream-ordered; no host sync; two launches.
 int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
-                        const uint32_t *list, const unsigned *list_count, int64_t list_cap) {
+                        const uint32_t *list, const unsigned *list_count, int64_t list_cap,
+                        unsigned *grp_done, unsigned grp_target, const int *overflow,
+                        unsigned long long *t_end) {
   SPAMM_TRY(ensure_scratch(ctx->k1_ticket, sizeof(unsigned), st, /*zeroed=*/true));
   unsigned *ticket = (unsigned *)ctx->k1_ticket.ptr;
   bool fused = false;
+  K1Overlap ovs{grp_done, grp_target, overflow, t_end};
+  const K1Overlap *ov = grp_done ? &ovs : nullptr;
   if (t->dtype == SPAMM_DTYPE_F64)
-    SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap, ticket, &fused));
+    SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap, ticket, ov, &fused));
   else
-    SPAMM_TRY(launch_leaf_norms<float>(t, st, list, list_count, list_cap, ticket, &fused));
+    SPAMM_TRY(launch_leaf_norms<float>(t, st, list, list_count, list_cap, ticket, ov, &fused));
   if (launches) ++*launches;
   if (fused) return SPAMM_OK;  // the last K1 CTA built the pyramid
   static bool carve = false;
@@ -816,7 +905,8 @@ static int tree_from(const void *src, bool src_on_host, int64_t n, int64_t ld, i
                           src_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                           ctx->stream);
     if (e != cudaSuccess) { set_error("copy: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
-    rc = build_pyramid_async(ctx, t, ctx->stream, nullptr, nullptr, nullptr, 0);
+    rc = build_pyramid_async(ctx, t, ctx->stream, nullptr, nullptr, nullptr, 0, nullptr, 0, nullptr,
+                             nullptr);
     if (rc) break;
     rc = finish_tree(ctx, t);
   } while (0);
