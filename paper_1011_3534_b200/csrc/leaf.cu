@@ -323,7 +323,8 @@ __global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
         const int item = (int)atomicAdd(&args.tc->gemm_ticket, 1ull);
         if (item >= ng * subs) break;
         ++items;
-        const int grp = item / subs, sub = item - grp * subs;
+        const int gi = item / subs, sub = item - gi * subs;
+        const int grp = args.order ? (int)args.order[gi] : gi;
         const int si = sub / subs_side, sj = sub - si * subs_side;
         const int64_t start = args.group_starts[grp];
         const int64_t end = grp + 1 < ng ? args.group_starts[grp + 1] : (int64_t)m;
@@ -653,6 +654,7 @@ int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, i
   } else {
     LeafArgs a2 = args;
     a2.grp_done = nullptr;
+    a2.order = nullptr;
     if (dtype == SPAMM_DTYPE_F64) leaf_simt_kernel<double><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
     else leaf_simt_kernel<float><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
   }

@@ -19,6 +19,7 @@ struct LeafArgs {
   unsigned long long *timeline;       // optional: per-CTA [start, end, items] (%globaltimer)
   int b_map5;                         // B streamed as the conflict-free 5-D TMA box
   unsigned *grp_done;                 // optional: per-group count of finished warp tiles
+  const uint32_t *order;              // optional: work order over the groups (longest first)
 };
 
 // Returns through *signals whether the launched kernel reports finished groups

@@ -170,6 +170,13 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       ta.dn_np = (double *)ctx->dn_np.ptr;
       ta.dn_status = (unsigned long long *)ctx->dn_status.ptr;
       ta.dn_status_q = dense_pruned_tiles(depth);
+      // Longest-first order for K3 is opt-in: measured slower on the c2
+      // sweep (the (i, j) order keeps A's block rows hot in L2 across CTAs)
+      static const bool lpt = getenv("SPAMM_LPT") != nullptr;
+      if (lpt) {
+        if ((rc = ensure_scratch(ctx->lpt_order, sizeof(uint32_t) * G, st))) break;
+        ta.lpt_order = (uint32_t *)ctx->lpt_order.ptr;
+      }
     }
     static const bool tv_timeline = getenv("SPAMM_TRAVERSE_TIMELINE") != nullptr;
     static unsigned long long *tv_tl = nullptr;
@@ -212,6 +219,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     la.ks = ta.ks;
     la.group_ids = ta.group_ids;
     la.group_starts = ta.group_starts;
+    la.order = ta.lpt_order;
     la.tc = dtc;
     static const bool want_timeline = getenv("SPAMM_GEMM_TIMELINE") != nullptr;
     if (want_timeline) {

@@ -1014,6 +1014,8 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   // ---------------- phase 2Q: C blocks in order, k lists ascending
   {
     constexpr int NB = 1 << D;
+    __shared__ unsigned s_hist[NB + 1];
+    __shared__ int s_last;
     constexpr int64_t G = int64_t(NB) * NB;
     constexpr unsigned long long tiles = (G + DN_THREADS - 1) / DN_THREADS;
     unsigned long long *status = a.dn_status + a.dn_status_q;
@@ -1041,9 +1043,17 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
         }
         cnt += __popc(wv[q]);
       }
+      if (a.lpt_order) {  // group sizes for the longest-first order of K3
+        for (int x = threadIdx.x; x <= NB; x += DN_THREADS) s_hist[x] = 0u;
+        __syncthreads();
+        if (cnt) atomicAdd(&s_hist[cnt], 1u);
+      }
       unsigned long long tile_total;
       const unsigned long long in_tile =
           block_exclusive<DN_THREADS>(pack2(cnt, cnt != 0), sh.warp, &tile_total);
+      if (a.lpt_order)
+        for (int x = threadIdx.x; x <= NB; x += DN_THREADS)
+          if (s_hist[x]) atomicAdd(&tc->lpt_hist[x], s_hist[x]);
       if (warp == 0) {
         const unsigned long long excl = lookback_exclusive(status, tile, tile_total);
         if (lane == 0) {
@@ -1101,10 +1111,44 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(&tc->groups_done, 1u) == tiles - 1) {
+        s_last = atomicAdd(&tc->groups_done, 1u) == tiles - 1;
+      }
+      __syncthreads();
+      if (s_last) {  // every group is written: clear the look-back state, order the groups
+        __threadfence();
+        if (threadIdx.x == 0) {
           for (unsigned long long q = 0; q < tiles; ++q) status[q] = 0ull;
-          __threadfence();
           tc->phase_ns[11] = globaltimer();
+        }
+        if (a.lpt_order) {
+          // counting sort by size, largest first (the order inside one size
+          // class is arbitrary: each group is one CTA's work either way)
+          if (threadIdx.x == 0) {
+            unsigned run = 0;
+            for (int x = NB; x >= 1; --x) {
+              s_hist[x] = run;
+              run += __ldcg(&tc->lpt_hist[x]);
+            }
+            s_hist[0] = run;  // number of groups
+          }
+          __syncthreads();
+          const unsigned ng = s_hist[0];
+          unsigned total = 0;
+          if (ng) total = __ldcg(&a.group_starts[ng - 1]);  // + the last group's size below
+          for (unsigned q = threadIdx.x; q < ng; q += DN_THREADS) {
+            const unsigned st = __ldcg(&a.group_starts[q]);
+            unsigned size;
+            if (q + 1 < ng) {
+              size = __ldcg(&a.group_starts[q + 1]) - st;
+            } else {  // the last group: its size from the histogram total
+              unsigned sum = 0;
+              for (int x = 1; x <= NB; ++x) sum += (unsigned)x * __ldcg(&tc->lpt_hist[x]);
+              size = sum - st;
+            }
+            (void)total;
+            const unsigned pos = atomicAdd(&s_hist[size], 1u);
+            a.lpt_order[pos] = q;
+          }
         }
       }
     }

@@ -35,6 +35,7 @@ struct TraverseCounters {
   unsigned long long phase_ns[16];           // %globaltimer at phase boundaries (CTA 0)
   unsigned long long dn_part[16][8][4];      // dense traversal: per-CTA-group tier counters
   unsigned long long k3_t0n, k3_t1, k1_t1;   // %globaltimer: ~(K3 first start), K3 last end, C tree end
+  unsigned lpt_hist[132];                    // dense traversal: groups per size (k count)
 };
 
 struct TraverseArgs {
@@ -65,6 +66,7 @@ struct TraverseArgs {
   unsigned long long dn_status_q;
   TraverseCounters *tc_clear;       // the previous call's counter set, zeroed by this call
   unsigned long long *timeline;     // optional per-CTA %globaltimer stamps (4 per CTA)
+  uint32_t *lpt_order;              // optional: groups by decreasing size (K3's work order)
 };
 
 // Launch the cooperative traversal kernel (one launch per multiply).
