@@ -47,6 +47,25 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
       : "d"(a), "d"(b));
 }
 
+// One DMMA.16x8x16: C(16x8) += A(16x16) B(16x8), f64, the inner index
+// ascending -- bit-identical to four chained m8n8k4 steps on both row halves
+// (tools/dmma_order.cu), with an eighth of the instructions.
+// Fragments: a_i = A(g + 8 (i & 1), t + 4 (i >> 1)); b_i = B(t + 4 i, g);
+// c_i = C(g + 8 (i >> 1), 2 t + (i & 1)).
+__device__ __forceinline__ void dmma16816(double &c0, double &c1, double &c2, double &c3,
+                                          const double (&a)[8], const double (&b)[4]) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+      "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+      : "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+        "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+// m16n8k16 is bit-identical and verified by the parity tests, but measured
+// ~3% slower in K3 than four m8n8k4 steps (its longer dependent chain per
+// accumulator); kept selectable.
+constexpr bool kUseM16N8K16 = false;
+
 // Level at which two distinct inner indices meet in the merge tree.
 __device__ __forceinline__ int merge_level(uint32_t k0, uint32_t k1) {
   return 32 - __clz(k0 ^ k1);
@@ -438,14 +457,25 @@ __global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
         for (int nt = 0; nt < C::NT8; ++nt)
 #pragma unroll
           for (int s4 = 0; s4 < 4; ++s4) bf[nt][s4] = stg[b_o[kq][s4][nt]];
+        if constexpr (C::MT8 == 2 && kUseM16N8K16) {
+          // 16-row warp tile: one m16n8k16 per n8 tile covers the four k4 steps
+          // of both m8 halves (same fragments, same registers, same order)
+          const double a16[8] = {af[0][0], af[1][0], af[0][1], af[1][1],
+                                 af[0][2], af[1][2], af[0][3], af[1][3]};
 #pragma unroll
-        for (int s4 = 0; s4 < 4; ++s4)
+          for (int nt = 0; nt < C::NT8; ++nt)
+            dmma16816(acc[nt * 2], acc[nt * 2 + 1], acc[(C::NT8 + nt) * 2],
+                      acc[(C::NT8 + nt) * 2 + 1], a16, bf[nt]);
+        } else {
 #pragma unroll
-          for (int mt = 0; mt < C::MT8; ++mt)
+          for (int s4 = 0; s4 < 4; ++s4)
 #pragma unroll
-            for (int nt = 0; nt < C::NT8; ++nt)
-              dmma884(acc[(mt * C::NT8 + nt) * 2], acc[(mt * C::NT8 + nt) * 2 + 1], af[mt][s4],
-                      bf[nt][s4]);
+            for (int mt = 0; mt < C::MT8; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < C::NT8; ++nt)
+                dmma884(acc[(mt * C::NT8 + nt) * 2], acc[(mt * C::NT8 + nt) * 2 + 1], af[mt][s4],
+                        bf[nt][s4]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_l(&empty_bar[stage]);
