@@ -355,6 +355,10 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   s.traverse_phase_us[0] = cc.phase_ns[15] ? (float)((double)(cc.phase_ns[0] - cc.phase_ns[15]) * 1e-3) : 0.f;
   cudaEventElapsedTime(&s.ms_cull, ctx->ev[0], ctx->ev[1]);
   cudaEventElapsedTime(&s.ms_total, ctx->ev[0], ctx->ev[4]);
+  static const bool tail_dbg = getenv("SPAMM_TAIL_DEBUG") != nullptr;
+  if (tail_dbg && cc.k3_t1 && cc.k1_t1)
+    fprintf(stderr, "[tail] k3 span %.1f us, C tree done %.1f us after K3\n",
+            (double)(cc.k3_t1 - ~cc.k3_t0n) * 1e-3, ((double)cc.k1_t1 - (double)cc.k3_t1) * 1e-3);
   if (ctx->last_overlapped && cc.k3_t0n && cc.k3_t1 && cc.k1_t1 > cc.k3_t1) {
     // K3 and the C tree overlap (no event can sit between them): K3's span
     // and the C tree's tail after it from the kernels' own %globaltimer stamps

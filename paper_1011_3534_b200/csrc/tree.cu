@@ -202,6 +202,7 @@ struct PyrTail {
   unsigned grp_target;
   const int *overflow;
   unsigned long long *t_end;  // %globaltimer when the C tree is complete
+  int pdl_wait;               // launched programmatically without grp_done: wait for the grid
 };
 
 // Whole pyramid above the leaves in one CTA: parent = ((c11 + c12) + c21) +
@@ -314,6 +315,10 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
   __shared__ U s_bits[K1_SQ_WARPS][K1_LT];
   // dense mode: every leaf; list mode: only the listed leaves (C blocks that
   // received products -- every other leaf of C is exactly zero)
+  // launched as a programmatic dependent of the leaf-product kernel: the CTA
+  // may be resident before that kernel finishes; without per-group counters
+  // it waits for the whole grid (and its stores) here
+  if (tail.pdl_wait) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int64_t n_leaves = list ? (int64_t)*list_count : nb * nb;
   const int64_t leaf0 = (int64_t)blockIdx.x * K1_LT;
   if (leaf0 < n_leaves) {
@@ -690,6 +695,7 @@ struct K1Overlap {
   unsigned grp_target;
   const int *overflow;
   unsigned long long *t_end;
+  bool pdl;  // programmatic dependent launch behind the leaf-product kernel
 };
 
 template <typename T, int S, int LT>
@@ -714,6 +720,7 @@ static int launch_staged(spamm_tree *t, cudaStream_t st, const uint32_t *list,
     tail.grp_target = ov->grp_target;
     tail.overflow = ov->overflow;
     tail.t_end = ov->t_end;
+    tail.pdl_wait = ov->pdl && !ov->grp_done;
   }
   double *nsq_leaf = t->nsq + level_offset(t->depth);
   uint8_t *occ_leaf = t->occ + level_offset(t->depth);
@@ -723,7 +730,7 @@ static int launch_staged(spamm_tree *t, cudaStream_t st, const uint32_t *list,
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  if (ov) {
+  if (ov && (ov->grp_done || ov->pdl)) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
@@ -749,12 +756,12 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
     // leaves per CTA, two CTAs per SM.
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
-    if (ov)
+    if (ov && ov->grp_done)
       SPAMM_TRY((launch_staged<T, 4, 8>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
     else if (n_leaves >= (int64_t)64 * sms)
-      SPAMM_TRY((launch_staged<T, 6, 32>(t, st, list, list_count, n_leaves, ticket, nullptr, fused)));
+      SPAMM_TRY((launch_staged<T, 6, 32>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
     else
-      SPAMM_TRY((launch_staged<T, 12, 8>(t, st, list, list_count, n_leaves, ticket, nullptr, fused)));
+      SPAMM_TRY((launch_staged<T, 12, 8>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
   } else {
     const int64_t grid = (n_leaves + 127) / 128;
     leaf_norm_direct_kernel<T><<<(unsigned)grid, 128, 0, st>>>(
@@ -800,8 +807,10 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
   SPAMM_TRY(ensure_scratch(ctx->k1_ticket, sizeof(unsigned), st, /*zeroed=*/true));
   unsigned *ticket = (unsigned *)ctx->k1_ticket.ptr;
   bool fused = false;
-  K1Overlap ovs{grp_done, grp_target, overflow, t_end};
-  const K1Overlap *ov = grp_done ? &ovs : nullptr;
+  // list mode follows the leaf-product kernel: launch it programmatically so
+  // its CTAs are resident (and waiting) as that kernel's CTAs retire
+  K1Overlap ovs{grp_done, grp_target, overflow, t_end, list != nullptr && t_end != nullptr};
+  const K1Overlap *ov = (grp_done || t_end) ? &ovs : nullptr;
   if (t->dtype == SPAMM_DTYPE_F64)
     SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap, ticket, ov, &fused));
   else
