@@ -97,7 +97,9 @@ struct DeviceContext {
   Scratch reduce_tmp;     // misc reduction scratch
   Scratch pyr_tickets;    // pyramid hand-off counters (self-resetting, zero at rest)
   Scratch k1_ticket;      // K1's last-CTA ticket for the fused pyramid (zero at rest)
-  Scratch dn_masks;       // dense traversal: pruned bitmasks (zero at rest)
+  Scratch dn_masks;       // dense traversal: two work sets (zero at rest)
+  size_t dn_set_words = 0;  // words per dense work set
+  int dense_parity = 0;     // which dense work set the next dense call uses
   Scratch dn_retained;    // dense traversal: retained leaf bitmask
   Scratch dn_np;          // dense traversal: leaf-tier pruned products
   Scratch dn_status;      // dense traversal: look-back state (zero at rest)

@@ -119,14 +119,18 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     if ((rc = ensure_scratch(ctx->counters, 2 * sizeof(TraverseCounters), st, true))) break;
     const bool dense = dense_traversal_ok(depth) && !(flags & SPAMM_TIERED_TRAVERSAL);
     if (dense) {
-      if ((rc = ensure_scratch(ctx->dn_masks, sizeof(uint32_t) * dense_mask_words(depth), st, true)))
-        break;
+      // two work sets (alternating with the counter sets), zero at rest
+      const size_t ww = dense_work_words(depth);
+      if (ctx->dn_set_words < ww) {
+        if (ctx->dn_masks.ptr) SPAMM_CUDA_BREAK(cudaFreeAsync(ctx->dn_masks.ptr, st));
+        ctx->dn_masks.ptr = nullptr;
+        ctx->dn_masks.bytes = 0;
+        if ((rc = ensure_scratch(ctx->dn_masks, 2 * sizeof(uint32_t) * ww, st, true))) break;
+        ctx->dn_set_words = ww;
+      }
       if ((rc = ensure_scratch(ctx->dn_retained, sizeof(uint32_t) * dense_retained_words(depth), st)))
         break;
       if ((rc = ensure_scratch(ctx->dn_np, sizeof(double) * dense_np_entries(depth), st))) break;
-      if ((rc = ensure_scratch(ctx->dn_status,
-                               sizeof(unsigned long long) * dense_status_entries(depth, nb), st, true)))
-        break;
     }
     if ((rc = ensure_scratch(ctx->keys[0], 2 * sizeof(uint32_t) * G, st))) break;  // counts, offsets
     if ((rc = ensure_scratch(ctx->group_starts, 2 * sizeof(uint32_t) * gcap, st))) break;
@@ -165,11 +169,13 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     ta.ks = (uint32_t *)ctx->keys[1].ptr;
     ta.tc_clear = tcs + (ctx->counter_parity ^ 1);
     if (dense) {
-      ta.dn_masks = (uint32_t *)ctx->dn_masks.ptr;
+      // the work sets alternate between dense calls only (a tiered call in
+      // between leaves them untouched)
+      ta.dn_masks = (uint32_t *)ctx->dn_masks.ptr + ctx->dense_parity * ctx->dn_set_words;
+      ta.dn_masks_clear = (uint32_t *)ctx->dn_masks.ptr + (ctx->dense_parity ^ 1) * ctx->dn_set_words;
+      ta.dn_work_words = ctx->dn_set_words;
       ta.dn_retained = (uint32_t *)ctx->dn_retained.ptr;
       ta.dn_np = (double *)ctx->dn_np.ptr;
-      ta.dn_status = (unsigned long long *)ctx->dn_status.ptr;
-      ta.dn_status_q = dense_pruned_tiles(depth);
       // Longest-first order for K3 is opt-in: measured slower on the c2
       // sweep (the (i, j) order keeps A's block rows hot in L2 across CTAs)
       static const bool lpt = getenv("SPAMM_LPT") != nullptr;
@@ -191,6 +197,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
                     : launch_traverse(ta, ctx->num_sms, st)))
       break;
     ctx->counter_parity ^= 1;
+    if (dense) ctx->dense_parity ^= 1;
     ++launches;
     // C's zero fill runs on the side stream, under the traversal (issued
     // after the cooperative launch so it cannot delay its residency)

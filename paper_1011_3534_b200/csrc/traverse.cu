@@ -713,17 +713,45 @@ __host__ __device__ constexpr uint64_t dn_base(int t) {  // first word of tier t
 // Per-tier counters are accumulated per warp in registers (ballot + popc over
 // the representatives), then per CTA in shared memory, then once per CTA in
 // global memory.
+//
+// Work-set layout (one of two parity sets, zero at rest: a call uses set p and
+// clears set p^1, which the previous call used):
+//   pm  [TOTAL_WORDS]   pruned-call bitmasks, tier-major, Morton order
+//   ptc [P_TILES]       pruned calls per 64-word scan tile
+//   qtc [Q_TILES]       retained leaf triples per 256-block grouping tile
+//   ne  [NE_WORDS]      non-empty C blocks (bit g = i * nb + j)
+//   tdn [D + 1]         scan tiles finished per tier (the budget waits on it)
+// All of them are filled during classification, so after the one grid barrier
+// every scan tile finds its output offset by summing its predecessors' counts
+// (one parallel read) -- no look-back chain.
+template <int D>
+struct DnLayout {
+  static constexpr uint64_t TOTAL_WORDS = dn_base(D + 1);
+  static constexpr uint64_t P_TILES = (TOTAL_WORDS + DN_PW - 1) / DN_PW;
+  static constexpr int NB = 1 << D;
+  static constexpr uint64_t G = uint64_t(NB) * NB;
+  static constexpr uint64_t Q_TILES = (G + DN_THREADS - 1) / DN_THREADS;
+  static constexpr uint64_t NE_WORDS = (G + 31) / 32;
+  static constexpr uint64_t PM = 0, PTC = TOTAL_WORDS, QTC = PTC + P_TILES, NE = QTC + Q_TILES,
+                            TDN = NE + NE_WORDS, WORDS = TDN + D + 1;
+};
+size_t dense_work_words(int depth);
+
 template <int D>
 __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs a) {
+  using LY = DnLayout<D>;
+  constexpr int NB = LY::NB;
+  constexpr uint64_t G = LY::G;
   __shared__ TvShared sh;
   __shared__ unsigned s_cnt[D + 1][4];  // alive, active, pruned(owned), skip(owned)
-  static_assert(D + 1 <= DN_MAX_DEPTH + 1, "depth");
+  __shared__ unsigned long long s_red[DN_THREADS / 32];
   TraverseCounters *tc = a.tc;
   const unsigned nblocks = gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned long long t_entry = globaltimer();
-  uint32_t *pm = a.dn_masks;                     // pruned, all tiers (tier-major)
-  constexpr uint64_t TOTAL_WORDS = dn_base(D + 1);
+  uint32_t *ws = a.dn_masks;                     // this call's work set
+  uint32_t *pm = ws + LY::PM, *ptc = ws + LY::PTC, *qtc = ws + LY::QTC, *ne = ws + LY::NE,
+           *tdn = ws + LY::TDN;
   uint32_t *am = a.dn_retained;                  // retained leaf triples (rewritten every call)
   double *npd = a.dn_np;                         // leaf-tier pruned products by Morton code
   constexpr uint64_t N_X = uint64_t(1) << (3 * D);
@@ -733,10 +761,14 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   const uint8_t *__restrict__ occ_a = a.occ_a;
   const uint8_t *__restrict__ occ_b = a.occ_b;
 
-  // the previous call's counters were read back already: leave them zero
+  // the previous call's counters and work set were read back / consumed
+  // already: leave them zero for the call after this one
   for (int x = blockIdx.x * DN_THREADS + threadIdx.x; x < (int)(sizeof(TraverseCounters) / 8);
        x += nblocks * DN_THREADS)
     reinterpret_cast<unsigned long long *>(a.tc_clear)[x] = 0ull;
+  for (uint64_t x = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x; x < a.dn_work_words;
+       x += (uint64_t)nblocks * DN_THREADS)
+    a.dn_masks_clear[x] = 0u;
   for (int x = threadIdx.x; x < (D + 1) * 4; x += DN_THREADS) (&s_cnt[0][0])[x] = 0u;
   __syncthreads();
 
@@ -777,16 +809,15 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
         wc[t][3] += cand && intersects && !oc && owned;
         if (pruned && owned) {
           const uint64_t m = x >> (3 * sh_t);
-          atomicOr(&pm[dn_base(t) + (m >> 5)], 1u << (m & 31));
+          const uint64_t w = dn_base(t) + (m >> 5);
+          atomicOr(&pm[w], 1u << (m & 31));
+          atomicAdd(&ptc[w / DN_PW], 1u);
         }
       }
       cand = active;
     }
     if (U >= 0 && !__any_sync(0xffffffffu, cand)) {  // nothing below survives
-      if (lane == 0) {
-        pm[dn_base(D) + (x >> 5)] = 0u;
-        am[x >> 5] = 0u;
-      }
+      if (lane == 0) am[x >> 5] = 0u;  // (pm's leaf words are zero at rest)
       continue;
     }
     // per-lane tiers: operands of both loaded at once
@@ -825,7 +856,9 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
       if (t < D) {
         if (rep && p_own) {
           const uint64_t m = x >> (3 * sh_t);
-          atomicOr(&pm[dn_base(t) + (m >> 5)], 1u << (m & 31));
+          const uint64_t w = dn_base(t) + (m >> 5);
+          atomicOr(&pm[w], 1u << (m & 31));
+          atomicAdd(&ptc[w / DN_PW], 1u);
         }
       } else {
         pruned_leaf = p_own;
@@ -837,9 +870,18 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
     const unsigned bp = __ballot_sync(0xffffffffu, pruned_leaf);
     const unsigned bv = __ballot_sync(0xffffffffu, active_leaf);
     if (pruned_leaf) npd[x] = np_leaf;
+    // C block of this lane's triple; a warp's blocks all lie in one grouping tile
+    const uint64_t g = (uint64_t)ix * NB + jx;
+    const unsigned same = __match_any_sync(0xffffffffu, g);
+    if (bv && lane == __ffs(same) - 1 && (bv & same)) atomicOr(&ne[g >> 5], 1u << (g & 31));
     if (lane == 0) {
-      pm[dn_base(D) + (x >> 5)] = bp;
+      const uint64_t w = dn_base(D) + (x >> 5);
+      if (bp) {
+        pm[w] = bp;
+        atomicAdd(&ptc[w / DN_PW], (unsigned)__popc(bp));
+      }
       am[x >> 5] = bv;
+      if (bv) atomicAdd(&qtc[g / DN_THREADS], (unsigned)__popc(bv));
     }
   }
   if (lane == 0) {
@@ -866,27 +908,41 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   grid_sync(&tc->bar_grid, nblocks);
   if (blockIdx.x == 0 && threadIdx.x == 0) tc->phase_ns[1] = globaltimer();
 
-  const unsigned n_p = nblocks / 2 > (unsigned)(D + 1) ? nblocks / 2 : (unsigned)(D + 1);
+  // sum of ptr[u] over u in [lo, hi) (and popc when `bits`), by the whole CTA
+  auto cta_sum = [&](const uint32_t *ptr, uint64_t lo, uint64_t hi, bool bits) -> unsigned long long {
+    unsigned long long v = 0;
+    for (uint64_t u = lo + threadIdx.x; u < hi; u += DN_THREADS) {
+      const uint32_t w = __ldcg(ptr + u);
+      v += bits ? (unsigned long long)__popc(w) : (unsigned long long)w;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) s_red[warp] = v;
+    __syncthreads();
+    unsigned long long r = 0;
+#pragma unroll
+    for (int q = 0; q < DN_THREADS / 32; ++q) r += s_red[q];
+    __syncthreads();
+    return r;
+  };
+
+  // roles after the barrier: budget CTAs (one per tier), grouping CTAs, scan CTAs
+  const unsigned n_b = D + 1;
+  const unsigned n_q = (unsigned)(LY::Q_TILES < (nblocks - n_b) / 4 ? LY::Q_TILES : (nblocks - n_b) / 4 > 0 ? (nblocks - n_b) / 4 : 1);
+  const unsigned n_p = nblocks - n_b - n_q;
 
   if (blockIdx.x < n_p) {
     // ---------------- phase 2P: pruned records, tier-major Morton order
     // Tiles of DN_PW words; the scan position of a set bit IS its place in
-    // the reference's pruned list.  The tile's B records are then dealt out
-    // one per thread (word found by binary search over the word prefixes,
-    // bit by __fns), so the work follows the records, not the words, and the
-    // stores are coalesced.
-    constexpr unsigned long long tiles = (TOTAL_WORDS + DN_PW - 1) / DN_PW;
-    unsigned long long *status = a.dn_status;
+    // the reference's pruned list.  The tile's records are dealt out one per
+    // thread (word by binary search over the word prefixes, bit by __fns), so
+    // the work follows the records, not the words, and the stores coalesce.
     __shared__ unsigned s_wpre[DN_PW + 1], s_bits[DN_PW];
-    // static round-robin tiles: every CTA is resident, so a tile's
-    // predecessors are always in progress (no ticket round trip)
-    for (unsigned long long tile = blockIdx.x; tile < tiles; tile += n_p) {
+    for (unsigned long long tile = blockIdx.x; tile < LY::P_TILES; tile += n_p) {
+      const unsigned long long base = cta_sum(ptc, 0, tile, false);
       const uint64_t w = tile * DN_PW + threadIdx.x;
       uint32_t bits = 0;
-      if (threadIdx.x < DN_PW && w < TOTAL_WORDS) {
-        bits = pm[w];
-        if (bits) pm[w] = 0u;  // zero at rest for the next call's atomicOr
-      }
+      if (threadIdx.x < DN_PW && w < LY::TOTAL_WORDS) bits = __ldcg(pm + w);
       unsigned long long tile_total;
       const unsigned long long in_tile =
           block_exclusive<DN_THREADS>(pack2(0u, (unsigned)__popc(bits)), sh.warp, &tile_total);
@@ -894,12 +950,7 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
         s_wpre[threadIdx.x] = unpack_b(in_tile);
         s_bits[threadIdx.x] = bits;
       }
-      if (warp == 0) {
-        const unsigned long long excl = lookback_exclusive(status, tile, tile_total);
-        if (lane == 0) sh.excl = excl;
-      }
       __syncthreads();
-      const unsigned long long base = unpack_b(sh.excl);
       const unsigned B = unpack_b(tile_total);
 #pragma unroll 4
       for (unsigned e = threadIdx.x; e < B; e += DN_THREADS) {
@@ -938,19 +989,21 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
         }
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == 0) {  // tell the budget CTAs of the tiers this tile covers
         __threadfence();
-        if (atomicAdd(&tc->budgets_done, 1u) == tiles - 1) {  // last tile: clear look-back state
-          for (unsigned long long q = 0; q < tiles; ++q) status[q] = 0ull;
-          __threadfence();
-        }
+        const uint64_t w0 = tile * DN_PW, w1 = w0 + DN_PW - 1;
+#pragma unroll
+        for (int t = 0; t <= D; ++t)
+          if (w0 < dn_base(t + 1) && w1 >= dn_base(t)) atomicAdd(&tdn[t], 1u);
       }
     }
-    if (a.timeline && threadIdx.x == 0) a.timeline[4 * blockIdx.x + 2] = globaltimer();
-    grid_sync(&tc->bar_sub, n_p);
-    if (blockIdx.x == 0 && threadIdx.x == 0) tc->phase_ns[2] = globaltimer();
-    if ((int)blockIdx.x > D) return;
-    // tier totals from the counter copies; CTA 0 publishes them
+    if (a.timeline && threadIdx.x == 0) a.timeline[4 * blockIdx.x + 3] = globaltimer();
+    return;
+  }
+
+  if (blockIdx.x >= nblocks - n_b) {
+    // ---------------- budget: one CTA per tier, numpy pairwise, summed in tier order
+    const int t = (int)(blockIdx.x - (nblocks - n_b));
     __shared__ unsigned long long s_tot[D + 1][4];
     for (int x = threadIdx.x; x < (D + 1) * 4; x += DN_THREADS) (&s_tot[0][0])[x] = 0ull;
     __syncthreads();
@@ -963,25 +1016,35 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
     unsigned long long pbase[D + 2];
     pbase[0] = 0;
 #pragma unroll
-    for (int t = 0; t <= D; ++t) pbase[t + 1] = pbase[t] + s_tot[t][2];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      for (int t = 0; t <= D; ++t) {
-        tc->n_alive[t] = s_tot[t][0];
-        tc->n_active[t] = s_tot[t][1];
-        tc->n_pruned[t] = s_tot[t][2];
-        tc->n_skip[t] = s_tot[t][3];
-        tc->pruned_base[t] = pbase[t];
+    for (int u = 0; u <= D; ++u) pbase[u + 1] = pbase[u] + s_tot[u][2];
+    if (t == 0 && threadIdx.x == 0) {  // publish the tier statistics
+      for (int u = 0; u <= D; ++u) {
+        tc->n_alive[u] = s_tot[u][0];
+        tc->n_active[u] = s_tot[u][1];
+        tc->n_pruned[u] = s_tot[u][2];
+        tc->n_skip[u] = s_tot[u][3];
+        tc->pruned_base[u] = pbase[u];
       }
       tc->n_cand[0] = 1;
-      for (int t = 1; t <= D; ++t) tc->n_cand[t] = 8ull * s_tot[t - 1][1];
+      for (int u = 1; u <= D; ++u) tc->n_cand[u] = 8ull * s_tot[u - 1][1];
       tc->first_grid_tier = D + 1;
       if (pbase[D + 1] > a.pruned_capacity) tc->overflow = 1;
     }
-    // ---------------- phase 3: per-tier pairwise budget, summed in tier order
-    const int t = blockIdx.x;
     const unsigned long long np_ = pbase[t + 1] - pbase[t];
     double s = 0.0;
     if (np_ && pbase[t + 1] <= a.pruned_capacity) {
+      // wait until every scan tile covering tier t has written its records
+      const unsigned need = (unsigned)((dn_base(t + 1) - 1) / DN_PW - dn_base(t) / DN_PW + 1);
+      if (threadIdx.x == 0) {
+        for (;;) {
+          unsigned v;
+          asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(tdn + t) : "memory");
+          if (v >= need) break;
+          __nanosleep(64);
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      }
+      __syncthreads();
       const double *src = a.pruned_vals + pbase[t];
       if (np_ <= PW_SMEM_VALS) {
         stage_values<DN_THREADS>(sh.u.pw.vals, src, np_);
@@ -1006,20 +1069,18 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
         tc->phase_ns[12] = globaltimer();
       }
       atomicMax(&tc->phase_ns[13], globaltimer());
+      if (a.timeline) a.timeline[4 * blockIdx.x + 3] = globaltimer();
     }
-    if (a.timeline && threadIdx.x == 0) a.timeline[4 * blockIdx.x + 3] = globaltimer();
     return;
   }
 
   // ---------------- phase 2Q: C blocks in order, k lists ascending
   {
-    constexpr int NB = 1 << D;
     __shared__ unsigned s_hist[NB + 1];
-    __shared__ int s_last;
-    constexpr int64_t G = int64_t(NB) * NB;
-    constexpr unsigned long long tiles = (G + DN_THREADS - 1) / DN_THREADS;
-    unsigned long long *status = a.dn_status + a.dn_status_q;
-    for (unsigned long long tile = blockIdx.x - n_p; tile < tiles; tile += nblocks - n_p) {
+    for (unsigned long long tile = blockIdx.x - n_p; tile < LY::Q_TILES; tile += n_q) {
+      // this tile's offsets: retained triples and non-empty blocks before it
+      const unsigned long long ks_base = cta_sum(qtc, 0, tile, false);
+      const unsigned long long slot_base = cta_sum(ne, 0, tile * DN_THREADS / 32, true);
       const int64_t g = (int64_t)tile * DN_THREADS + threadIdx.x;
       const uint32_t i = (uint32_t)(g >> D), j = (uint32_t)(g & (NB - 1));
       const uint32_t base = (spread3(i) << 2) | (spread3(j) << 1);
@@ -1030,7 +1091,7 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
 #pragma unroll
       for (int q = 0; q < NW; ++q) {
         wv[q] = 0u;
-        if (g < G) {
+        if (g < (int64_t)G) {
           if constexpr (NB >= 4) {
             const uint32_t x0 = base | spread3((uint32_t)(4 * q));
             wv[q] = (am[x0 >> 5] >> (x0 & 31)) & 0x303u;
@@ -1054,23 +1115,15 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
       if (a.lpt_order)
         for (int x = threadIdx.x; x <= NB; x += DN_THREADS)
           if (s_hist[x]) atomicAdd(&tc->lpt_hist[x], s_hist[x]);
-      if (warp == 0) {
-        const unsigned long long excl = lookback_exclusive(status, tile, tile_total);
-        if (lane == 0) {
-          sh.excl = excl;
-          atomicAdd(&tc->num_groups, unpack_b(tile_total));
-        }
-      }
-      __syncthreads();
-      if (a.timeline && threadIdx.x == 0) a.timeline[4 * blockIdx.x + 2] = globaltimer();
-      const unsigned long long pre = sh.excl + in_tile;
-      const unsigned tile_off = unpack_a(sh.excl), tile_cnt = unpack_a(tile_total);
+      if (threadIdx.x == 0) atomicAdd(&tc->num_groups, unpack_b(tile_total));
+      const unsigned tile_off = (unsigned)ks_base, tile_cnt = unpack_a(tile_total);
       const bool fits = tile_off + tile_cnt <= a.capacity;
       const bool staged = tile_cnt <= 16384u;  // always for depth <= 6
       if (cnt) {  // group records are always written; k lists only within capacity
-        const unsigned off = unpack_a(pre);
-        a.group_ids[unpack_b(pre)] = (uint32_t)g;
-        a.group_starts[unpack_b(pre)] = off;
+        const unsigned off = tile_off + unpack_a(in_tile);
+        const unsigned slot = (unsigned)slot_base + unpack_b(in_tile);
+        a.group_ids[slot] = (uint32_t)g;
+        a.group_starts[slot] = off;
         if (!fits) {
           tc->overflow = 1;
         } else if (staged) {
@@ -1109,53 +1162,59 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
           a.ks[tile_off + e] = sh.u.qks[e];
       }
       __syncthreads();
+    }
+    if (a.lpt_order) {
+      // the last grouping CTA orders the groups, largest first (counting sort;
+      // the order within a size class is arbitrary -- each group is one CTA's
+      // work either way)
+      __shared__ int s_last;
       if (threadIdx.x == 0) {
         __threadfence();
-        s_last = atomicAdd(&tc->groups_done, 1u) == tiles - 1;
+        s_last = atomicAdd(&tc->groups_done, 1u) == n_q - 1;
       }
       __syncthreads();
-      if (s_last) {  // every group is written: clear the look-back state, order the groups
+      if (s_last) {
         __threadfence();
         if (threadIdx.x == 0) {
-          for (unsigned long long q = 0; q < tiles; ++q) status[q] = 0ull;
-          tc->phase_ns[11] = globaltimer();
+          unsigned run = 0;
+          for (int x = NB; x >= 1; --x) {
+            s_hist[x] = run;
+            run += __ldcg(&tc->lpt_hist[x]);
+          }
+          s_hist[0] = run;  // number of groups
         }
-        if (a.lpt_order) {
-          // counting sort by size, largest first (the order inside one size
-          // class is arbitrary: each group is one CTA's work either way)
-          if (threadIdx.x == 0) {
-            unsigned run = 0;
-            for (int x = NB; x >= 1; --x) {
-              s_hist[x] = run;
-              run += __ldcg(&tc->lpt_hist[x]);
-            }
-            s_hist[0] = run;  // number of groups
-          }
-          __syncthreads();
-          const unsigned ng = s_hist[0];
-          unsigned total = 0;
-          if (ng) total = __ldcg(&a.group_starts[ng - 1]);  // + the last group's size below
-          for (unsigned q = threadIdx.x; q < ng; q += DN_THREADS) {
-            const unsigned st = __ldcg(&a.group_starts[q]);
-            unsigned size;
-            if (q + 1 < ng) {
-              size = __ldcg(&a.group_starts[q + 1]) - st;
-            } else {  // the last group: its size from the histogram total
-              unsigned sum = 0;
-              for (int x = 1; x <= NB; ++x) sum += (unsigned)x * __ldcg(&tc->lpt_hist[x]);
-              size = sum - st;
-            }
-            (void)total;
-            const unsigned pos = atomicAdd(&s_hist[size], 1u);
-            a.lpt_order[pos] = q;
-          }
+        __syncthreads();
+        const unsigned ng = s_hist[0];
+        unsigned tot = 0;
+        for (int x = 1; x <= NB; ++x) tot += (unsigned)x * __ldcg(&tc->lpt_hist[x]);
+        for (unsigned q = threadIdx.x; q < ng; q += DN_THREADS) {
+          const unsigned st = __ldcg(&a.group_starts[q]);
+          const unsigned size = (q + 1 < ng ? __ldcg(&a.group_starts[q + 1]) : tot) - st;
+          const unsigned pos = atomicAdd(&s_hist[size], 1u);
+          a.lpt_order[pos] = q;
         }
       }
     }
   }
   if (threadIdx.x == 0) {
     atomicMax(&tc->phase_ns[13], globaltimer());
+    tc->phase_ns[11] = globaltimer();
     if (a.timeline) a.timeline[4 * blockIdx.x + 3] = globaltimer();
+  }
+}
+
+template <int D>
+static size_t dense_work_words_d() { return (size_t)DnLayout<D>::WORDS; }
+size_t dense_work_words(int depth) {
+  switch (depth) {
+    case 0: return dense_work_words_d<0>();
+    case 1: return dense_work_words_d<1>();
+    case 2: return dense_work_words_d<2>();
+    case 3: return dense_work_words_d<3>();
+    case 4: return dense_work_words_d<4>();
+    case 5: return dense_work_words_d<5>();
+    case 6: return dense_work_words_d<6>();
+    default: return dense_work_words_d<7>();
   }
 }
 

@@ -59,7 +59,9 @@ struct TraverseArgs {
   uint32_t *group_starts;           // their offsets into ks
   uint32_t *ks;                     // inner indices, bucket-major, ascending per bucket
   // dense traversal (depth <= 7)
-  uint32_t *dn_masks;               // pruned bitmasks, all tiers (zero at rest)
+  uint32_t *dn_masks;               // this call's work set (DnLayout; zero at entry)
+  uint32_t *dn_masks_clear;         // the previous call's work set, zeroed by this call
+  unsigned long long dn_work_words; // words per work set
   uint32_t *dn_retained;            // retained leaf-triple bitmask
   double *dn_np;                    // leaf-tier pruned norm products, by Morton code
   unsigned long long *dn_status;    // look-back state: pruned scan, then (+dn_status_q) groups
@@ -74,6 +76,7 @@ int launch_traverse(const TraverseArgs &args, int num_sms, cudaStream_t st);
 // Dense single-pass variant for shallow trees (see traverse.cu).
 bool dense_traversal_ok(int depth);
 size_t dense_mask_words(int depth);
+size_t dense_work_words(int depth);
 size_t dense_retained_words(int depth);
 size_t dense_pruned_tiles(int depth);
 size_t dense_np_entries(int depth);
