@@ -38,6 +38,13 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+WORKLOAD_DESC = {
+    "c1": "A=u0*0.9^|i-j|, B=u1*0.9^|i-j|",
+    "c2": "A=B=sym(u*0.95^|i-j|)",
+    "c3_l2": "A=sym(u0/(|i-j|^2+1)), B=sym(u1/(|i-j|^2+1))",
+    "c3_l3": "A=sym(u0/(|i-j|^3+1)), B=sym(u1/(|i-j|^3+1))",
+    "c5": "A=B=sym(u*0.98^|i-j|)",
+}
 METRIC = "SpAMM time & retained-leaf FP64 TFLOP/s vs tau, n=4096-65536, 1/2/4/8 B200"
 
 
@@ -51,6 +58,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu/context")
+    p.add_argument("--dtype", default="f64", choices=["f64", "f32"],
+                   help="storage/compute precision (c5's FP32 variant: f32)")
     p.add_argument("--dist", action="store_true",
                    help="use the torch.distributed (NCCL) path even at world size 1")
     return p.parse_args()
@@ -116,7 +125,7 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- the oracle
-def cpu_reference(a, leaf, taus, steps, warmup):
+def cpu_reference(a, leaf, taus, steps, warmup, b=None):
     """Time the oracle port (C restatement of the reference, OpenMP over all
     host cores) on the same workload: per tau cull + leaf stage + C's tree on
     prebuilt operand pyramids, like the GPU's value leg."""
@@ -125,6 +134,11 @@ def cpu_reference(a, leaf, taus, steps, warmup):
 
     pa = oracle.pad(a, leaf)
     na, oa = oracle.build_pyramid(pa, leaf)
+    if b is None or b is a:
+        pb, nb_, ob = pa, na, oa
+    else:
+        pb = oracle.pad(b, leaf)
+        nb_, ob = oracle.build_pyramid(pb, leaf)
     N = pa.shape[0]
     depth = oracle.depth_for(N, leaf)
     times, flops = [], 0.0
@@ -132,8 +146,8 @@ def cpu_reference(a, leaf, taus, steps, warmup):
         t0 = time.perf_counter()
         f = 0.0
         for tau in taus:
-            st, trip, _, _ = oracle.cull(na, oa, na, oa, depth, N, tau, collect_boxes=False)
-            c = oracle.leaf_stage(pa, pa, leaf, trip)
+            st, trip, _, _ = oracle.cull(na, oa, nb_, ob, depth, N, tau, collect_boxes=False)
+            c = oracle.leaf_stage(pa, pb, leaf, trip)
             oracle.build_pyramid(c, leaf)
             f += leaf_flops(leaf, st["leaf_matmuls"])
         dt = time.perf_counter() - t0
@@ -148,10 +162,15 @@ def run_reference(args, cfg_name):
     if rank != 0:
         return
     from paper_1011_3534_b200 import workloads
-    a, _, leaf, taus = workloads.make_config(cfg_name)
+    if cfg_name in workloads.DEVICE_CONFIGS:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"{cfg_name} is generated on the GPU (> 100 GB of host staging); "
+                          "the CPU port runs on c1-c3"}), flush=True)
+        return
+    a, b, leaf, taus = workloads.make_config(cfg_name)
     steps = max(1, args.steps)
     warm = max(0, args.warmup)
-    value, sec_per_step, cores = cpu_reference(a, leaf, taus, steps, warm)
+    value, sec_per_step, cores = cpu_reference(a, leaf, taus, steps, warm, b)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": steps, "warmup": warm,
@@ -196,12 +215,28 @@ def run_b200(args, cfg_name):
     if use_dist:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    a_host, _, leaf, taus = workloads.make_config(cfg_name)
-    n = a_host.shape[0]
     from paper_1011_3534_b200 import distributed as spd
 
+    dev_cfg = cfg_name in workloads.DEVICE_CONFIGS
+    tdtype = torch.float32 if args.dtype == "f32" else torch.float64
+    if dev_cfg:  # generated on the GPU (c5: > 100 GB of host staging otherwise)
+        at, _, leaf, taus = workloads.make_config_device(cfg_name, f"cuda:{local}", tdtype)
+        n = at.shape[0]
+        a_host = b_host = None
+        a = sp.from_device_pointer(at.data_ptr(), n, leaf_size=leaf,
+                                   dtype=np.float32 if args.dtype == "f32" else np.float64)
+        del at
+        torch.cuda.empty_cache()
+        b = a
+    else:
+        a_host, b_host, leaf, taus = workloads.make_config(cfg_name)
+        if args.dtype == "f32":
+            a_host = a_host.astype(np.float32)
+            b_host = a_host if b_host is None or b_host is a_host else b_host.astype(np.float32)
+        n = a_host.shape[0]
+        a = sp.from_dense(a_host, leaf_size=leaf)
+        b = a if b_host is a_host else sp.from_dense(b_host, leaf_size=leaf)
     shard = spd.row_shard(rank, world, n, leaf) if use_dist else None
-    a = sp.from_dense(a_host, leaf_size=leaf)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def one_step(collect=None):
@@ -210,7 +245,7 @@ def run_b200(args, cfg_name):
         for tau in taus:
             flush.zero_()
             torch.cuda.synchronize()
-            c, st, det = sp.spamm_detailed(a, a, sp.SpammConfig(tau=tau), rows=shard)
+            c, st, det = sp.spamm_detailed(a, b, sp.SpammConfig(tau=tau), rows=shard)
             f += leaf_flops(leaf, st.leaf_matmuls)
             ms += det.ms_total
             gemm += det.ms_gemm
@@ -262,7 +297,9 @@ def run_b200(args, cfg_name):
     local_gemm = sum(x[3] for step in per_tau_all for x in step)
     achieved = local_f / (local_gemm * 1e-3) / 1e12 if local_gemm > 0 else 0.0
     traffic = k3_traffic()
-    roofline = {"bound": "tensor", "kernel": "leaf_dmma_ws_kernel<64> (K3)", "achieved": achieved,
+    kname = ("leaf_dmma_ws_kernel<%d> (K3)" % min(leaf, 64) if args.dtype == "f64" and leaf >= 32
+             else "leaf_simt_kernel (K3, FMA pipe)")
+    roofline = {"bound": "tensor", "kernel": kname, "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": peak_src,
                 "traffic": traffic.get("bytes_per_launch") if traffic else None,
@@ -271,9 +308,10 @@ def run_b200(args, cfg_name):
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded numpy PCG64, SURVEY §8(d))",
-        "config": {"workload": f"{cfg_name}: n={n} leaf={leaf} A=B=sym(u*0.95^|i-j|), "
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+        "data": ("synthetic, generated on the GPU (torch Philox stream, the recipe's formula)"
+                 if dev_cfg else "synthetic (seeded numpy PCG64, SURVEY §8(d))"),
+        "config": {"workload": f"{cfg_name}: n={n} leaf={leaf} {WORKLOAD_DESC.get(cfg_name, '')}, "
                                f"tau sweep {list(taus)}, one spamm per tau per step",
                    "l2": "flushed (256 MiB write) before every multiply",
                    "parallelism": (f"C block-row shards x{world} (no data-path collective)"
@@ -284,27 +322,39 @@ def run_b200(args, cfg_name):
         "gpu_launches": launches // max(args.steps, 1),
     }
 
-    if rank == 0 and world == 1 and not args.profile:
-        # --- context: dense cuBLAS DGEMM on the same matrix
+    if rank == 0 and world == 1 and not args.profile and n <= 16384:
+        # --- context: dense cuBLAS GEMM on the same matrices
         at = torch.from_numpy(a_host).cuda()
+        bt = at if b_host is a_host else torch.from_numpy(b_host).cuda()
         for _ in range(2):
-            torch.matmul(at, at)
+            torch.matmul(at, bt)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
-        torch.matmul(at, at)
+        torch.matmul(at, bt)
         e1.record()
         torch.cuda.synchronize()
         dg = e0.elapsed_time(e1)
-        line["config"]["context_dense_cublas_dgemm"] = {
+        line["config"]["context_dense_cublas_gemm"] = {
             "ms": dg, "tflops": 2.0 * n ** 3 / (dg * 1e-3) / 1e12}
-        del at
+        del at, bt
+    elif rank == 0 and world == 1 and not args.profile:
+        # 2 n^3 at the measured cuBLAS DGEMM 8192^3 rate (a 65536^3 product takes ~16 s)
+        with open(os.path.join(ROOT, "profiles", "fp64_peaks.json")) as fh:
+            rate = json.load(fh)["cublas_dgemm_8192_tflops"]
+        line["config"]["context_dense_cublas_gemm"] = {
+            "ms": 2.0 * n ** 3 / (rate * 1e12) * 1e3, "tflops": rate,
+            "note": "estimated from the measured cuBLAS DGEMM 8192^3 rate"}
 
     if not args.no_e2e and not args.profile:
-        line["e2e"] = e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist)
+        if dev_cfg:
+            line["e2e"] = {"unavailable": "inputs generated on the GPU: host staging of a "
+                                          f"{n}x{n} operand is {n * n * 8 / 1e9:.0f} GB"}
+        else:
+            line["e2e"] = e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host)
 
-    if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
-        cv, sec, cores = cpu_reference(a_host, leaf, taus, 1, 1)
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile and not dev_cfg:
+        cv, sec, cores = cpu_reference(a_host, leaf, taus, 1, 1, b_host)
         line["cpu_baseline"] = {"value": cv, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                                 "sample": f"one full {cfg_name} tau sweep ({sec:.2f} s) after "
                                           "one warm-up sweep",
@@ -315,7 +365,7 @@ def run_b200(args, cfg_name):
         torch.distributed.destroy_process_group()
 
 
-def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist):
+def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
     """The same metric through the public API with host buffers.
 
     Every step: pinned host A -> from_dense (H2D + K1 pyramid), one spamm per
@@ -325,13 +375,19 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist):
     import torch
 
     n = a_host.shape[0]
-    pin_a = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+    tdt = torch.float32 if a_host.dtype == np.float32 else torch.float64
+    esz = a_host.dtype.itemsize
+    pin_a = torch.empty((n, n), dtype=tdt, pin_memory=True).numpy()
     pin_a[...] = a_host
+    same = b_host is None or b_host is a_host
+    if not same:
+        pin_b = torch.empty((n, n), dtype=tdt, pin_memory=True).numpy()
+        pin_b[...] = b_host
     if shard is None:
         r0, r1 = 0, n
     else:
         r0, r1 = min(shard[0] * leaf, n), min(shard[1] * leaf, n)
-    pin_c = torch.empty((max(r1 - r0, 1), n), dtype=torch.float64, pin_memory=True)
+    pin_c = torch.empty((max(r1 - r0, 1), n), dtype=tdt, pin_memory=True)
     t0 = None
     e_f = 0.0
     for it in range(args.warmup + args.steps):
@@ -341,33 +397,34 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist):
                 torch.distributed.barrier()
             t0 = time.perf_counter()
         at = sp.from_dense(pin_a, leaf_size=leaf)
+        bt = at if same else sp.from_dense(pin_b, leaf_size=leaf)
         f = 0.0
         for tau in taus:
             if shard is None:
-                c, st = sp.spamm(at, at, sp.SpammConfig(tau=tau))
+                c, st = sp.spamm(at, bt, sp.SpammConfig(tau=tau))
                 c.to_dense(out=pin_c.numpy())
             else:
                 from paper_1011_3534_b200 import distributed as spd
-                c, st, _ = sp.spamm_detailed(at, at, sp.SpammConfig(tau=tau), rows=shard)
+                c, st, _ = sp.spamm_detailed(at, bt, sp.SpammConfig(tau=tau), rows=shard)
                 if r1 > r0:
                     pin_c[: r1 - r0].copy_(spd.tree_storage(c)[r0:r1, :n])
             f += leaf_flops(leaf, st.leaf_matmuls)
             del c
-        del at
+        del at, bt
         if it >= args.warmup:
             e_f += f
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
-    d2h = len(taus) * (r1 - r0) * n * 8
+    d2h = len(taus) * (r1 - r0) * n * esz
     if use_dist:
         t = torch.tensor([el, e_f], dtype=torch.float64, device="cuda")
         mx = t[:1].clone()
         torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(t[1:])
         el, e_f = float(mx.item()), float(t[1].item())
-        d2h = len(taus) * n * n * 8  # all bands together
+        d2h = len(taus) * n * n * esz  # all bands together
     return {"value": e_f / el / 1e12, "unit": "TFLOP/s",
-            "h2d_bytes_per_step": n * n * 8 * (dist_world() if use_dist else 1),
+            "h2d_bytes_per_step": n * n * esz * (1 if same else 2) * (dist_world() if use_dist else 1),
             "d2h_bytes_per_step": d2h,
             "ms_per_step": el / args.steps * 1e3,
             "timing": "host wall clock around synchronous public-API calls (max over ranks)"}

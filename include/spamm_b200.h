@@ -58,7 +58,7 @@ extern "C" {
 #define SPAMM_TIER_TAU_DECAY 0x4u /* prune tier t against tau / 8**t          */
 #define SPAMM_KEEP_TRIPLES 0x8u   /* keep the retained leaf (i,j,k) list      */
 /* Traversal kernel selection (results are identical either way): shallow
- * trees (depth <= 7) default to the dense single-pass kernel; this flag
+ * trees (depth <= 6) default to the dense single-pass kernel; this flag
  * forces the tiered breadth-first kernel (testing / comparison). */
 #define SPAMM_TIERED_TRAVERSAL 0x10u
 

@@ -135,6 +135,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     if ((rc = ensure_scratch(ctx->keys[0], 2 * sizeof(uint32_t) * G, st))) break;  // counts, offsets
     if ((rc = ensure_scratch(ctx->group_starts, 2 * sizeof(uint32_t) * gcap, st))) break;
     if ((rc = ensure_scratch(ctx->keys[1], sizeof(uint32_t) * cap, st))) break;  // ks
+    if ((rc = ensure_scratch(ctx->pw_part, sizeof(double) * MAX_TIERS * 128, st))) break;
     TraverseCounters *tcs = (TraverseCounters *)ctx->counters.ptr;
     TraverseCounters *dtc = tcs + ctx->counter_parity;
 
@@ -168,6 +169,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     ta.group_starts = ta.group_ids + gcap;
     ta.ks = (uint32_t *)ctx->keys[1].ptr;
     ta.tc_clear = tcs + (ctx->counter_parity ^ 1);
+    ta.pw_part = (double *)ctx->pw_part.ptr;
     if (dense) {
       // the work sets alternate between dense calls only (a tiered call in
       // between leaves them untouched)

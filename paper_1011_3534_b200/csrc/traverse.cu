@@ -355,6 +355,103 @@ __device__ double pairwise_cta(TvShared &sh, const double *a, long long n) {
   return r;
 }
 
+// ---------------------------------------------------- multi-CTA budget
+// A tier with more pruned calls than one CTA can stage is split along the
+// top of numpy's recursion: its 2^L subtrees (L = pw_top_depth) are summed
+// by different CTAs with pairwise_cta, and the last of them folds the top
+// tree, left + right at every split node, exactly as the recursion adds.
+constexpr int PW_TOP_MAX = 6;  // at most 64 subtrees per tier
+constexpr int PW_PART = 128;   // heap slots per tier for the top tree
+
+__device__ __forceinline__ int pw_top_depth(long long n) {
+  int L = 0;
+  for (long long m = n; m > PW_SMEM_VALS && L < PW_TOP_MAX; m = (m + 1) / 2) ++L;
+  return L;
+}
+
+// Path s of 2^L through the top of the recursion over n values: the node's
+// range, and the depth at which it became a leaf (<= 128 values) or L.
+__device__ __forceinline__ int pw_subtree(long long n, int L, int s, long long &st, long long &len) {
+  st = 0;
+  len = n;
+  int d = 0;
+  for (; d < L && len > 128; ++d) {
+    long long n2 = len / 2;
+    n2 -= n2 % 8;
+    if ((s >> (L - 1 - d)) & 1) {
+      st += n2;
+      len -= n2;
+    } else {
+      len = n2;
+    }
+  }
+  return d;
+}
+
+// Budget work item s of tier t (the whole CTA).  vals: the tier's pruned
+// products in reference order.  Returns true to the thread that completed the
+// tier's sum (tc->tier_budget[t] is final).
+template <int NT>
+__device__ bool budget_item(TvShared &sh, TraverseCounters *tc, double *part, const double *vals,
+                            long long np_, int t, int s) {
+  const int L = pw_top_depth(np_);
+  long long st, len;
+  const int d = pw_subtree(np_, L, s, st, len);
+  const bool rep = (s & ((1 << (L - d)) - 1)) == 0;
+  if (rep && np_) {
+    const double *src = vals + st;
+    if (len <= PW_SMEM_VALS) {
+      stage_values<NT>(sh.u.pw.vals, src, (unsigned long long)len);
+      __syncthreads();
+      src = sh.u.pw.vals;
+    }
+    const double v = pairwise_cta(sh, src, len);
+    if (threadIdx.x == 0) part[t * PW_PART + (1 << d) - 1 + (s >> (L - d))] = v;
+  }
+  bool done = false;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&tc->pw_done[t], 1u) == (1u << L) - 1) {  // last item of the tier: fold
+      __threadfence();
+      double r = 0.0;
+      if (np_) {
+        if (L == 0) {
+          r = __ldcg(&part[t * PW_PART]);
+        } else {
+          // nodes split iff their range has > 128 values (and depth < L)
+          for (int dd = L - 1; dd >= 0; --dd)
+            for (int id = 0; id < (1 << dd); ++id) {
+              long long st2, len2;
+              const int dl = pw_subtree(np_, dd, id, st2, len2);
+              if (dl < dd || len2 <= 128) continue;  // a leaf (or under one)
+              const int node = (1 << dd) - 1 + id, c0 = (1 << (dd + 1)) - 1 + 2 * id;
+              part[t * PW_PART + node] =
+                  __dadd_rn(__ldcg(&part[t * PW_PART + c0]), __ldcg(&part[t * PW_PART + c0 + 1]));
+            }
+          r = __ldcg(&part[t * PW_PART]);
+        }
+      }
+      tc->tier_budget[t] = r;
+      done = true;
+    }
+  }
+  return done;
+}
+
+// Items of all tiers, tier by tier: item -> (tier, subtree).
+__device__ __forceinline__ bool budget_item_of(const unsigned long long *np_t, int ntiers, int item,
+                                               int &t, int &s) {
+  for (t = 0; t < ntiers; ++t) {
+    const int k = 1 << pw_top_depth((long long)np_t[t]);
+    if (item < k) {
+      s = item;
+      return true;
+    }
+    item -= k;
+  }
+  return false;
+}
+
 // All-ascending bitonic network (min to the lower index at every comparator;
 // the first step of each merge compares mirror positions), so +inf padding
 // past n never moves into the real range.  Distinct keys -> unique result.
@@ -511,29 +608,26 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
   unsigned long long m = tc->n_active[depth];
   if (m > a.capacity) m = a.capacity;
   const uint64_t *leaf_codes = a.codes[depth & 1];
-  const int nbud = depth + 1;  // CTAs 0..depth compute the budget, then leave
+  // CTAs 0..nbud-1 compute the budget, then leave
+  const int nbud = (int)((depth + 1) * 8 < (int)nblocks / 2 ? (depth + 1) * 8 : (int)nblocks / 2);
 
-  // ---------------- omitted_budget: one CTA per tier, concurrent with the
-  // grouping below (those CTAs never meet the later barriers); the last tier
+  // ---------------- omitted_budget: the first nbud CTAs, concurrent with the
+  // grouping below (those CTAs never meet the later barriers): numpy's
+  // pairwise sum per tier, large tiers split over several CTAs; the last tier
   // to finish adds the tier sums in tier order, as the reference's Python
   // float does.
   if ((int)blockIdx.x < nbud) {
-    const int t = blockIdx.x;
-    const unsigned long long np_ = tc->n_pruned[t];
-    double s = 0.0;
-    if (np_ && tc->pruned_base[t] + np_ <= a.pruned_capacity) {
-      const double *src = a.pruned_vals + tc->pruned_base[t];
-      if (np_ <= PW_SMEM_VALS) {
-        stage_values<TV_THREADS>(sh.u.pw.vals, src, np_);
-        __syncthreads();
-        src = sh.u.pw.vals;
-      }
-      s = pairwise_cta(sh, src, (long long)np_);
-    }
-    if (threadIdx.x == 0) {
-      tc->tier_budget[t] = s;
-      __threadfence();
-      if (atomicAdd(&tc->budgets_done, 1u) == (unsigned)depth) {
+    const int ntiers = depth + 1;
+    int total = 0;
+    for (int t = 0; t < ntiers; ++t) total += 1 << pw_top_depth((long long)tc->n_pruned[t]);
+    for (int item = blockIdx.x; item < total; item += nbud) {
+      int t, sub;
+      budget_item_of(tc->n_pruned, ntiers, item, t, sub);
+      const unsigned long long np_ = tc->n_pruned[t];
+      const bool ok = tc->pruned_base[t] + np_ <= a.pruned_capacity;
+      const bool done = budget_item<TV_THREADS>(sh, tc, a.pw_part, a.pruned_vals + tc->pruned_base[t],
+                                                ok ? (long long)np_ : 0, t, sub);
+      if (done && atomicAdd(&tc->tiers_done, 1u) == (unsigned)depth) {
         __threadfence();
         tc->phase_ns[12] = globaltimer();
         double b = 0.0;
@@ -541,8 +635,9 @@ __global__ void __launch_bounds__(TV_THREADS) traverse_kernel(TraverseArgs a) {
           if (tc->n_pruned[u]) b = __dadd_rn(b, __ldcg(&tc->tier_budget[u]));
         tc->budget = b;
       }
-      atomicMax(&tc->phase_ns[13], globaltimer());
+      __syncthreads();
     }
+    if (threadIdx.x == 0) atomicMax(&tc->phase_ns[13], globaltimer());
     return;
   }
   const unsigned gi = blockIdx.x - nbud, gn = nblocks - nbud;  // grouping CTAs
@@ -927,7 +1022,8 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   };
 
   // roles after the barrier: budget CTAs (one per tier), grouping CTAs, scan CTAs
-  const unsigned n_b = D + 1;
+  // one budget CTA per tier plus a few for the subtrees of large tiers
+  const unsigned n_b = (D + 1) + 8 < nblocks / 4 ? (D + 1) + 8 : nblocks / 4;
   const unsigned n_q = (unsigned)(LY::Q_TILES < (nblocks - n_b) / 4 ? LY::Q_TILES : (nblocks - n_b) / 4 > 0 ? (nblocks - n_b) / 4 : 1);
   const unsigned n_p = nblocks - n_b - n_q;
 
@@ -1002,9 +1098,11 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   }
 
   if (blockIdx.x >= nblocks - n_b) {
-    // ---------------- budget: one CTA per tier, numpy pairwise, summed in tier order
-    const int t = (int)(blockIdx.x - (nblocks - n_b));
+    // ---------------- budget: numpy pairwise per tier (large tiers split over
+    // several CTAs), summed in tier order
+    const int bj = (int)(blockIdx.x - (nblocks - n_b));
     __shared__ unsigned long long s_tot[D + 1][4];
+    __shared__ unsigned long long s_np[D + 1];
     for (int x = threadIdx.x; x < (D + 1) * 4; x += DN_THREADS) (&s_tot[0][0])[x] = 0ull;
     __syncthreads();
     for (int x = threadIdx.x; x < DN_PARTS * (D + 1) * 4; x += DN_THREADS) {
@@ -1017,7 +1115,8 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
     pbase[0] = 0;
 #pragma unroll
     for (int u = 0; u <= D; ++u) pbase[u + 1] = pbase[u] + s_tot[u][2];
-    if (t == 0 && threadIdx.x == 0) {  // publish the tier statistics
+    if (threadIdx.x <= D) s_np[threadIdx.x] = s_tot[threadIdx.x][2];
+    if (bj == 0 && threadIdx.x == 0) {  // publish the tier statistics
       for (int u = 0; u <= D; ++u) {
         tc->n_alive[u] = s_tot[u][0];
         tc->n_active[u] = s_tot[u][1];
@@ -1030,33 +1129,31 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
       tc->first_grid_tier = D + 1;
       if (pbase[D + 1] > a.pruned_capacity) tc->overflow = 1;
     }
-    const unsigned long long np_ = pbase[t + 1] - pbase[t];
-    double s = 0.0;
-    if (np_ && pbase[t + 1] <= a.pruned_capacity) {
-      // wait until every scan tile covering tier t has written its records
-      const unsigned need = (unsigned)((dn_base(t + 1) - 1) / DN_PW - dn_base(t) / DN_PW + 1);
-      if (threadIdx.x == 0) {
-        for (;;) {
-          unsigned v;
-          asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(tdn + t) : "memory");
-          if (v >= need) break;
-          __nanosleep(64);
+    __syncthreads();
+    int total = 0;
+    for (int u = 0; u <= D; ++u) total += 1 << pw_top_depth((long long)s_np[u]);
+    for (int item = bj; item < total; item += n_b) {
+      int t, sub;
+      budget_item_of(s_np, D + 1, item, t, sub);
+      const unsigned long long np_ = s_np[t];
+      const bool ok = pbase[t + 1] <= a.pruned_capacity;
+      if (np_ && ok) {
+        // wait until every scan tile covering tier t has written its records
+        const unsigned need = (unsigned)((dn_base(t + 1) - 1) / DN_PW - dn_base(t) / DN_PW + 1);
+        if (threadIdx.x == 0) {
+          for (;;) {
+            unsigned v;
+            asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(tdn + t) : "memory");
+            if (v >= need) break;
+            __nanosleep(64);
+          }
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      }
-      __syncthreads();
-      const double *src = a.pruned_vals + pbase[t];
-      if (np_ <= PW_SMEM_VALS) {
-        stage_values<DN_THREADS>(sh.u.pw.vals, src, np_);
         __syncthreads();
-        src = sh.u.pw.vals;
       }
-      s = pairwise_cta(sh, src, (long long)np_);
-    }
-    if (threadIdx.x == 0) {
-      tc->tier_budget[t] = s;
-      __threadfence();
-      if (atomicAdd(&tc->sort_ticket, 1ull) == (unsigned long long)D) {
+      const bool done = budget_item<DN_THREADS>(sh, tc, a.pw_part, a.pruned_vals + pbase[t],
+                                                ok ? (long long)np_ : 0, t, sub);
+      if (done && atomicAdd(&tc->tiers_done, 1u) == (unsigned)D) {
         __threadfence();
         double tb[D + 1];
 #pragma unroll
@@ -1068,6 +1165,9 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
         tc->budget = b;
         tc->phase_ns[12] = globaltimer();
       }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
       atomicMax(&tc->phase_ns[13], globaltimer());
       if (a.timeline) a.timeline[4 * blockIdx.x + 3] = globaltimer();
     }
@@ -1218,7 +1318,9 @@ size_t dense_work_words(int depth) {
   }
 }
 
-bool dense_traversal_ok(int depth) { return depth <= DN_MAX_DEPTH; }
+// Dense for depth <= 6 (c2: 36-42 us vs 47-53 us tiered); at depth 7 the
+// 2M-triple classification costs more than the tiers (c3: 109-115 vs 79-104 us).
+bool dense_traversal_ok(int depth) { return depth <= 6; }
 size_t dense_mask_words(int depth) { return (size_t)dn_base(depth + 1); }
 size_t dense_retained_words(int depth) { return (size_t)dn_words(depth); }
 size_t dense_np_entries(int depth) { return (size_t)1 << (3 * depth); }

@@ -36,6 +36,8 @@ struct TraverseCounters {
   unsigned long long dn_part[16][8][4];      // dense traversal: per-CTA-group tier counters
   unsigned long long k3_t0n, k3_t1, k1_t1;   // %globaltimer: ~(K3 first start), K3 last end, C tree end
   unsigned lpt_hist[132];                    // dense traversal: groups per size (k count)
+  unsigned pw_done[MAX_TIERS];               // budget items finished per tier
+  unsigned tiers_done, pad1;                 // tiers whose budget is final
 };
 
 struct TraverseArgs {
@@ -69,6 +71,7 @@ struct TraverseArgs {
   TraverseCounters *tc_clear;       // the previous call's counter set, zeroed by this call
   unsigned long long *timeline;     // optional per-CTA %globaltimer stamps (4 per CTA)
   uint32_t *lpt_order;              // optional: groups by decreasing size (K3's work order)
+  double *pw_part;                  // budget: per-tier top-of-recursion partial sums
 };
 
 // Launch the cooperative traversal kernel (one launch per multiply).

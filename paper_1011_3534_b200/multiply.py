@@ -114,7 +114,7 @@ def spamm_detailed(a, b, config=None, keep_triples=False, rows=None, traversal="
     device timings).  ``rows=(lo, hi)`` restricts the product to C leaf block
     rows [lo, hi) -- the shard of one rank in the multi-GPU layout.
     ``traversal="tiered"`` forces the breadth-first tier kernel even where
-    the dense single-pass kernel applies (depth <= 7); results are identical."""
+    the dense single-pass kernel applies (depth <= 6); results are identical."""
     _require_conformable(a, b)
     if config is None:
         config = SpammConfig()

@@ -59,3 +59,39 @@ def make_config(name):
     cfg = CONFIGS[name]
     a, b = cfg["make"]()
     return a, b, cfg["leaf"], cfg["taus"]
+
+
+# ------------------------------------------------------------ on-device inputs
+# c5 (n = 65536) would need > 100 GB of host staging through numpy.  These
+# generators build the same formulas on the GPU with torch's Philox stream
+# (same distribution, different draw than numpy's PCG64), row block by row
+# block, for measurement runs only; parity is pinned on the host recipe above.
+DEVICE_CONFIGS = {
+    "c5": dict(n=65536, leaf=64, taus=(1e-8,), lam=0.98, seed=0),
+}
+
+
+def exponential_decay_device(n, lam, seed, device, dtype=None, block=4096):
+    """sym(u * lam**|i-j|) with u ~ U[-1, 1), built on `device` (torch tensor)."""
+    import torch
+
+    dtype = dtype or torch.float64
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    u = torch.empty((n, n), dtype=torch.float64, device=device)
+    u.uniform_(-1.0, 1.0, generator=g)
+    a = torch.empty((n, n), dtype=dtype, device=device)
+    idx = torch.arange(n, device=device, dtype=torch.float64)
+    for r0 in range(0, n, block):
+        r1 = min(n, r0 + block)
+        d = (idx[r0:r1, None] - idx[None, :]).abs_()
+        a[r0:r1] = (0.5 * (u[r0:r1] + u[:, r0:r1].T) * torch.pow(lam, d)).to(dtype)
+        del d
+    del u
+    return a
+
+
+def make_config_device(name, device, dtype=None):
+    cfg = DEVICE_CONFIGS[name]
+    a = exponential_decay_device(cfg["n"], cfg["lam"], cfg["seed"], device, dtype)
+    return a, a, cfg["leaf"], cfg["taus"]

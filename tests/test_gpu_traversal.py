@@ -1,4 +1,4 @@
-"""The dense single-pass traversal (depth <= 7) against the tiered
+"""The dense single-pass traversal (depth <= 6) against the tiered
 breadth-first kernel and the oracle: identical statistics, per-tier counts,
 pruned boxes (reference order), budget bits, retained triples and C, over
 depths 0..7, row shards, tau sweeps and tier tau decay."""
