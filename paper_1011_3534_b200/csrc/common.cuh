@@ -108,6 +108,7 @@ struct DeviceContext {
   Scratch grp_done;       // per-group finished-tile counters (zero at rest)
   Scratch lpt_order;      // groups by decreasing size (K3's work order)
   Scratch pw_part;        // budget: per-tier partial sums of the split recursion
+  Scratch grp_mark;       // non-empty C blocks (bitmask, zero at rest)
   size_t cull_capacity = 0;   // survivor capacity per ping-pong buffer (items)
   size_t pruned_capacity = 0; // pruned capacity (items, all tiers)
   void *host_pinned = nullptr;  // small pinned staging for counters

@@ -35,6 +35,59 @@ int finish_tree(DeviceContext *ctx, spamm_tree *t);
 void k1_timeline_enable(cudaStream_t st);
 void k1_timeline_dump(unsigned long long k3_end, unsigned long long k3_start);
 
+// ------------------------------------------------- C's empty blocks
+// K3 writes every C block that receives products; the others must be zero.
+// Instead of zero-filling all of C before K3 (at n = 65536 that is 34 GB of
+// writes in front of the product), these two kernels zero only the empty
+// blocks (and their leaf-level norm entries) on a side stream, concurrently
+// with K3.
+__global__ void mark_groups_kernel(const uint32_t *__restrict__ group_ids,
+                                   const unsigned *__restrict__ num_groups,
+                                   uint32_t *__restrict__ mark, int64_t G, unsigned cap) {
+  unsigned n = *num_groups;
+  if (n > cap) n = cap;
+  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const uint32_t g = group_ids[q];
+    if ((int64_t)g < G) atomicOr(&mark[g >> 5], 1u << (g & 31));
+  }
+}
+
+__global__ void zero_empty_kernel(unsigned char *__restrict__ padded, int64_t N, int32_t leaf,
+                                  int64_t nb, int esz, uint32_t *__restrict__ mark,
+                                  double *__restrict__ nsq_leaf, uint8_t *__restrict__ occ_leaf,
+                                  double *__restrict__ nrm_leaf) {
+  const int64_t G = nb * nb;
+  const int64_t w = blockIdx.x;
+  const uint32_t bits = mark[w];
+  const int64_t row_bytes = (int64_t)leaf * esz;
+  for (int b = 0; b < 32; ++b) {
+    const int64_t g = w * 32 + b;
+    if (g >= G || ((bits >> b) & 1u)) continue;  // uniform across the CTA
+    const int64_t bi = g / nb, bj = g - bi * nb;
+    unsigned char *base = padded + (bi * leaf) * N * esz + bj * row_bytes;
+    if (row_bytes % 16 == 0) {
+      const int per_row = (int)(row_bytes / 16);
+      for (int r = 0; r < leaf; ++r) {
+        uint4 *row = reinterpret_cast<uint4 *>(base + (int64_t)r * N * esz);
+        for (int c = threadIdx.x; c < per_row; c += blockDim.x) row[c] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    } else {
+      const int64_t total = row_bytes * leaf;
+      for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+        const int64_t r = e / row_bytes, c = e - r * row_bytes;
+        base[r * N * esz + c] = 0;
+      }
+    }
+    if (threadIdx.x == 0) {
+      nsq_leaf[g] = 0.0;
+      occ_leaf[g] = 0;
+      nrm_leaf[g] = 0.0;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) mark[w] = 0u;  // zero at rest
+}
+
 static int check_conformable(const spamm_tree *a, const spamm_tree *b) {
   // quadtree.py:209-215
   if (!a || !b) {
@@ -201,19 +254,39 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     ctx->counter_parity ^= 1;
     if (dense) ctx->dense_parity ^= 1;
     ++launches;
-    // C's zero fill runs on the side stream, under the traversal (issued
-    // after the cooperative launch so it cannot delay its residency)
-    SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
-    SPAMM_CUDA_BREAK(cudaMemsetAsync(c->padded, 0, (size_t)(c->N * c->N * c->elem_size()), ctx->side));
-    // C's leaf level: only blocks that receive products are recomputed below
-    SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nsq + level_offset(depth), 0, sizeof(double) * G, ctx->side));
-    SPAMM_CUDA_BREAK(cudaMemsetAsync(c->occ + level_offset(depth), 0, G, ctx->side));
-    SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nrm + level_offset(depth), 0, sizeof(double) * G, ctx->side));
-    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));
-    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
+    // C's zero fill on the side stream.  Small products: a memset of all of C
+    // under the traversal (hidden: 134 MB at c2).  Large products (c5: 34 GB,
+    // 5 ms of writes): only the empty blocks, once the group list exists,
+    // by single-warp CTAs that fit beside K3's CTAs -- concurrently with K3.
+    const bool big_c = (size_t)(c->N * c->N * c->elem_size()) > (size_t(2) << 30);
+    if (!big_c) {
+      SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));  // (fork: before the traversal)
+      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->padded, 0, (size_t)(c->N * c->N * c->elem_size()), ctx->side));
+      // C's leaf level: only blocks that receive products are recomputed below
+      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nsq + level_offset(depth), 0, sizeof(double) * G, ctx->side));
+      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->occ + level_offset(depth), 0, G, ctx->side));
+      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nrm + level_offset(depth), 0, sizeof(double) * G, ctx->side));
+      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));
+      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
+      SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));
+    } else {
+      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->fork, st));
+      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
+      SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
+      const int64_t words = (G + 31) / 32;
+      if ((rc = ensure_scratch(ctx->grp_mark, sizeof(uint32_t) * words, ctx->side, true))) break;
+      uint32_t *mark = (uint32_t *)ctx->grp_mark.ptr;
+      mark_groups_kernel<<<(unsigned)std::min<int64_t>((gcap + 255) / 256, 1024), 256, 0, ctx->side>>>(
+          ta.group_ids, &dtc->num_groups, mark, G, (unsigned)gcap);
+      zero_empty_kernel<<<(unsigned)words, 32, 0, ctx->side>>>(
+          (unsigned char *)c->padded, c->N, c->leaf, nb, (int)c->elem_size(), mark,
+          c->nsq + level_offset(depth), c->occ + level_offset(depth), c->nrm + level_offset(depth));
+      SPAMM_CUDA_BREAK(cudaGetLastError());
+      launches += 2;
+      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));
+    }
 
     // ------------------------------------------------ K3 leaf products -> C
-    SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[2], st));
     LeafArgs la{};
     la.a = a->padded;
@@ -252,8 +325,8 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     if (!overlapped) SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[3], st));
 
     // ------------------------------------------- C's tree (multiply.py:220)
-    // Overlapped: a programmatic dependent launch that starts once every K3
-    // CTA is resident and reads each C block as soon as K3 has stored it.
+    // (after the empty blocks are zero: the pyramid reads every leaf)
+    if (big_c) SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));
     {
       const int tile = a->leaf < 64 ? a->leaf : 64;
       const unsigned subs = (unsigned)((a->leaf / tile) * (a->leaf / tile));

