@@ -22,6 +22,10 @@
  *   spamm_stats               <- multiply.ProductStats        multiply.py:93-116
  *   spamm_product_boxes       <- ProductStats.boxes / PrunedBox multiply.py:77-90, :214-218
  *   spamm_tree_diff_norm      <- the dense norm in multiply_error  multiply.py:276
+ *   spamm_tree_add            <- quadtree.add                 quadtree.py:280-293
+ *   spamm_tree_scale          <- quadtree.scale               quadtree.py:296-299
+ *   spamm_tree_filter_drop    <- quadtree.filter_drop         quadtree.py:302-316
+ *   spamm_tree_diagonal       <- the diagonal of quadtree.trace quadtree.py:274-277
  *   spamm_multiply_rows       <- (new) output block-row shard of spamm for multi-GPU
  *                                partitioning; the reference is single-process.
  */
@@ -127,6 +131,22 @@ SPAMM_API int spamm_tree_pyramid_to_host(const spamm_tree *t, double *nsq, uint8
 SPAMM_API int spamm_tree_device_ptrs(const spamm_tree *t, void **padded, double **nsq, uint8_t **occ);
 /* ||A - B||_F computed on the device (multiply_error, multiply.py:276). */
 SPAMM_API int spamm_tree_diff_norm(const spamm_tree *a, const spamm_tree *b, double *out);
+
+/* ------------------------------------------------------------ tree algebra
+ * (the purification driver's element-wise operations; every result is a new
+ * tree with its pyramid rebuilt, bit-identical to the reference's numpy) */
+/* out = a + b; a block nonzero in only one operand is copied bit for bit
+ * (quadtree.py:280-293).  Status 2 (DimensionMismatchError) if not conformable. */
+SPAMM_API int spamm_tree_add(const spamm_tree *a, const spamm_tree *b, spamm_tree **out);
+/* out = m * dtype(s) element-wise (quadtree.py:296-299). */
+SPAMM_API int spamm_tree_scale(const spamm_tree *m, double s, spamm_tree **out);
+/* Leaves with rn(sqrt(norm_sq)) < tau zeroed (quadtree.py:302-316).  When no
+ * leaf drops, *dropped_any = 0 and *out = NULL: the input is the result. */
+SPAMM_API int spamm_tree_filter_drop(const spamm_tree *m, double tau, spamm_tree **out,
+                                     int32_t *dropped_any);
+/* The logical diagonal (n elements of the tree's dtype) to host memory, for
+ * trace = numpy add.reduce of it (quadtree.py:274-277). */
+SPAMM_API int spamm_tree_diagonal(const spamm_tree *m, void *host_out);
 SPAMM_API void spamm_tree_free(spamm_tree *t);
 
 /* -- multiply --------------------------------------------------------------- */

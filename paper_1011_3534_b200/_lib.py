@@ -91,6 +91,10 @@ def load(path=LIB_PATH):
         L.spamm_tree_pyramid_to_host.argtypes = [vp, vp, vp]
         L.spamm_tree_device_ptrs.argtypes = [vp, pp, pp, pp]
         L.spamm_tree_diff_norm.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_double)]
+        L.spamm_tree_add.argtypes = [vp, vp, pp]
+        L.spamm_tree_scale.argtypes = [vp, ctypes.c_double, pp]
+        L.spamm_tree_filter_drop.argtypes = [vp, ctypes.c_double, pp, ctypes.POINTER(i32)]
+        L.spamm_tree_diagonal.argtypes = [vp, vp]
         L.spamm_tree_free.argtypes = [vp]
         L.spamm_tree_free.restype = None
         L.spamm_multiply.argtypes = [vp, vp, ctypes.c_double, u32, pp, ctypes.POINTER(Stats), pp]

@@ -1,0 +1,221 @@
+// algebra.cu -- tree algebra on the device: add, scale, filter_drop and the
+// diagonal for trace (quadtree.py:269-322), the element-wise building blocks
+// of the purification driver (purification.py:115-142).
+//
+// Each result is a new tree whose pyramid is rebuilt by K1 (with the same
+// canonicalisation of all-zero leaves as every tree), so results are
+// bit-identical to the reference's numpy expressions:
+//   add      out = a + b, except that a block nonzero in only one operand is
+//            that operand's block, bit for bit (quadtree.py:283-293)
+//   scale    out = padded * dtype(s)                      (quadtree.py:296-299)
+//   filter   blocks with rn(sqrt(nsq)) < tau zeroed; the input itself when
+//            nothing drops                               (quadtree.py:302-316)
+//   trace    the diagonal, summed on the host with numpy's own add.reduce
+//            (quadtree.py:274-277: pairwise order, padded dtype)
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace spamm {
+
+int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out);
+void free_tree_async(spamm_tree *t, cudaStream_t st);
+int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
+                        const uint32_t *list, const unsigned *list_count, int64_t list_cap,
+                        unsigned *grp_done, unsigned grp_target, const int *overflow,
+                        unsigned long long *t_end);
+int finish_tree(DeviceContext *ctx, spamm_tree *t);
+
+// one row per CTA (grid-stride over rows), columns across the threads
+template <typename T>
+__global__ void add_kernel(const T *__restrict__ a, const T *__restrict__ b, T *__restrict__ out,
+                           int64_t N, int32_t leaf, int64_t nb, const uint8_t *__restrict__ oa,
+                           const uint8_t *__restrict__ ob) {
+  for (int64_t r = blockIdx.x; r < N; r += gridDim.x) {
+    const int64_t brow = (r / leaf) * nb;
+    const T *ar = a + r * N;
+    const T *br = b + r * N;
+    T *orow = out + r * N;
+    for (int64_t c = threadIdx.x; c < N; c += blockDim.x) {
+      const int64_t g = brow + c / leaf;
+      const bool na = oa[g], nbz = ob[g];
+      const T x = ar[c], y = br[c];
+      orow[c] = (na && !nbz) ? x : (!na && nbz) ? y : (T)(x + y);
+    }
+  }
+}
+
+template <typename T>
+__global__ void scale_kernel(const T *__restrict__ a, T *__restrict__ out, int64_t count, T s) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i] * s;
+}
+
+// leaves to drop: occupied and rn(sqrt(nsq)) < tau (the tree's cached nrm)
+__global__ void drop_mark_kernel(const uint8_t *__restrict__ occ, const double *__restrict__ nrm,
+                                 int64_t G, double tau, uint8_t *__restrict__ drop,
+                                 unsigned *__restrict__ count) {
+  unsigned local = 0;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const bool d = occ[g] && nrm[g] < tau;
+    drop[g] = d;
+    local += d;
+  }
+  for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
+template <typename T>
+__global__ void filter_kernel(const T *__restrict__ a, T *__restrict__ out, int64_t N, int32_t leaf,
+                              int64_t nb, const uint8_t *__restrict__ drop) {
+  for (int64_t r = blockIdx.x; r < N; r += gridDim.x) {
+    const int64_t brow = (r / leaf) * nb;
+    for (int64_t c = threadIdx.x; c < N; c += blockDim.x)
+      out[r * N + c] = drop[brow + c / leaf] ? T(0) : a[r * N + c];
+  }
+}
+
+static int grid_rows(DeviceContext *ctx, int64_t N) {
+  return (int)std::min<int64_t>(N, (int64_t)ctx->num_sms * 16);
+}
+
+static int finish_new(DeviceContext *ctx, spamm_tree *t, spamm_tree **out) {
+  int rc = build_pyramid_async(ctx, t, ctx->stream, nullptr, nullptr, nullptr, 0, nullptr, 0,
+                               nullptr, nullptr);
+  if (!rc) rc = finish_tree(ctx, t);
+  if (rc) {
+    free_tree_async(t, ctx->stream);
+    return rc;
+  }
+  *out = t;
+  return SPAMM_OK;
+}
+
+static int same_shape(const spamm_tree *a, const spamm_tree *b) {
+  if (!a || !b) {
+    set_error("null tree");
+    return SPAMM_ERR_VALUE;
+  }
+  if (a->n != b->n || a->leaf != b->leaf) {  // quadtree.py:209-215
+    set_error("trees not conformable: (%lld, leaf %d) vs (%lld, leaf %d)", (long long)a->n, a->leaf,
+              (long long)b->n, b->leaf);
+    return SPAMM_ERR_DIMENSION;
+  }
+  if (a->dtype != b->dtype || a->device != b->device) {
+    set_error("trees differ in dtype or device");
+    return SPAMM_ERR_VALUE;
+  }
+  return SPAMM_OK;
+}
+
+}  // namespace spamm
+
+using namespace spamm;
+
+extern "C" {
+
+SPAMM_API int spamm_tree_add(const spamm_tree *a, const spamm_tree *b, spamm_tree **out) {
+  SPAMM_TRY(same_shape(a, b));
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(a->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  spamm_tree *t = nullptr;
+  SPAMM_TRY(alloc_tree(ctx, a->n, a->leaf, a->dtype, &t));
+  const uint8_t *oa = a->occ + level_offset(a->depth), *ob = b->occ + level_offset(b->depth);
+  if (a->dtype == SPAMM_DTYPE_F64)
+    add_kernel<double><<<grid_rows(ctx, a->N), 256, 0, ctx->stream>>>(
+        (const double *)a->padded, (const double *)b->padded, (double *)t->padded, a->N, a->leaf,
+        a->nb, oa, ob);
+  else
+    add_kernel<float><<<grid_rows(ctx, a->N), 256, 0, ctx->stream>>>(
+        (const float *)a->padded, (const float *)b->padded, (float *)t->padded, a->N, a->leaf,
+        a->nb, oa, ob);
+  if (cudaGetLastError() != cudaSuccess) {
+    free_tree_async(t, ctx->stream);
+    set_error("add kernel launch failed");
+    return SPAMM_ERR_CUDA;
+  }
+  return finish_new(ctx, t, out);
+}
+
+SPAMM_API int spamm_tree_scale(const spamm_tree *m, double s, spamm_tree **out) {
+  if (!m) {
+    set_error("null tree");
+    return SPAMM_ERR_VALUE;
+  }
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(m->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  spamm_tree *t = nullptr;
+  SPAMM_TRY(alloc_tree(ctx, m->n, m->leaf, m->dtype, &t));
+  const int64_t count = m->N * m->N;
+  const int grid = (int)std::min<int64_t>((count + 255) / 256, (int64_t)ctx->num_sms * 32);
+  if (m->dtype == SPAMM_DTYPE_F64)
+    scale_kernel<double><<<grid, 256, 0, ctx->stream>>>((const double *)m->padded,
+                                                        (double *)t->padded, count, s);
+  else
+    scale_kernel<float><<<grid, 256, 0, ctx->stream>>>((const float *)m->padded, (float *)t->padded,
+                                                       count, (float)s);
+  if (cudaGetLastError() != cudaSuccess) {
+    free_tree_async(t, ctx->stream);
+    set_error("scale kernel launch failed");
+    return SPAMM_ERR_CUDA;
+  }
+  return finish_new(ctx, t, out);
+}
+
+SPAMM_API int spamm_tree_filter_drop(const spamm_tree *m, double tau, spamm_tree **out,
+                                     int32_t *dropped_any) {
+  if (!m) {
+    set_error("null tree");
+    return SPAMM_ERR_VALUE;
+  }
+  if (!(tau >= 0.0)) {  // quadtree.py:309-310
+    set_error("tau must be >= 0, got %g", tau);
+    return SPAMM_ERR_VALUE;
+  }
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(m->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const int64_t G = m->nb * m->nb;
+  SPAMM_TRY(ensure_scratch(ctx->reduce_tmp, (size_t)G + 64, ctx->stream));
+  uint8_t *drop = (uint8_t *)ctx->reduce_tmp.ptr + 64;
+  unsigned *count = (unsigned *)ctx->reduce_tmp.ptr;
+  SPAMM_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned), ctx->stream));
+  drop_mark_kernel<<<(unsigned)std::min<int64_t>((G + 255) / 256, 4096), 256, 0, ctx->stream>>>(
+      m->occ + level_offset(m->depth), m->nrm + level_offset(m->depth), G, tau, drop, count);
+  unsigned *hc = (unsigned *)ctx->host_pinned;
+  SPAMM_CUDA_TRY(cudaMemcpyAsync(hc, count, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  *dropped_any = *hc != 0;
+  *out = nullptr;
+  if (!*hc) return SPAMM_OK;  // nothing drops: the caller keeps the input tree
+  spamm_tree *t = nullptr;
+  SPAMM_TRY(alloc_tree(ctx, m->n, m->leaf, m->dtype, &t));
+  if (m->dtype == SPAMM_DTYPE_F64)
+    filter_kernel<double><<<grid_rows(ctx, m->N), 256, 0, ctx->stream>>>(
+        (const double *)m->padded, (double *)t->padded, m->N, m->leaf, m->nb, drop);
+  else
+    filter_kernel<float><<<grid_rows(ctx, m->N), 256, 0, ctx->stream>>>(
+        (const float *)m->padded, (float *)t->padded, m->N, m->leaf, m->nb, drop);
+  return finish_new(ctx, t, out);
+}
+
+SPAMM_API int spamm_tree_diagonal(const spamm_tree *m, void *host_out) {
+  if (!m || !host_out) {
+    set_error("null argument");
+    return SPAMM_ERR_VALUE;
+  }
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(m->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const int64_t esz = m->elem_size();
+  SPAMM_CUDA_TRY(cudaMemcpy2DAsync(host_out, (size_t)esz, m->padded, (size_t)((m->N + 1) * esz),
+                                   (size_t)esz, (size_t)m->n, cudaMemcpyDeviceToHost, ctx->stream));
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SPAMM_OK;
+}
+
+}  // extern "C"

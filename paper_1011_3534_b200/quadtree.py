@@ -301,6 +301,47 @@ def to_dense(m, out=None):
     return m.to_dense(out=out)
 
 
+def trace(m):
+    """Sum of the logical diagonal (quadtree.py:274-277): the diagonal comes
+    off the device and numpy's own add.reduce sums it (pairwise order, the
+    tree's dtype), so the value is the reference's bit for bit."""
+    d = np.empty(m.logical_dim, dtype=m.dtype)
+    _lib.check(_lib.load().spamm_tree_diagonal(m._handle, d.ctypes.data_as(ctypes.c_void_p)))
+    return float(np.add.reduce(d))
+
+
+def add(a, b):
+    """Tree sum a + b (quadtree.py:280-293): where only one operand has a
+    nonzero block that block passes through bit-identically; blocks that
+    cancel to zero become Empty."""
+    _require_conformable(a, b)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.load().spamm_tree_add(a._handle, b._handle, ctypes.byref(h)))
+    return _wrap(h.value)
+
+
+def scale(m, s):
+    """Tree scaled by a scalar in the tree's dtype (quadtree.py:296-299);
+    scaling by 0 yields the Empty tree."""
+    h = ctypes.c_void_p()
+    _lib.check(_lib.load().spamm_tree_scale(m._handle, float(m.dtype.type(s)), ctypes.byref(h)))
+    return _wrap(h.value)
+
+
+def filter_drop(m, tau):
+    """Drop every leaf whose Frobenius norm is < tau (quadtree.py:302-316);
+    returns ``m`` itself when nothing drops.  tau < 0 is rejected."""
+    if tau < 0:
+        raise ValueError(f"tau must be >= 0, got {tau}")
+    h = ctypes.c_void_p()
+    dropped = ctypes.c_int32(0)
+    _lib.check(_lib.load().spamm_tree_filter_drop(m._handle, float(tau), ctypes.byref(h),
+                                                  ctypes.byref(dropped)))
+    if not dropped.value:
+        return m
+    return _wrap(h.value)
+
+
 def node_norm(m):
     """Frobenius norm from the root's cached norm (quadtree.py:269-271)."""
     return m.norm()

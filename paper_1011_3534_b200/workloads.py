@@ -61,6 +61,58 @@ def make_config(name):
     return a, b, cfg["leaf"], cfg["taus"]
 
 
+# --------------------------------------------------- config 4: SP2 lattice
+def interleave3(x, y, z, bits):
+    """Morton index of lattice site (x, y, z), x-major in every 3-bit group
+    (the reference's ordering._interleave3 convention, ordering.py:24-34)."""
+    s = np.zeros_like(np.asarray(x), dtype=np.int64)
+    for b in range(bits):
+        s |= (((np.asarray(x) >> b) & 1) << (3 * b + 2)) | (((np.asarray(y) >> b) & 1) << (3 * b + 1)) \
+            | ((np.asarray(z) >> b) & 1) << (3 * b)
+    return s
+
+
+def cubic_lattice_hamiltonian(L, seed=0, hopping=-1.0, onsite=0.5):
+    """BASELINE config 4 / SURVEY.md §8(d): tight-binding Hamiltonian of an
+    L x L x L periodic cubic lattice (L a power of two), sites ordered along
+    the Morton curve (site s = interleave3(x, y, z), a bijection onto
+    [0, L^3)), nearest-neighbour hopping -1 (assigned, so L = 2's coinciding
+    neighbours are one bond), on-site energies default_rng(seed).uniform(
+    -onsite, onsite, n) indexed by s.  Dense float64 (host)."""
+    bits = int(L).bit_length() - 1
+    assert 1 << bits == L, "L must be a power of two"
+    n = L ** 3
+    h = np.zeros((n, n))
+    x, y, z = np.meshgrid(np.arange(L), np.arange(L), np.arange(L), indexing="ij")
+    x, y, z = x.ravel(), y.ravel(), z.ravel()
+    s = interleave3(x, y, z, bits)
+    for dx, dy, dz in ((1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)):
+        t = interleave3((x + dx) % L, (y + dy) % L, (z + dz) % L, bits)
+        h[s, t] = hopping
+    h[np.arange(n), np.arange(n)] = np.random.default_rng(seed).uniform(-onsite, onsite, n)
+    return h
+
+
+def cubic_lattice_hamiltonian_device(L, device, seed=0, hopping=-1.0, onsite=0.5):
+    """The same matrix built on the GPU (torch float64 tensor): the on-site
+    draw is numpy's (n values), the n x n fill happens on the device."""
+    import torch
+
+    bits = int(L).bit_length() - 1
+    n = L ** 3
+    h = torch.zeros((n, n), dtype=torch.float64, device=device)
+    x, y, z = np.meshgrid(np.arange(L), np.arange(L), np.arange(L), indexing="ij")
+    x, y, z = x.ravel(), y.ravel(), z.ravel()
+    s = torch.from_numpy(interleave3(x, y, z, bits)).to(device)
+    for dx, dy, dz in ((1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)):
+        t = torch.from_numpy(interleave3((x + dx) % L, (y + dy) % L, (z + dz) % L, bits)).to(device)
+        h[s, t] = hopping
+    d = torch.from_numpy(np.random.default_rng(seed).uniform(-onsite, onsite, n)).to(device)
+    idx = torch.arange(n, device=device)
+    h[idx, idx] = d
+    return h
+
+
 # ------------------------------------------------------------ on-device inputs
 # c5 (n = 65536) would need > 100 GB of host staging through numpy.  These
 # generators build the same formulas on the GPU with torch's Philox stream
