@@ -37,6 +37,7 @@ EXPORTED = (
     "spamm_tree_pyramid_to_host", "spamm_tree_device_ptrs", "spamm_tree_diff_norm",
     "spamm_tree_free", "spamm_multiply", "spamm_multiply_rows", "spamm_product_boxes",
     "spamm_product_triples", "spamm_product_free",
+    "spamm_tree_add", "spamm_tree_scale", "spamm_tree_filter_drop", "spamm_tree_diagonal",
 )
 
 
