@@ -135,6 +135,9 @@ def tree_from_padded(padded, n, leaf, device=None):
     from .quadtree import _wrap
 
     assert padded.is_cuda and padded.is_contiguous()
+    from .quadtree import _sync_torch
+
+    _sync_torch()  # torch's collectives/kernels that filled `padded` come first
     code = _lib.DTYPE_F64 if padded.dtype == __import__("torch").float64 else _lib.DTYPE_F32
     h = ctypes.c_void_p()
     dev = padded.device.index if device is None else device

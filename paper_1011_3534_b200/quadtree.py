@@ -276,9 +276,22 @@ def from_dense(dense, leaf_size=4, dtype=None, device=None):
     return _wrap(h.value)
 
 
+def _sync_torch():
+    """Order device data produced by torch (on its streams) before the
+    library's own stream reads it."""
+    import sys
+
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
+        torch.cuda.synchronize()
+
+
 def from_device_pointer(ptr, n, leaf_size=4, dtype=np.float64, device=None, ld=None):
     """Build a tree from an n x n array already resident in device memory
-    (e.g. a torch CUDA tensor's ``data_ptr()``); no host staging."""
+    (e.g. a torch CUDA tensor's ``data_ptr()``); no host staging.  The
+    library works on its own CUDA stream, so work queued by torch that
+    produces the array is waited for first."""
+    _sync_torch()
     target = np.dtype(dtype)
     if target not in _SUPPORTED_DTYPES:
         raise ValueError(f"unsupported element dtype {target}")
