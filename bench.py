@@ -368,10 +368,11 @@ def run_b200(args, cfg_name):
 def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
     """The same metric through the public API with host buffers.
 
-    Every step: pinned host A -> from_dense (H2D + K1 pyramid), one spamm per
-    tau, and the product back to pinned host memory.  With row shards each
-    rank multiplies its C block rows and reads back only its own row band
-    (bands partition C); wall time is the max over ranks."""
+    Every step: pinned host A (and B) -> from_dense (H2D + K1 pyramid), one
+    spamm per tau, and each product back to pinned host memory as its nonzero
+    leaf blocks and norm pyramid.  With row shards each rank multiplies its C
+    block rows and reads back only those (bands partition C); wall time is
+    the max over ranks."""
     import torch
 
     n = a_host.shape[0]
@@ -383,31 +384,32 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
     if not same:
         pin_b = torch.empty((n, n), dtype=tdt, pin_memory=True).numpy()
         pin_b[...] = b_host
-    if shard is None:
-        r0, r1 = 0, n
-    else:
-        r0, r1 = min(shard[0] * leaf, n), min(shard[1] * leaf, n)
-    pin_c = torch.empty((max(r1 - r0, 1), n), dtype=tdt, pin_memory=True)
+    # the product comes back as its nonzero leaf blocks (the tree's content;
+    # empty blocks are implicit zeros), in one transfer per multiply; with row
+    # shards each rank holds (and reads back) only its own block rows
+    nbk = -(-n // leaf)
+    G = (1 << (max(nbk - 1, 0)).bit_length()) ** 2
+    pin_blk = torch.empty((G, leaf, leaf), dtype=tdt, pin_memory=True).numpy()
     t0 = None
     e_f = 0.0
+    d2h = 0
     for it in range(args.warmup + args.steps):
         if it == args.warmup:
             torch.cuda.synchronize()
             if use_dist:
                 torch.distributed.barrier()
             t0 = time.perf_counter()
+            d2h = 0
         at = sp.from_dense(pin_a, leaf_size=leaf)
         bt = at if same else sp.from_dense(pin_b, leaf_size=leaf)
         f = 0.0
         for tau in taus:
             if shard is None:
                 c, st = sp.spamm(at, bt, sp.SpammConfig(tau=tau))
-                c.to_dense(out=pin_c.numpy())
             else:
-                from paper_1011_3534_b200 import distributed as spd
                 c, st, _ = sp.spamm_detailed(at, bt, sp.SpammConfig(tau=tau), rows=shard)
-                if r1 > r0:
-                    pin_c[: r1 - r0].copy_(spd.tree_storage(c)[r0:r1, :n])
+            ids, blocks = c.nonzero_blocks(out=pin_blk)
+            d2h += blocks.nbytes + ids.nbytes + c._pyramid()[2].nbytes + c._pyramid()[3].nbytes
             f += leaf_flops(leaf, st.leaf_matmuls)
             del c
         del at, bt
@@ -415,18 +417,19 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
             e_f += f
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
-    d2h = len(taus) * (r1 - r0) * n * esz
+    d2h = d2h // max(args.steps, 1)
     if use_dist:
-        t = torch.tensor([el, e_f], dtype=torch.float64, device="cuda")
+        t = torch.tensor([el, e_f, float(d2h)], dtype=torch.float64, device="cuda")
         mx = t[:1].clone()
         torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(t[1:])
-        el, e_f = float(mx.item()), float(t[1].item())
-        d2h = len(taus) * n * n * esz  # all bands together
+        el, e_f, d2h = float(mx.item()), float(t[1].item()), int(t[2].item())
     return {"value": e_f / el / 1e12, "unit": "TFLOP/s",
             "h2d_bytes_per_step": n * n * esz * (1 if same else 2) * (dist_world() if use_dist else 1),
             "d2h_bytes_per_step": d2h,
             "ms_per_step": el / args.steps * 1e3,
+            "result": "each product read back as its nonzero leaf blocks + norm pyramid "
+                      "(QuadTreeMatrix.nonzero_blocks)",
             "timing": "host wall clock around synchronous public-API calls (max over ranks)"}
 
 

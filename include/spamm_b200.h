@@ -26,6 +26,7 @@
  *   spamm_tree_scale          <- quadtree.scale               quadtree.py:296-299
  *   spamm_tree_filter_drop    <- quadtree.filter_drop         quadtree.py:302-316
  *   spamm_tree_diagonal       <- the diagonal of quadtree.trace quadtree.py:274-277
+ *   spamm_tree_blocks_to_host <- _blocks[_leaf_nonzero]       quadtree.py:120-151
  *   spamm_multiply_rows       <- (new) output block-row shard of spamm for multi-GPU
  *                                partitioning; the reference is single-process.
  */
@@ -144,6 +145,12 @@ SPAMM_API int spamm_tree_scale(const spamm_tree *m, double s, spamm_tree **out);
  * leaf drops, *dropped_any = 0 and *out = NULL: the input is the result. */
 SPAMM_API int spamm_tree_filter_drop(const spamm_tree *m, double tau, spamm_tree **out,
                                      int32_t *dropped_any);
+/* The listed leaves (ids: leaf indices i * block_grid + j) copied to host
+ * memory as a contiguous [count][leaf][leaf] array in one transfer -- the
+ * nonzero blocks of a tree (the reference's _blocks[_leaf_nonzero],
+ * quadtree.py:120-151) without moving its empty blocks. */
+SPAMM_API int spamm_tree_blocks_to_host(const spamm_tree *m, const int64_t *ids, int64_t count,
+                                        void *host_out);
 /* The logical diagonal (n elements of the tree's dtype) to host memory, for
  * trace = numpy add.reduce of it (quadtree.py:274-277). */
 SPAMM_API int spamm_tree_diagonal(const spamm_tree *m, void *host_out);

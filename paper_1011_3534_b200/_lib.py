@@ -38,6 +38,7 @@ EXPORTED = (
     "spamm_tree_free", "spamm_multiply", "spamm_multiply_rows", "spamm_product_boxes",
     "spamm_product_triples", "spamm_product_free",
     "spamm_tree_add", "spamm_tree_scale", "spamm_tree_filter_drop", "spamm_tree_diagonal",
+    "spamm_tree_blocks_to_host",
 )
 
 
@@ -96,6 +97,7 @@ def load(path=LIB_PATH):
         L.spamm_tree_scale.argtypes = [vp, ctypes.c_double, pp]
         L.spamm_tree_filter_drop.argtypes = [vp, ctypes.c_double, pp, ctypes.POINTER(i32)]
         L.spamm_tree_diagonal.argtypes = [vp, vp]
+        L.spamm_tree_blocks_to_host.argtypes = [vp, vp, i64, vp]
         L.spamm_tree_free.argtypes = [vp]
         L.spamm_tree_free.restype = None
         L.spamm_multiply.argtypes = [vp, vp, ctypes.c_double, u32, pp, ctypes.POINTER(Stats), pp]

@@ -77,6 +77,30 @@ __global__ void filter_kernel(const T *__restrict__ a, T *__restrict__ out, int6
   }
 }
 
+// copy the listed leaves into a contiguous [count][b][b] buffer
+__global__ void gather_blocks_kernel(const unsigned char *__restrict__ padded, int64_t N, int32_t leaf,
+                                     int64_t nb, int esz, const int64_t *__restrict__ ids,
+                                     unsigned char *__restrict__ out) {
+  const int64_t q = blockIdx.x;
+  const int64_t g = ids[q], bi = g / nb, bj = g - bi * nb;
+  const int64_t row_bytes = (int64_t)leaf * esz;
+  const unsigned char *src = padded + (bi * leaf) * N * esz + bj * row_bytes;
+  unsigned char *dst = out + q * row_bytes * leaf;
+  if (row_bytes % 16 == 0) {
+    const int per_row = (int)(row_bytes / 16);
+    for (int e = threadIdx.x; e < per_row * leaf; e += blockDim.x) {
+      const int r = e / per_row, c = e - r * per_row;
+      reinterpret_cast<uint4 *>(dst + r * row_bytes)[c] =
+          reinterpret_cast<const uint4 *>(src + (int64_t)r * N * esz)[c];
+    }
+  } else {
+    for (int64_t e = threadIdx.x; e < row_bytes * leaf; e += blockDim.x) {
+      const int64_t r = e / row_bytes, c = e - r * row_bytes;
+      dst[e] = src[r * N * esz + c];
+    }
+  }
+}
+
 static int grid_rows(DeviceContext *ctx, int64_t N) {
   return (int)std::min<int64_t>(N, (int64_t)ctx->num_sms * 16);
 }
@@ -201,6 +225,33 @@ SPAMM_API int spamm_tree_filter_drop(const spamm_tree *m, double tau, spamm_tree
     filter_kernel<float><<<grid_rows(ctx, m->N), 256, 0, ctx->stream>>>(
         (const float *)m->padded, (float *)t->padded, m->N, m->leaf, m->nb, drop);
   return finish_new(ctx, t, out);
+}
+
+SPAMM_API int spamm_tree_blocks_to_host(const spamm_tree *m, const int64_t *ids, int64_t count,
+                                        void *host_out) {
+  if (!m || (count && (!ids || !host_out)) || count < 0) {
+    set_error("null argument");
+    return SPAMM_ERR_VALUE;
+  }
+  if (!count) return SPAMM_OK;
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(m->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const int64_t esz = m->elem_size(), bytes = count * m->leaf * m->leaf * esz;
+  SPAMM_TRY(ensure_scratch(ctx->reduce_tmp, (size_t)(bytes + count * 8 + 256), ctx->stream));
+  int64_t *dids = (int64_t *)ctx->reduce_tmp.ptr;
+  unsigned char *dbuf = (unsigned char *)ctx->reduce_tmp.ptr + ((count * 8 + 255) / 256) * 256;
+  SPAMM_CUDA_TRY(cudaMemcpyAsync(dids, ids, count * 8, cudaMemcpyHostToDevice, ctx->stream));
+  for (int64_t q = 0; q < count; q += 65535) {
+    const int64_t k = std::min<int64_t>(65535, count - q);
+    gather_blocks_kernel<<<(unsigned)k, 256, 0, ctx->stream>>>(
+        (const unsigned char *)m->padded, m->N, m->leaf, m->nb, (int)esz, dids + q,
+        dbuf + q * m->leaf * m->leaf * esz);
+  }
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  SPAMM_CUDA_TRY(cudaMemcpyAsync(host_out, dbuf, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SPAMM_OK;
 }
 
 SPAMM_API int spamm_tree_diagonal(const spamm_tree *m, void *host_out) {

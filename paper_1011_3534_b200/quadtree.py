@@ -202,6 +202,24 @@ class QuadTreeMatrix:
         return self._occupied[self.depth]
 
     # -- queries --------------------------------------------------------------
+    def nonzero_blocks(self, out=None):
+        """(ids, blocks): the tree's nonzero leaves -- the reference's
+        ``_blocks[_leaf_nonzero]`` with their indices i * block_grid + j in
+        ascending order -- read back in one transfer (extension: the product
+        without its empty blocks).  ``out``: optional C-contiguous
+        (>= count, b, b) host array of the tree's dtype (e.g. pinned)."""
+        occ = np.asarray(self._occupied[self.depth]).reshape(-1)
+        ids = np.flatnonzero(occ).astype(np.int64)
+        b = self.leaf_size
+        if out is None:
+            out = np.empty((len(ids), b, b), dtype=self.dtype)
+        elif (out.dtype != self.dtype or out.ndim != 3 or out.shape[1:] != (b, b)
+              or out.shape[0] < len(ids) or not out.flags.c_contiguous):
+            raise ValueError("out must be a C-contiguous (>= count, b, b) array of the tree dtype")
+        _lib.check(_lib.load().spamm_tree_blocks_to_host(self._handle, ids.ctypes.data, len(ids),
+                                                         out.ctypes.data))
+        return ids, out[:len(ids)]
+
     def to_dense(self, out=None):
         """Fresh n x n host array with the padding stripped (quadtree.py:184-187).
 

@@ -313,3 +313,26 @@ def test_c5_full_size_symmetric_product():
             assert torch.equal(x, y), ("C not symmetric", r0, c0)
     # C's root norm agrees with the blocks' norms (pyramid over the product)
     assert c.norm() > 0
+
+
+@pytest.mark.gpu
+def test_nonzero_blocks_match_padded():
+    rng = np.random.default_rng(5)
+    n, leaf = 200, 16
+    x = rng.uniform(-1, 1, (n, n))
+    x[:48, :] = 0.0
+    x[:, 100:150] = 0.0
+    t = sp.from_dense(x, leaf_size=leaf)
+    ids, blocks = t.nonzero_blocks()
+    occ = np.asarray(t._leaf_nonzero).reshape(-1)
+    assert np.array_equal(ids, np.flatnonzero(occ))
+    ref = np.asarray(t._blocks).reshape(-1, leaf, leaf)[ids]
+    assert np.array_equal(blocks.view(np.uint64), ref.view(np.uint64))
+    c, _ = sp.spamm(t, t, sp.SpammConfig(tau=1e-3))
+    ids, blocks = c.nonzero_blocks()
+    dense = np.zeros((c.padded_dim, c.padded_dim))
+    nb = c.block_grid
+    for g, blk in zip(ids, blocks):
+        i, j = divmod(int(g), nb)
+        dense[i * leaf:(i + 1) * leaf, j * leaf:(j + 1) * leaf] = blk
+    assert np.array_equal(dense, c._padded)
