@@ -312,12 +312,12 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     // per-group completion counters let C's norm kernel overlap K3
     if ((rc = ensure_scratch(ctx->grp_done, sizeof(unsigned) * G, st, /*zeroed=*/true))) break;
     la.grp_done = (unsigned *)ctx->grp_done.ptr;
-    // The overlapped C tree (programmatic dependent launch of K1 beside K3)
-    // is opt-in: measured on B200, K1 CTAs cannot co-reside with K3 CTAs
-    // (per-SMSP register budget of K3's 17 warps x 96 registers), so they
-    // only start as K3 CTAs retire and the overlap does not pay.
-    static const bool overlap = getenv("SPAMM_CTREE_OVERLAP") != nullptr;
-    if (!overlap) la.grp_done = nullptr;
+    // The C tree overlaps K3's tail: K1 is a programmatic dependent launch
+    // whose CTAs (one per SM) start on the SMs K3's CTAs vacate and read each
+    // C block once K3 has stored it (per-group counters), instead of waiting
+    // for K3's grid to complete (c2: C tree 35-37 us after K3, was 45-49).
+    static const bool no_overlap = getenv("SPAMM_NO_CTREE_OVERLAP") != nullptr;
+    if (no_overlap) la.grp_done = nullptr;
     static const bool k1tl = getenv("SPAMM_K1_TIMELINE") != nullptr;
     if (k1tl) k1_timeline_enable(st);
     bool overlapped = false;

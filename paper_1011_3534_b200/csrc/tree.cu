@@ -728,6 +728,15 @@ static int launch_staged(spamm_tree *t, cudaStream_t st, const uint32_t *list,
   cfg.gridDim = dim3((unsigned)((n_leaves + LT - 1) / LT));
   cfg.blockDim = dim3(K1_THREADS);
   cfg.dynamicSmemBytes = smem;
+  if (ov && ov->grp_done) {
+    // one CTA per SM (the padding makes a second one not fit): the CTAs start
+    // on SMs as the leaf kernel's CTAs retire and must not pile onto the
+    // first ones (measured: 35-37 us vs 44-45 us with 60 KB, two per SM)
+    static const size_t pad = (size_t)120 << 10;
+    cfg.dynamicSmemBytes = std::max(smem, pad);
+    SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)cfg.dynamicSmemBytes));
+  }
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   if (ov && (ov->grp_done || ov->pdl)) {
@@ -757,7 +766,7 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
     if (ov && ov->grp_done)
-      SPAMM_TRY((launch_staged<T, 4, 8>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
+      SPAMM_TRY((launch_staged<T, 12, 8>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
     else if (n_leaves >= (int64_t)64 * sms)
       SPAMM_TRY((launch_staged<T, 6, 32>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
     else
