@@ -128,7 +128,8 @@ SPAMM_API int spamm_tree_padded_to_host(const spamm_tree *t, void *host);
 /* nsq: (4^(depth+1)-1)/3 doubles, occ: same count of bytes; level k
  * (2^k x 2^k row-major) starts at (4^k - 1)/3. */
 SPAMM_API int spamm_tree_pyramid_to_host(const spamm_tree *t, double *nsq, uint8_t *occ);
-/* Raw device pointers (borrowed) for collective plumbing. */
+/* Raw device pointers (borrowed) for collective plumbing (a band tree's
+ * storage outside its rows is undefined; see spamm_multiply_rows). */
 SPAMM_API int spamm_tree_device_ptrs(const spamm_tree *t, void **padded, double **nsq, uint8_t **occ);
 /* ||A - B||_F computed on the device (multiply_error, multiply.py:276). */
 SPAMM_API int spamm_tree_diff_norm(const spamm_tree *a, const spamm_tree *b, double *out);
@@ -162,8 +163,12 @@ SPAMM_API int spamm_multiply(const spamm_tree *a, const spamm_tree *b, double ta
 /* Shard of spamm_multiply restricted to C leaf block rows [row_lo, row_hi):
  * only triples whose leaf rows intersect the range are traversed; pruned and
  * skipped calls are counted by the shard owning the call's first row, so the
- * per-shard integer stats sum exactly to the unsharded ones.  C holds only
- * the shard's rows (others +0.0); its pyramid covers those rows. */
+ * per-shard integer stats sum exactly to the unsharded ones.  C is a band
+ * tree: only the shard's rows are computed and stored; the others are zero
+ * by definition (zero norms) and are zero-filled on the first whole-storage
+ * read (to_host, padded_to_host, diff_norm, tree algebra) -- so a shard
+ * never writes the other ranks' rows.  spamm_tree_device_ptrs hands out the
+ * raw storage, where those rows are undefined until then. */
 SPAMM_API int spamm_multiply_rows(const spamm_tree *a, const spamm_tree *b, double tau, uint32_t flags,
                         int64_t row_lo, int64_t row_hi, spamm_tree **c, spamm_stats *stats,
                         spamm_product **product);

@@ -145,6 +145,8 @@ SPAMM_API int spamm_tree_add(const spamm_tree *a, const spamm_tree *b, spamm_tre
   DeviceContext *ctx;
   SPAMM_TRY(get_context(a->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(materialize(ctx, a));
+  SPAMM_TRY(materialize(ctx, b));
   spamm_tree *t = nullptr;
   SPAMM_TRY(alloc_tree(ctx, a->n, a->leaf, a->dtype, &t));
   const uint8_t *oa = a->occ + level_offset(a->depth), *ob = b->occ + level_offset(b->depth);
@@ -172,6 +174,7 @@ SPAMM_API int spamm_tree_scale(const spamm_tree *m, double s, spamm_tree **out) 
   DeviceContext *ctx;
   SPAMM_TRY(get_context(m->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(materialize(ctx, m));
   spamm_tree *t = nullptr;
   SPAMM_TRY(alloc_tree(ctx, m->n, m->leaf, m->dtype, &t));
   const int64_t count = m->N * m->N;
@@ -203,6 +206,7 @@ SPAMM_API int spamm_tree_filter_drop(const spamm_tree *m, double tau, spamm_tree
   DeviceContext *ctx;
   SPAMM_TRY(get_context(m->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(materialize(ctx, m));
   const int64_t G = m->nb * m->nb;
   SPAMM_TRY(ensure_scratch(ctx->reduce_tmp, (size_t)G + 64, ctx->stream));
   uint8_t *drop = (uint8_t *)ctx->reduce_tmp.ptr + 64;
@@ -262,6 +266,7 @@ SPAMM_API int spamm_tree_diagonal(const spamm_tree *m, void *host_out) {
   DeviceContext *ctx;
   SPAMM_TRY(get_context(m->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(materialize(ctx, m));
   const int64_t esz = m->elem_size();
   SPAMM_CUDA_TRY(cudaMemcpy2DAsync(host_out, (size_t)esz, m->padded, (size_t)((m->N + 1) * esz),
                                    (size_t)esz, (size_t)m->n, cudaMemcpyDeviceToHost, ctx->stream));

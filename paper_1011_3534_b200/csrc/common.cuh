@@ -132,5 +132,16 @@ struct spamm_tree {
   uint8_t *occ = nullptr;   // concatenated occupancy pyramid
   double *nrm = nullptr;    // rn(sqrt(nsq)): the factors of the pruning test
   double root_norm_sq = 0.0;
+  // Band trees (a row-sharded product): only leaf rows [valid_lo, valid_hi)
+  // of `padded` were written; the rest is zero by definition (its norms are
+  // zero) and is zero-filled on first whole-storage access (materialize()).
+  // valid_hi < 0: all storage defined.
+  int64_t valid_lo = 0, valid_hi = -1;
   int64_t elem_size() const { return dtype == SPAMM_DTYPE_F64 ? 8 : 4; }
 };
+
+namespace spamm {
+struct DeviceContext;
+// zero-fill a band tree's undefined rows (stream-ordered on ctx->stream)
+int materialize(DeviceContext *ctx, const spamm_tree *t);
+}  // namespace spamm

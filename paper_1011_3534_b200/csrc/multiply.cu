@@ -55,7 +55,7 @@ __global__ void mark_groups_kernel(const uint32_t *__restrict__ group_ids,
 __global__ void zero_empty_kernel(unsigned char *__restrict__ padded, int64_t N, int32_t leaf,
                                   int64_t nb, int esz, uint32_t *__restrict__ mark,
                                   double *__restrict__ nsq_leaf, uint8_t *__restrict__ occ_leaf,
-                                  double *__restrict__ nrm_leaf) {
+                                  double *__restrict__ nrm_leaf, int64_t row_lo, int64_t row_hi) {
   const int64_t G = nb * nb;
   const int64_t w = blockIdx.x;
   const uint32_t bits = mark[w];
@@ -64,6 +64,12 @@ __global__ void zero_empty_kernel(unsigned char *__restrict__ padded, int64_t N,
     const int64_t g = w * 32 + b;
     if (g >= G || ((bits >> b) & 1u)) continue;  // uniform across the CTA
     const int64_t bi = g / nb, bj = g - bi * nb;
+    if (threadIdx.x == 0) {
+      nsq_leaf[g] = 0.0;
+      occ_leaf[g] = 0;
+      nrm_leaf[g] = 0.0;
+    }
+    if (bi < row_lo || bi >= row_hi) continue;  // outside a band tree's rows: never read
     unsigned char *base = padded + (bi * leaf) * N * esz + bj * row_bytes;
     if (row_bytes % 16 == 0) {
       const int per_row = (int)(row_bytes / 16);
@@ -77,11 +83,6 @@ __global__ void zero_empty_kernel(unsigned char *__restrict__ padded, int64_t N,
         const int64_t r = e / row_bytes, c = e - r * row_bytes;
         base[r * N * esz + c] = 0;
       }
-    }
-    if (threadIdx.x == 0) {
-      nsq_leaf[g] = 0.0;
-      occ_leaf[g] = 0;
-      nrm_leaf[g] = 0.0;
     }
   }
   __syncthreads();
@@ -258,10 +259,21 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     // under the traversal (hidden: 134 MB at c2).  Large products (c5: 34 GB,
     // 5 ms of writes): only the empty blocks, once the group list exists,
     // by single-warp CTAs that fit beside K3's CTAs -- concurrently with K3.
-    const bool big_c = (size_t)(c->N * c->N * c->elem_size()) > (size_t(2) << 30);
+    // A row-sharded product is a band tree: only its block rows are zeroed and
+    // written; the rest is zero by definition and filled only if the whole
+    // storage is ever read (materialize()).
+    const bool band = row_lo > 0 || row_hi < nb;
+    const int64_t band_r0 = row_lo * c->leaf, band_r1 = std::min<int64_t>(row_hi * c->leaf, c->N);
+    const size_t band_bytes = (size_t)((band_r1 - band_r0) * c->N * c->elem_size());
+    const bool big_c = band_bytes > (size_t(2) << 30);
+    if (band) {
+      c->valid_lo = row_lo;
+      c->valid_hi = row_hi;
+    }
     if (!big_c) {
       SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));  // (fork: before the traversal)
-      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->padded, 0, (size_t)(c->N * c->N * c->elem_size()), ctx->side));
+      SPAMM_CUDA_BREAK(cudaMemsetAsync((char *)c->padded + band_r0 * c->N * c->elem_size(), 0,
+                                       band_bytes, ctx->side));
       // C's leaf level: only blocks that receive products are recomputed below
       SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nsq + level_offset(depth), 0, sizeof(double) * G, ctx->side));
       SPAMM_CUDA_BREAK(cudaMemsetAsync(c->occ + level_offset(depth), 0, G, ctx->side));
@@ -280,7 +292,8 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
           ta.group_ids, &dtc->num_groups, mark, G, (unsigned)gcap);
       zero_empty_kernel<<<(unsigned)words, 32, 0, ctx->side>>>(
           (unsigned char *)c->padded, c->N, c->leaf, nb, (int)c->elem_size(), mark,
-          c->nsq + level_offset(depth), c->occ + level_offset(depth), c->nrm + level_offset(depth));
+          c->nsq + level_offset(depth), c->occ + level_offset(depth), c->nrm + level_offset(depth),
+          row_lo, row_hi);
       SPAMM_CUDA_BREAK(cudaGetLastError());
       launches += 2;
       SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));

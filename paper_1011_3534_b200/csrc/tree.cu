@@ -875,6 +875,19 @@ void free_tree_async(spamm_tree *t, cudaStream_t st) {
   delete t;
 }
 
+int materialize(DeviceContext *ctx, const spamm_tree *tc) {
+  spamm_tree *t = const_cast<spamm_tree *>(tc);  // the values (zeros) do not change
+  if (t->valid_hi < 0) return SPAMM_OK;
+  const int64_t esz = t->elem_size(), row = t->N * esz;
+  const int64_t r0 = t->valid_lo * t->leaf, r1 = std::min<int64_t>(t->valid_hi * t->leaf, t->N);
+  if (r0 > 0) SPAMM_CUDA_TRY(cudaMemsetAsync(t->padded, 0, (size_t)(r0 * row), ctx->stream));
+  if (r1 < t->N)
+    SPAMM_CUDA_TRY(cudaMemsetAsync((char *)t->padded + r1 * row, 0, (size_t)((t->N - r1) * row),
+                                   ctx->stream));
+  t->valid_hi = -1;
+  return SPAMM_OK;
+}
+
 int finish_tree(DeviceContext *ctx, spamm_tree *t) {
   SPAMM_CUDA_TRY(cudaMemcpyAsync(&t->root_norm_sq, t->nsq, sizeof(double), cudaMemcpyDeviceToHost,
                                  ctx->stream));
@@ -1027,6 +1040,7 @@ int spamm_tree_to_host(const spamm_tree *t, void *host, int64_t ld) {
   DeviceContext *ctx;
   SPAMM_TRY(get_context(t->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(materialize(ctx, t));
   const int64_t esz = t->elem_size();
   SPAMM_CUDA_TRY(cudaMemcpy2DAsync(host, (size_t)(ld * esz), t->padded, (size_t)(t->N * esz),
                                    (size_t)(t->n * esz), (size_t)t->n, cudaMemcpyDeviceToHost,
@@ -1040,6 +1054,7 @@ int spamm_tree_padded_to_host(const spamm_tree *t, void *host) {
   DeviceContext *ctx;
   SPAMM_TRY(get_context(t->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(materialize(ctx, t));
   SPAMM_CUDA_TRY(cudaMemcpyAsync(host, t->padded, (size_t)(t->N * t->N * t->elem_size()),
                                  cudaMemcpyDeviceToHost, ctx->stream));
   SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -1076,6 +1091,8 @@ int spamm_tree_diff_norm(const spamm_tree *a, const spamm_tree *b, double *out) 
   DeviceContext *ctx;
   SPAMM_TRY(get_context(a->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(materialize(ctx, a));
+  SPAMM_TRY(materialize(ctx, b));
   const int blocks = ctx->num_sms * 4;
   SPAMM_TRY(ensure_scratch(ctx->reduce_tmp, sizeof(double) * (blocks + 1), ctx->stream));
   double *part = (double *)ctx->reduce_tmp.ptr;
