@@ -64,11 +64,6 @@ __global__ void zero_empty_kernel(unsigned char *__restrict__ padded, int64_t N,
     const int64_t g = w * 32 + b;
     if (g >= G || ((bits >> b) & 1u)) continue;  // uniform across the CTA
     const int64_t bi = g / nb, bj = g - bi * nb;
-    if (threadIdx.x == 0) {
-      nsq_leaf[g] = 0.0;
-      occ_leaf[g] = 0;
-      nrm_leaf[g] = 0.0;
-    }
     if (bi < row_lo || bi >= row_hi) continue;  // outside a band tree's rows: never read
     unsigned char *base = padded + (bi * leaf) * N * esz + bj * row_bytes;
     if (row_bytes % 16 == 0) {
@@ -282,6 +277,12 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
       SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));
     } else {
+      // leaf-level norms of C on the main stream (small; K1's pyramid reads
+      // them); the block data on the side stream, joined after K1 (no event
+      // wait may sit between K3 and its programmatic dependent K1)
+      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nsq + level_offset(depth), 0, sizeof(double) * G, st));
+      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->occ + level_offset(depth), 0, G, st));
+      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nrm + level_offset(depth), 0, sizeof(double) * G, st));
       SPAMM_CUDA_BREAK(cudaEventRecord(ctx->fork, st));
       SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
       SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
@@ -329,8 +330,11 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     // whose CTAs (one per SM) start on the SMs K3's CTAs vacate and read each
     // C block once K3 has stored it (per-group counters), instead of waiting
     // for K3's grid to complete (c2: C tree 35-37 us after K3, was 45-49).
+    // Only for small block grids: the overlapped K1 runs one 8-leaf CTA per
+    // SM, which suits ~1k C blocks (c2) but not 10^4-10^6 (c3, c5), where the
+    // regular K1 (32 leaves per CTA, two per SM) finishes in fewer waves.
     static const bool no_overlap = getenv("SPAMM_NO_CTREE_OVERLAP") != nullptr;
-    if (no_overlap) la.grp_done = nullptr;
+    if (no_overlap || G > 4096) la.grp_done = nullptr;
     static const bool k1tl = getenv("SPAMM_K1_TIMELINE") != nullptr;
     if (k1tl) k1_timeline_enable(st);
     bool overlapped = false;
@@ -338,8 +342,6 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     if (!overlapped) SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[3], st));
 
     // ------------------------------------------- C's tree (multiply.py:220)
-    // (after the empty blocks are zero: the pyramid reads every leaf)
-    if (big_c) SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));
     {
       const int tile = a->leaf < 64 ? a->leaf : 64;
       const unsigned subs = (unsigned)((a->leaf / tile) * (a->leaf / tile));
@@ -349,6 +351,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
         break;
     }
     ctx->last_overlapped = overlapped;
+    if (big_c) SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));  // C's empty blocks
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
     SPAMM_CUDA_BREAK(cudaMemcpyAsync(hc, dtc, sizeof(TraverseCounters), cudaMemcpyDeviceToHost, st));
     SPAMM_CUDA_BREAK(cudaMemcpyAsync(&c->root_norm_sq, c->nsq, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -454,17 +457,22 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   if (tail_dbg && cc.k3_t1 && cc.k1_t1)
     fprintf(stderr, "[tail] k3 span %.1f us, C tree done %.1f us after K3\n",
             (double)(cc.k3_t1 - ~cc.k3_t0n) * 1e-3, ((double)cc.k1_t1 - (double)cc.k3_t1) * 1e-3);
-  if (ctx->last_overlapped && cc.k3_t0n && cc.k3_t1 && cc.k1_t1 > cc.k3_t1) {
+  if (ctx->last_overlapped && cc.k3_t0n && cc.k3_t1) {
     // K3 and the C tree overlap (no event can sit between them): K3's span
-    // and the C tree's tail after it from the kernels' own %globaltimer stamps
+    // from its own %globaltimer stamps; the C tree's tail after it from K1's
+    // stamp when the pyramid is fused into K1, else the rest of the multiply
     s.ms_gemm = (float)((double)(cc.k3_t1 - ~cc.k3_t0n) * 1e-6);
     s.ms_leaf = s.ms_gemm;
-    s.ms_ctree = (float)((double)(cc.k1_t1 - cc.k3_t1) * 1e-6);
+    if (cc.k1_t1 > cc.k3_t1)
+      s.ms_ctree = (float)((double)(cc.k1_t1 - cc.k3_t1) * 1e-6);
+    else
+      s.ms_ctree = std::max(0.f, s.ms_total - s.ms_cull - s.ms_gemm);
   } else {
     cudaEventElapsedTime(&s.ms_leaf, ctx->ev[1], ctx->ev[3]);
     cudaEventElapsedTime(&s.ms_gemm, ctx->ev[2], ctx->ev[3]);
     cudaEventElapsedTime(&s.ms_ctree, ctx->ev[3], ctx->ev[4]);
   }
+  (void)cudaGetLastError();  // (timing queries must not leave an error for the next call)
 
   // ------------------------------------------------------- product records
   if (product) {
