@@ -95,7 +95,8 @@ def test_dense_vs_oracle_with_empty_blocks():
 
 def test_repeated_calls_leave_state_clean():
     # alternating depths / traversal kernels must not leak state between calls
-    mats = [(sp.from_dense(_decay(n, n), leaf_size=16), n) for n in (1024, 128, 512, 16, 1024)]
+    # (4096 at leaf 16 is depth 8: tiered traversal, separate pyramid kernel)
+    mats = [(sp.from_dense(_decay(n, n), leaf_size=16), n) for n in (1024, 128, 4096, 512, 16, 1024)]
     ref = {}
     for rep in range(3):
         for a, n in mats:
