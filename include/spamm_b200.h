@@ -21,12 +21,18 @@
  *                                (_leaf_stage :224-257, _merge_contributions :119-141)
  *   spamm_stats               <- multiply.ProductStats        multiply.py:93-116
  *   spamm_product_boxes       <- ProductStats.boxes / PrunedBox multiply.py:77-90, :214-218
+ *   spamm_tree_recompute_norms<- the fresh norms of audit_norm_cache quadtree.py:325-340
  *   spamm_tree_diff_norm      <- the dense norm in multiply_error  multiply.py:276
  *   spamm_tree_add            <- quadtree.add                 quadtree.py:280-293
  *   spamm_tree_scale          <- quadtree.scale               quadtree.py:296-299
  *   spamm_tree_filter_drop    <- quadtree.filter_drop         quadtree.py:302-316
  *   spamm_tree_diagonal       <- the diagonal of quadtree.trace quadtree.py:274-277
  *   spamm_tree_blocks_to_host <- _blocks[_leaf_nonzero]       quadtree.py:120-151
+ *   spamm_boxes_morton_order  <- the sort in write_box_log     multiply.py:306-315
+ *                                (key: ordering._interleave3   ordering.py:24-34)
+ *   spamm_tree_toeplitz       <- generators.gen_exponential / gen_algebraic
+ *                                                              generators.py:24-43
+ *   spamm_tree_tridiagonal    <- generators.gen_model_hamiltonian generators.py:76-88
  *   spamm_multiply_rows       <- (new) output block-row shard of spamm for multi-GPU
  *                                partitioning; the reference is single-process.
  */
@@ -130,6 +136,10 @@ SPAMM_API int spamm_tree_padded_to_host(const spamm_tree *t, void *host);
 SPAMM_API int spamm_tree_pyramid_to_host(const spamm_tree *t, double *nsq, uint8_t *occ);
 /* Raw device pointers (borrowed) for collective plumbing (a band tree's
  * storage outside its rows is undefined; see spamm_multiply_rows). */
+/* The squared-norm pyramid recomputed from the leaf data by K1 into scratch
+ * storage and copied to host (same layout as spamm_tree_pyramid_to_host):
+ * the fresh side of audit_norm_cache (quadtree.py:325-340). */
+SPAMM_API int spamm_tree_recompute_norms(const spamm_tree *t, double *nsq_host);
 SPAMM_API int spamm_tree_device_ptrs(const spamm_tree *t, void **padded, double **nsq, uint8_t **occ);
 /* ||A - B||_F computed on the device (multiply_error, multiply.py:276). */
 SPAMM_API int spamm_tree_diff_norm(const spamm_tree *a, const spamm_tree *b, double *out);
@@ -177,6 +187,26 @@ SPAMM_API int spamm_product_boxes(const spamm_product *p, int64_t *out, int64_t 
 /* triples: 3 int32 per retained leaf product (i, j, k), sorted by (i, j, k). */
 SPAMM_API int spamm_product_triples(const spamm_product *p, int32_t *out, int64_t capacity);
 SPAMM_API void spamm_product_free(spamm_product *p);
+
+/* -- box log ordering ------------------------------------------------------- */
+/* order[r] = index of the box written r-th in a box log: boxes (5 int64 each,
+ * i_lo, j_lo, k_lo, edge, tier) stably sorted on the device by the Morton key
+ * of (i_lo, j_lo, k_lo), i-major bit interleave (multiply.py:306-315 with
+ * ordering.py:24-34).  Coordinates must lie in [0, 2^21). */
+SPAMM_API int spamm_boxes_morton_order(const int64_t *boxes, int64_t count, int32_t device,
+                                       int64_t *order);
+
+/* -- generators --------------------------------------------------------------- */
+/* Tree of the n x n Toeplitz matrix element(i, j) = table[|i - j|], written
+ * directly into device storage (gen_exponential: table[d] = exp(-alpha d);
+ * gen_algebraic: table[d] = d^-p, table[0] = 0; generators.py:24-43). */
+SPAMM_API int spamm_tree_toeplitz(const double *table, int64_t n, int32_t leaf_size, int32_t dtype,
+                                  int32_t device, spamm_tree **out);
+/* Tree of the symmetric tridiagonal matrix with diag[i] on (i, i) and off[i]
+ * on (i, i+1) and (i+1, i) (gen_model_hamiltonian, generators.py:76-88). */
+SPAMM_API int spamm_tree_tridiagonal(const double *diag, const double *off, int64_t n,
+                                     int32_t leaf_size, int32_t dtype, int32_t device,
+                                     spamm_tree **out);
 
 #ifdef __cplusplus
 }

@@ -38,7 +38,8 @@ EXPORTED = (
     "spamm_tree_free", "spamm_multiply", "spamm_multiply_rows", "spamm_product_boxes",
     "spamm_product_triples", "spamm_product_free",
     "spamm_tree_add", "spamm_tree_scale", "spamm_tree_filter_drop", "spamm_tree_diagonal",
-    "spamm_tree_blocks_to_host",
+    "spamm_tree_blocks_to_host", "spamm_boxes_morton_order", "spamm_tree_toeplitz",
+    "spamm_tree_tridiagonal", "spamm_tree_recompute_norms",
 )
 
 
@@ -107,6 +108,10 @@ def load(path=LIB_PATH):
         L.spamm_product_triples.argtypes = [vp, vp, i64]
         L.spamm_product_free.argtypes = [vp]
         L.spamm_product_free.restype = None
+        L.spamm_boxes_morton_order.argtypes = [vp, i64, i32, vp]
+        L.spamm_tree_recompute_norms.argtypes = [vp, vp]
+        L.spamm_tree_toeplitz.argtypes = [vp, i64, i32, i32, i32, pp]
+        L.spamm_tree_tridiagonal.argtypes = [vp, vp, i64, i32, i32, i32, pp]
         _lib = L
         return L
 

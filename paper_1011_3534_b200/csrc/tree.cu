@@ -1074,6 +1074,42 @@ int spamm_tree_pyramid_to_host(const spamm_tree *t, double *nsq, uint8_t *occ) {
   return SPAMM_OK;
 }
 
+int spamm_tree_recompute_norms(const spamm_tree *t, double *nsq_host) {
+  if (!t || !nsq_host) { set_error("null argument"); return SPAMM_ERR_VALUE; }
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(t->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(materialize(ctx, t));
+  // a view of the same leaf data with a scratch pyramid
+  spamm_tree view = *t;
+  view.nsq = nullptr;
+  view.occ = nullptr;
+  view.nrm = nullptr;
+  const int64_t P = pyramid_size(t->depth);
+  int rc = SPAMM_OK;
+  cudaError_t e = cudaMallocAsync((void **)&view.nsq, sizeof(double) * P, ctx->stream);
+  if (e == cudaSuccess) e = cudaMallocAsync((void **)&view.occ, P, ctx->stream);
+  if (e == cudaSuccess) e = cudaMallocAsync((void **)&view.nrm, sizeof(double) * P, ctx->stream);
+  if (e == cudaSuccess) {
+    rc = build_pyramid_async(ctx, &view, ctx->stream, nullptr, nullptr, nullptr, 0, nullptr, 0,
+                             nullptr, nullptr);
+    if (rc == SPAMM_OK)
+      e = cudaMemcpyAsync(nsq_host, view.nsq, sizeof(double) * P, cudaMemcpyDeviceToHost,
+                          ctx->stream);
+  }
+  if (view.nsq) cudaFreeAsync(view.nsq, ctx->stream);
+  if (view.occ) cudaFreeAsync(view.occ, ctx->stream);
+  if (view.nrm) cudaFreeAsync(view.nrm, ctx->stream);
+  const cudaError_t es = cudaStreamSynchronize(ctx->stream);
+  if (rc) return rc;
+  if (e == cudaSuccess) e = es;
+  if (e != cudaSuccess) {
+    set_error("norm recompute: %s", cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? SPAMM_ERR_NOMEM : SPAMM_ERR_CUDA;
+  }
+  return SPAMM_OK;
+}
+
 int spamm_tree_device_ptrs(const spamm_tree *t, void **padded, double **nsq, uint8_t **occ) {
   if (!t) { set_error("null tree"); return SPAMM_ERR_VALUE; }
   if (padded) *padded = t->padded;

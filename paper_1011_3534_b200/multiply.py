@@ -192,6 +192,75 @@ def multiply_error(a, b, config):
     return diff_norm(approx, exact), stats.omitted_budget
 
 
+def norm_submultiplicativity_check(a, b):
+    """The norm bounds pruning relies on, checked on actual data
+    (multiply.py:281-303): ||AB||_F <= ||A||_F ||B||_F and, at tier 1,
+    ||AB||_F <= sum over quadrant pairs of child-norm products, each with
+    8 ulp of slack.  The exact product runs on the GPU."""
+    _require_conformable(a, b)
+    c = exact_multiply(a, b)
+    slack = 1.0 + 8 * float(np.finfo(a.dtype).eps)
+    nc = node_norm(c)
+    if nc > node_norm(a) * node_norm(b) * slack:
+        return False
+    if a.depth >= 1:
+        an = np.sqrt(a._norm_sq[1])
+        bn = np.sqrt(b._norm_sq[1])
+        bound = 0.0
+        for i in range(2):
+            for j in range(2):
+                bound += an[i, 0] * bn[0, j] + an[i, 1] * bn[1, j]
+        if nc > bound * slack:
+            return False
+    return True
+
+
+def _box_array(boxes):
+    rows = [(bx.i_lo, bx.j_lo, bx.k_lo, bx.edge, bx.tier) for bx in boxes]
+    return np.array(rows, dtype=np.int64).reshape(-1, 5)
+
+
+def morton_order(boxes, device=None):
+    """Indices of ``boxes`` in box-log order: a stable sort by the i-major
+    Morton key of (i_lo, j_lo, k_lo) (multiply.py:312, ordering.py:24-34),
+    computed on the GPU (csrc/boxes.cu)."""
+    from .quadtree import get_device
+
+    arr = boxes if isinstance(boxes, np.ndarray) else _box_array(boxes)
+    arr = np.ascontiguousarray(arr, dtype=np.int64).reshape(-1, 5)
+    order = np.empty(arr.shape[0], np.int64)
+    if arr.shape[0]:
+        dev = get_device() if device is None else int(device)
+        _lib.check(_lib.load().spamm_boxes_morton_order(arr.ctypes.data, arr.shape[0], dev,
+                                                        order.ctypes.data))
+    return order
+
+
+def write_box_log(boxes, path, padded_dim):
+    """Write a box log (multiply.py:306-315): one ``tier i_lo j_lo k_lo edge``
+    line per pruned box, boxes in Morton order of their lower corners so that
+    nearby cuboids are nearby in the file.  The order is computed on the GPU."""
+    arr = _box_array(boxes)
+    order = morton_order(arr)
+    with open(path, "w") as fh:
+        if arr.shape[0]:
+            np.savetxt(fh, arr[order][:, [4, 0, 1, 2, 3]], fmt="%d", delimiter=" ")
+
+
+def read_box_log(path):
+    """Parse a box log written by write_box_log (multiply.py:318-328)."""
+    out = []
+    with open(path) as fh:
+        for line in fh:
+            tok = line.split()
+            if not tok:
+                continue
+            tier, i_lo, j_lo, k_lo, edge = (int(t) for t in tok)
+            out.append(PrunedBox(i_lo, j_lo, k_lo, edge, tier))
+    return out
+
+
 __all__ = ["SpammConfig", "PrunedBox", "ProductStats", "MultiplyDetail", "spamm",
            "spamm_detailed", "exact_multiply", "multiply_error", "diff_norm", "node_norm",
+           "norm_submultiplicativity_check", "write_box_log", "read_box_log", "morton_order",
            "QuadTreeMatrix"]

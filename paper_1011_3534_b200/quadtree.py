@@ -376,3 +376,18 @@ def filter_drop(m, tau):
 def node_norm(m):
     """Frobenius norm from the root's cached norm (quadtree.py:269-271)."""
     return m.norm()
+
+
+def audit_norm_cache(m):
+    """Maximum relative discrepancy between the cached norm pyramid and one
+    recomputed from the leaf data (quadtree.py:325-340); 0.0 for a healthy
+    tree.  The recomputation is K1 on the device into scratch storage."""
+    nsq = m._pyramid()[2]
+    fresh = np.empty_like(nsq)
+    _lib.check(_lib.load().spamm_tree_recompute_norms(m._handle, fresh.ctypes.data))
+    worst = 0.0
+    for off, side in _level_slices(m.depth):
+        stored = nsq[off:off + side * side]
+        denom = np.where(stored > 0, stored, 1.0)
+        worst = max(worst, float((np.abs(fresh[off:off + side * side] - stored) / denom).max()))
+    return worst
