@@ -11,8 +11,10 @@ device-resident trees (cull + leaf products + C's tree), i.e. the sweep.
              TFLOP/s; each spamm timed with CUDA events on the library's own
              stream; L2 flushed (256 MiB write) before every multiply.
 * e2e        the same metric through the public API with host buffers:
-             from_dense(pinned A) -> spamm per tau -> to_dense(pinned C),
-             host->device and device->host copies inside the timed region.
+             from_dense(pinned A) -> spamm per tau -> each product's nonzero
+             blocks + pyramid to pinned host memory (the block copy on a
+             copy-out stream, overlapping the next call), host->device and
+             device->host copies inside the timed region.
 * roofline   the leaf-product kernel (K3) against the measured FP64 DMMA peak
              (profiles/fp64_peaks.json, measured on this pool's B200s).
 * cpu_baseline / --impl reference: the C restatement of the reference
@@ -389,7 +391,11 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
     # shards each rank holds (and reads back) only its own block rows
     nbk = -(-n // leaf)
     G = (1 << (max(nbk - 1, 0)).bit_length()) ** 2
-    pin_blk = torch.empty((G, leaf, leaf), dtype=tdt, pin_memory=True).numpy()
+    # one pinned buffer per tau: a product's copy overlaps the next multiply
+    # (and the next step's host->device copy of A: PCIe is full duplex); a
+    # buffer is reused only after its previous transfer has been waited for
+    pin_blk = [torch.empty((G, leaf, leaf), dtype=tdt, pin_memory=True).numpy() for _ in taus]
+    pending = [None] * len(taus)
     t0 = None
     e_f = 0.0
     d2h = 0
@@ -403,18 +409,23 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
         at = sp.from_dense(pin_a, leaf_size=leaf)
         bt = at if same else sp.from_dense(pin_b, leaf_size=leaf)
         f = 0.0
-        for tau in taus:
+        for q, tau in enumerate(taus):
             if shard is None:
                 c, st = sp.spamm(at, bt, sp.SpammConfig(tau=tau))
             else:
                 c, st, _ = sp.spamm_detailed(at, bt, sp.SpammConfig(tau=tau), rows=shard)
-            ids, blocks = c.nonzero_blocks(out=pin_blk)
-            d2h += blocks.nbytes + ids.nbytes + c._pyramid()[2].nbytes + c._pyramid()[3].nbytes
+            if pending[q] is not None:
+                pending[q].wait()
+            pending[q] = c.nonzero_blocks(out=pin_blk[q], wait=False)
+            d2h += (pending[q].blocks.nbytes + pending[q].ids.nbytes + c._pyramid()[2].nbytes
+                    + c._pyramid()[3].nbytes)
             f += leaf_flops(leaf, st.leaf_matmuls)
             del c
         del at, bt
         if it >= args.warmup:
             e_f += f
+    for p in pending:
+        p.wait()
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     d2h = d2h // max(args.steps, 1)
@@ -429,7 +440,8 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
             "d2h_bytes_per_step": d2h,
             "ms_per_step": el / args.steps * 1e3,
             "result": "each product read back as its nonzero leaf blocks + norm pyramid "
-                      "(QuadTreeMatrix.nonzero_blocks)",
+                      "(QuadTreeMatrix.nonzero_blocks, copy-out stream overlapping the next "
+                      "call; all copies waited for inside the timed region)",
             "timing": "host wall clock around synchronous public-API calls (max over ranks)"}
 
 

@@ -28,6 +28,7 @@
  *   spamm_tree_filter_drop    <- quadtree.filter_drop         quadtree.py:302-316
  *   spamm_tree_diagonal       <- the diagonal of quadtree.trace quadtree.py:274-277
  *   spamm_tree_blocks_to_host <- _blocks[_leaf_nonzero]       quadtree.py:120-151
+ *   (+ _async / spamm_transfer_wait: the same copy overlapping later calls)
  *   spamm_boxes_morton_order  <- the sort in write_box_log     multiply.py:306-315
  *                                (key: ordering._interleave3   ordering.py:24-34)
  *   spamm_tree_toeplitz       <- generators.gen_exponential / gen_algebraic
@@ -159,9 +160,24 @@ SPAMM_API int spamm_tree_filter_drop(const spamm_tree *m, double tau, spamm_tree
 /* The listed leaves (ids: leaf indices i * block_grid + j) copied to host
  * memory as a contiguous [count][leaf][leaf] array in one transfer -- the
  * nonzero blocks of a tree (the reference's _blocks[_leaf_nonzero],
- * quadtree.py:120-151) without moving its empty blocks. */
+ * quadtree.py:120-151) without moving its empty blocks.  ids == NULL: every
+ * nonzero leaf in ascending order (count must be their number), listed on the
+ * device. */
 SPAMM_API int spamm_tree_blocks_to_host(const spamm_tree *m, const int64_t *ids, int64_t count,
                                         void *host_out);
+/* Asynchronous spamm_tree_blocks_to_host: the gather is ordered after every
+ * earlier call on the tree's device, the copy runs on a separate copy-out
+ * stream, and the call returns at once with a transfer handle.  host_out
+ * should be pinned (page-locked) for the copy to overlap later calls; it must
+ * stay valid until spamm_transfer_wait(*out) returns, which blocks until the
+ * bytes are in host_out and releases the handle (exactly once per handle).
+ * ids == NULL: every nonzero leaf in ascending order (count must be their
+ * number), the list formed on the device. */
+typedef struct spamm_transfer spamm_transfer;
+SPAMM_API int spamm_tree_blocks_to_host_async(const spamm_tree *m, const int64_t *ids,
+                                              int64_t count, void *host_out,
+                                              spamm_transfer **out);
+SPAMM_API int spamm_transfer_wait(spamm_transfer *t);
 /* The logical diagonal (n elements of the tree's dtype) to host memory, for
  * trace = numpy add.reduce of it (quadtree.py:274-277). */
 SPAMM_API int spamm_tree_diagonal(const spamm_tree *m, void *host_out);

@@ -40,6 +40,7 @@ EXPORTED = (
     "spamm_tree_add", "spamm_tree_scale", "spamm_tree_filter_drop", "spamm_tree_diagonal",
     "spamm_tree_blocks_to_host", "spamm_boxes_morton_order", "spamm_tree_toeplitz",
     "spamm_tree_tridiagonal", "spamm_tree_recompute_norms",
+    "spamm_tree_blocks_to_host_async", "spamm_transfer_wait",
 )
 
 
@@ -99,6 +100,8 @@ def load(path=LIB_PATH):
         L.spamm_tree_filter_drop.argtypes = [vp, ctypes.c_double, pp, ctypes.POINTER(i32)]
         L.spamm_tree_diagonal.argtypes = [vp, vp]
         L.spamm_tree_blocks_to_host.argtypes = [vp, vp, i64, vp]
+        L.spamm_tree_blocks_to_host_async.argtypes = [vp, vp, i64, vp, pp]
+        L.spamm_transfer_wait.argtypes = [vp]
         L.spamm_tree_free.argtypes = [vp]
         L.spamm_tree_free.restype = None
         L.spamm_multiply.argtypes = [vp, vp, ctypes.c_double, u32, pp, ctypes.POINTER(Stats), pp]

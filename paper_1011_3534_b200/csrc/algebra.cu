@@ -101,6 +101,38 @@ __global__ void gather_blocks_kernel(const unsigned char *__restrict__ padded, i
   }
 }
 
+// ids of the nonzero leaves (occupancy leaf level), ascending -- the device
+// side of flatnonzero(_leaf_nonzero); one CTA, a contiguous chunk per thread
+__global__ void __launch_bounds__(1024) occ_ids_kernel(const uint8_t *__restrict__ occ, int64_t G,
+                                                       int64_t *__restrict__ ids) {
+  __shared__ int64_t warp_tot[32];
+  const int64_t per = (G + blockDim.x - 1) / blockDim.x;
+  const int64_t lo0 = (int64_t)threadIdx.x * per;
+  const int64_t lo = lo0 < G ? lo0 : G, hi = lo + per < G ? lo + per : G;
+  int64_t cnt = 0;
+  for (int64_t g = lo; g < hi; ++g) cnt += occ[g] != 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t inc = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    warp_tot[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  int64_t pos = inc - cnt + (warp ? warp_tot[warp - 1] : 0);
+  for (int64_t g = lo; g < hi; ++g)
+    if (occ[g]) ids[pos++] = g;
+}
+
 static int grid_rows(DeviceContext *ctx, int64_t N) {
   return (int)std::min<int64_t>(N, (int64_t)ctx->num_sms * 16);
 }
@@ -233,7 +265,7 @@ SPAMM_API int spamm_tree_filter_drop(const spamm_tree *m, double tau, spamm_tree
 
 SPAMM_API int spamm_tree_blocks_to_host(const spamm_tree *m, const int64_t *ids, int64_t count,
                                         void *host_out) {
-  if (!m || (count && (!ids || !host_out)) || count < 0) {
+  if (!m || (count && !host_out) || count < 0) {
     set_error("null argument");
     return SPAMM_ERR_VALUE;
   }
@@ -245,7 +277,13 @@ SPAMM_API int spamm_tree_blocks_to_host(const spamm_tree *m, const int64_t *ids,
   SPAMM_TRY(ensure_scratch(ctx->reduce_tmp, (size_t)(bytes + count * 8 + 256), ctx->stream));
   int64_t *dids = (int64_t *)ctx->reduce_tmp.ptr;
   unsigned char *dbuf = (unsigned char *)ctx->reduce_tmp.ptr + ((count * 8 + 255) / 256) * 256;
-  SPAMM_CUDA_TRY(cudaMemcpyAsync(dids, ids, count * 8, cudaMemcpyHostToDevice, ctx->stream));
+  if (ids) {
+    SPAMM_TRY(materialize(ctx, m));  // any block may be listed
+    SPAMM_CUDA_TRY(cudaMemcpyAsync(dids, ids, count * 8, cudaMemcpyHostToDevice, ctx->stream));
+  } else {  // every nonzero leaf, listed on the device
+    occ_ids_kernel<<<1, 1024, 0, ctx->stream>>>(m->occ + level_offset(m->depth), m->nb * m->nb,
+                                                dids);
+  }
   for (int64_t q = 0; q < count; q += 65535) {
     const int64_t k = std::min<int64_t>(65535, count - q);
     gather_blocks_kernel<<<(unsigned)k, 256, 0, ctx->stream>>>(
@@ -255,6 +293,125 @@ SPAMM_API int spamm_tree_blocks_to_host(const spamm_tree *m, const int64_t *ids,
   SPAMM_CUDA_TRY(cudaGetLastError());
   SPAMM_CUDA_TRY(cudaMemcpyAsync(host_out, dbuf, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SPAMM_OK;
+}
+
+// A pending device->host block transfer: the gather runs on the library's
+// stream (ordered after the product that wrote the blocks), the copy on the
+// context's copy-out stream, so the transfer overlaps whatever the caller
+// launches next (the next multiply, or the next matrix's host->device copy:
+// PCIe is full duplex).
+}  // extern "C"
+struct spamm_transfer {
+  int device = 0;
+  cudaEvent_t done = nullptr;
+  spamm::Scratch staging;  // taken from / returned to the context's idle list
+};
+extern "C" {
+
+SPAMM_API int spamm_tree_blocks_to_host_async(const spamm_tree *m, const int64_t *ids,
+                                              int64_t count, void *host_out,
+                                              spamm_transfer **out) {
+  if (!m || !out || (count && !host_out) || count < 0) {
+    set_error("null argument");
+    return SPAMM_ERR_VALUE;
+  }
+  *out = nullptr;
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(m->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  auto *t = new spamm_transfer;
+  t->device = m->device;
+  const int64_t esz = m->elem_size(), bytes = count * m->leaf * m->leaf * esz;
+  const int64_t id_bytes = ((count * 8 + 255) / 256) * 256;
+  int rc = SPAMM_OK;
+  do {
+    cudaError_t e = cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming);
+    if (e == cudaSuccess && count) {
+      // a persistent staging buffer (allocation-free in steady state)
+      const size_t need = (size_t)(bytes + id_bytes);
+      size_t best = ctx->xfer_free.size();
+      for (size_t q = 0; q < ctx->xfer_free.size(); ++q)
+        if (ctx->xfer_free[q].bytes >= need &&
+            (best == ctx->xfer_free.size() || ctx->xfer_free[q].bytes < ctx->xfer_free[best].bytes))
+          best = q;
+      if (best < ctx->xfer_free.size()) {
+        t->staging = ctx->xfer_free[best];
+        ctx->xfer_free.erase(ctx->xfer_free.begin() + best);
+      } else {
+        e = cudaStreamSynchronize(ctx->stream);
+        if (e == cudaSuccess) e = cudaMalloc(&t->staging.ptr, need);
+        if (e == cudaSuccess) t->staging.bytes = need;
+      }
+    }
+    if (e != cudaSuccess) {
+      set_error("transfer setup: %s", cudaGetErrorString(e));
+      rc = e == cudaErrorMemoryAllocation ? SPAMM_ERR_NOMEM : SPAMM_ERR_CUDA;
+      break;
+    }
+    if (count) {
+      int64_t *dids = (int64_t *)t->staging.ptr;
+      unsigned char *dbuf = (unsigned char *)t->staging.ptr + id_bytes;
+      if (ids) {
+        SPAMM_TRY(materialize(ctx, m));  // any block may be listed
+        e = cudaMemcpyAsync(dids, ids, count * 8, cudaMemcpyHostToDevice, ctx->stream);
+      } else {
+        // every nonzero leaf: ids from the occupancy pyramid on the device (no
+        // host->device copy); occupied blocks are always defined
+        occ_ids_kernel<<<1, 1024, 0, ctx->stream>>>(m->occ + level_offset(m->depth),
+                                                    m->nb * m->nb, dids);
+        e = cudaGetLastError();
+      }
+      for (int64_t q = 0; e == cudaSuccess && q < count; q += 65535) {
+        const int64_t k = std::min<int64_t>(65535, count - q);
+        gather_blocks_kernel<<<(unsigned)k, 256, 0, ctx->stream>>>(
+            (const unsigned char *)m->padded, m->N, m->leaf, m->nb, (int)esz, dids + q,
+            dbuf + q * m->leaf * m->leaf * esz);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaEventRecord(ctx->join, ctx->stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->copy_out, ctx->join, 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(host_out, dbuf, bytes, cudaMemcpyDeviceToHost, ctx->copy_out);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(t->done, count ? ctx->copy_out : ctx->stream);
+    if (e != cudaSuccess) {
+      set_error("transfer: %s", cudaGetErrorString(e));
+      rc = SPAMM_ERR_CUDA;
+    }
+  } while (0);
+  if (rc) {
+    if (t->staging.ptr) {
+      cudaStreamSynchronize(ctx->stream);
+      ctx->xfer_free.push_back(t->staging);
+    }
+    if (t->done) cudaEventDestroy(t->done);
+    delete t;
+    return rc;
+  }
+  *out = t;
+  return SPAMM_OK;
+}
+
+SPAMM_API int spamm_transfer_wait(spamm_transfer *t) {
+  if (!t) {
+    set_error("null transfer");
+    return SPAMM_ERR_VALUE;
+  }
+  const cudaError_t e = cudaEventSynchronize(t->done);
+  if (t->staging.ptr) {  // the copy is complete: the buffer is idle again
+    DeviceContext *ctx;
+    if (get_context(t->device, &ctx) == SPAMM_OK) {
+      std::lock_guard<std::mutex> lk(ctx->mu);
+      ctx->xfer_free.push_back(t->staging);
+    }
+  }
+  cudaEventDestroy(t->done);
+  delete t;
+  if (e != cudaSuccess) {
+    set_error("transfer: %s", cudaGetErrorString(e));
+    return SPAMM_ERR_CUDA;
+  }
   return SPAMM_OK;
 }
 

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "spamm_b200.h"
 
@@ -84,6 +85,7 @@ struct DeviceContext {
   int num_sms = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;       // overlaps memory-bound fills with compute
+  cudaStream_t copy_out = nullptr;   // device->host result transfers (overlap the next call)
   cudaEvent_t fork = nullptr, join = nullptr;
   cudaEvent_t ev[8] = {};
   std::mutex mu;
@@ -108,14 +110,19 @@ struct DeviceContext {
   Scratch grp_done;       // per-group finished-tile counters (zero at rest)
   Scratch lpt_order;      // groups by decreasing size (K3's work order)
   Scratch pw_part;        // budget: per-tier partial sums of the split recursion
-  Scratch grp_mark;       // non-empty C blocks (bitmask, zero at rest)
   size_t cull_capacity = 0;   // survivor capacity per ping-pong buffer (items)
   size_t pruned_capacity = 0; // pruned capacity (items, all tiers)
   void *host_pinned = nullptr;  // small pinned staging for counters
+  std::vector<Scratch> xfer_free;  // idle device staging buffers of async block transfers
 };
 
 int get_context(int device, DeviceContext **ctx);
 int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed = false);
+// Zero `bytes` at `p` with a kernel (16-byte stores; any alignment).  Used on
+// the multiply path instead of cudaMemsetAsync, which is carried out by a
+// copy engine and so queues behind device->host copies in flight (an async
+// product read-back would otherwise stall the next multiply).
+int zero_async(void *p, size_t bytes, cudaStream_t st, int ctas);
 
 }  // namespace spamm
 
@@ -132,16 +139,17 @@ struct spamm_tree {
   uint8_t *occ = nullptr;   // concatenated occupancy pyramid
   double *nrm = nullptr;    // rn(sqrt(nsq)): the factors of the pruning test
   double root_norm_sq = 0.0;
-  // Band trees (a row-sharded product): only leaf rows [valid_lo, valid_hi)
-  // of `padded` were written; the rest is zero by definition (its norms are
-  // zero) and is zero-filled on first whole-storage access (materialize()).
-  // valid_hi < 0: all storage defined.
-  int64_t valid_lo = 0, valid_hi = -1;
+  // Lazy empty blocks (every product): only the leaf blocks whose occupancy
+  // is set were written; the others are zero by definition (their norms are
+  // zero, and no multiply, norm or block read touches them) and are zero-
+  // filled on the first whole-storage access (materialize()).  A row-sharded
+  // product (band tree) is the same thing: blocks outside its rows are empty.
+  bool lazy_empty = false;
   int64_t elem_size() const { return dtype == SPAMM_DTYPE_F64 ? 8 : 4; }
 };
 
 namespace spamm {
 struct DeviceContext;
-// zero-fill a band tree's undefined rows (stream-ordered on ctx->stream)
+// zero-fill a lazy tree's empty blocks (stream-ordered on ctx->stream)
 int materialize(DeviceContext *ctx, const spamm_tree *t);
 }  // namespace spamm

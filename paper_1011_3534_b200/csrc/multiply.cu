@@ -35,55 +35,6 @@ int finish_tree(DeviceContext *ctx, spamm_tree *t);
 void k1_timeline_enable(cudaStream_t st);
 void k1_timeline_dump(unsigned long long k3_end, unsigned long long k3_start);
 
-// ------------------------------------------------- C's empty blocks
-// K3 writes every C block that receives products; the others must be zero.
-// Instead of zero-filling all of C before K3 (at n = 65536 that is 34 GB of
-// writes in front of the product), these two kernels zero only the empty
-// blocks (and their leaf-level norm entries) on a side stream, concurrently
-// with K3.
-__global__ void mark_groups_kernel(const uint32_t *__restrict__ group_ids,
-                                   const unsigned *__restrict__ num_groups,
-                                   uint32_t *__restrict__ mark, int64_t G, unsigned cap) {
-  unsigned n = *num_groups;
-  if (n > cap) n = cap;
-  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
-    const uint32_t g = group_ids[q];
-    if ((int64_t)g < G) atomicOr(&mark[g >> 5], 1u << (g & 31));
-  }
-}
-
-__global__ void zero_empty_kernel(unsigned char *__restrict__ padded, int64_t N, int32_t leaf,
-                                  int64_t nb, int esz, uint32_t *__restrict__ mark,
-                                  double *__restrict__ nsq_leaf, uint8_t *__restrict__ occ_leaf,
-                                  double *__restrict__ nrm_leaf, int64_t row_lo, int64_t row_hi) {
-  const int64_t G = nb * nb;
-  const int64_t w = blockIdx.x;
-  const uint32_t bits = mark[w];
-  const int64_t row_bytes = (int64_t)leaf * esz;
-  for (int b = 0; b < 32; ++b) {
-    const int64_t g = w * 32 + b;
-    if (g >= G || ((bits >> b) & 1u)) continue;  // uniform across the CTA
-    const int64_t bi = g / nb, bj = g - bi * nb;
-    if (bi < row_lo || bi >= row_hi) continue;  // outside a band tree's rows: never read
-    unsigned char *base = padded + (bi * leaf) * N * esz + bj * row_bytes;
-    if (row_bytes % 16 == 0) {
-      const int per_row = (int)(row_bytes / 16);
-      for (int r = 0; r < leaf; ++r) {
-        uint4 *row = reinterpret_cast<uint4 *>(base + (int64_t)r * N * esz);
-        for (int c = threadIdx.x; c < per_row; c += blockDim.x) row[c] = make_uint4(0u, 0u, 0u, 0u);
-      }
-    } else {
-      const int64_t total = row_bytes * leaf;
-      for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
-        const int64_t r = e / row_bytes, c = e - r * row_bytes;
-        base[r * N * esz + c] = 0;
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) mark[w] = 0u;  // zero at rest
-}
-
 static int check_conformable(const spamm_tree *a, const spamm_tree *b) {
   // quadtree.py:209-215
   if (!a || !b) {
@@ -250,55 +201,23 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     ctx->counter_parity ^= 1;
     if (dense) ctx->dense_parity ^= 1;
     ++launches;
-    // C's zero fill on the side stream.  Small products: a memset of all of C
-    // under the traversal (hidden: 134 MB at c2).  Large products (c5: 34 GB,
-    // 5 ms of writes): only the empty blocks, once the group list exists,
-    // by single-warp CTAs that fit beside K3's CTAs -- concurrently with K3.
-    // A row-sharded product is a band tree: only its block rows are zeroed and
-    // written; the rest is zero by definition and filled only if the whole
-    // storage is ever read (materialize()).
-    const bool band = row_lo > 0 || row_hi < nb;
-    const int64_t band_r0 = row_lo * c->leaf, band_r1 = std::min<int64_t>(row_hi * c->leaf, c->N);
-    const size_t band_bytes = (size_t)((band_r1 - band_r0) * c->N * c->elem_size());
-    const bool big_c = band_bytes > (size_t(2) << 30);
-    if (band) {
-      c->valid_lo = row_lo;
-      c->valid_hi = row_hi;
-    }
-    if (!big_c) {
-      SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));  // (fork: before the traversal)
-      SPAMM_CUDA_BREAK(cudaMemsetAsync((char *)c->padded + band_r0 * c->N * c->elem_size(), 0,
-                                       band_bytes, ctx->side));
-      // C's leaf level: only blocks that receive products are recomputed below
-      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nsq + level_offset(depth), 0, sizeof(double) * G, ctx->side));
-      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->occ + level_offset(depth), 0, G, ctx->side));
-      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nrm + level_offset(depth), 0, sizeof(double) * G, ctx->side));
-      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));
-      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
-      SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));
-    } else {
-      // leaf-level norms of C on the main stream (small; K1's pyramid reads
-      // them); the block data on the side stream, joined after K1 (no event
-      // wait may sit between K3 and its programmatic dependent K1)
-      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nsq + level_offset(depth), 0, sizeof(double) * G, st));
-      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->occ + level_offset(depth), 0, G, st));
-      SPAMM_CUDA_BREAK(cudaMemsetAsync(c->nrm + level_offset(depth), 0, sizeof(double) * G, st));
-      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->fork, st));
-      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
-      SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
-      const int64_t words = (G + 31) / 32;
-      if ((rc = ensure_scratch(ctx->grp_mark, sizeof(uint32_t) * words, ctx->side, true))) break;
-      uint32_t *mark = (uint32_t *)ctx->grp_mark.ptr;
-      mark_groups_kernel<<<(unsigned)std::min<int64_t>((gcap + 255) / 256, 1024), 256, 0, ctx->side>>>(
-          ta.group_ids, &dtc->num_groups, mark, G, (unsigned)gcap);
-      zero_empty_kernel<<<(unsigned)words, 32, 0, ctx->side>>>(
-          (unsigned char *)c->padded, c->N, c->leaf, nb, (int)c->elem_size(), mark,
-          c->nsq + level_offset(depth), c->occ + level_offset(depth), c->nrm + level_offset(depth),
-          row_lo, row_hi);
-      SPAMM_CUDA_BREAK(cudaGetLastError());
-      launches += 2;
-      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));
-    }
+    // C's block storage is not zero-filled: a product is a lazy tree whose
+    // empty blocks (no retained triple; the same as occupancy clear) are
+    // zero by definition and never read by a multiply, a norm build or a
+    // nonzero-block read -- they are filled only if the whole storage is ever
+    // read (materialize()).  That removes N^2 bytes of writes per multiply
+    // (134 MB at c2, 34 GB at c5).  A row-sharded product (band tree) is the
+    // same case: blocks outside its rows are empty.  C's leaf-level norms are
+    // zeroed on the side stream under the traversal (only blocks that receive
+    // products are recomputed below).
+    c->lazy_empty = true;
+    SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));  // (fork: before the traversal)
+    if ((rc = zero_async(c->nsq + level_offset(depth), sizeof(double) * G, ctx->side, 64))) break;
+    if ((rc = zero_async(c->occ + level_offset(depth), G, ctx->side, 64))) break;
+    if ((rc = zero_async(c->nrm + level_offset(depth), sizeof(double) * G, ctx->side, 64))) break;
+    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));
+    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
+    SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));
 
     // ------------------------------------------------ K3 leaf products -> C
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[2], st));
@@ -351,7 +270,6 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
         break;
     }
     ctx->last_overlapped = overlapped;
-    if (big_c) SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));  // C's empty blocks
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
     SPAMM_CUDA_BREAK(cudaMemcpyAsync(hc, dtc, sizeof(TraverseCounters), cudaMemcpyDeviceToHost, st));
     SPAMM_CUDA_BREAK(cudaMemcpyAsync(&c->root_norm_sq, c->nsq, sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -48,6 +48,7 @@ int get_context(int device, DeviceContext **out) {
     SPAMM_CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
     SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
     SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
     SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming));
     for (auto &e : ctx->ev) SPAMM_CUDA_TRY(cudaEventCreate(&e));
@@ -65,6 +66,27 @@ int get_context(int device, DeviceContext **out) {
   return SPAMM_OK;
 }
 
+__global__ void zero_fill_kernel(unsigned char *__restrict__ p, size_t bytes) {
+  const size_t head = (16 - ((uintptr_t)p & 15)) & 15;
+  const size_t h = head < bytes ? head : bytes;
+  const size_t body = (bytes - h) / 16, tail0 = h + body * 16;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x,
+               stride = (size_t)gridDim.x * blockDim.x;
+  uint4 *q = reinterpret_cast<uint4 *>(p + h);
+  for (size_t i = tid; i < body; i += stride) q[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (tid < h) p[tid] = 0;
+  if (tid < bytes - tail0) p[tail0 + tid] = 0;
+}
+
+int zero_async(void *p, size_t bytes, cudaStream_t st, int ctas) {
+  if (!bytes) return SPAMM_OK;
+  const size_t want = (bytes / 16 + 255) / 256 + 1;
+  const unsigned grid = (unsigned)std::min<size_t>(want, (size_t)std::max(ctas, 1));
+  zero_fill_kernel<<<grid, 256, 0, st>>>((unsigned char *)p, bytes);
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  return SPAMM_OK;
+}
+
 int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed) {
   if (s.bytes >= bytes) return SPAMM_OK;
   if (s.ptr) SPAMM_CUDA_TRY(cudaFreeAsync(s.ptr, stream));
@@ -73,7 +95,7 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed) {
   size_t want = bytes + bytes / 4 + 256;
   SPAMM_CUDA_TRY(cudaMallocAsync(&s.ptr, want, stream));
   s.bytes = want;
-  if (zeroed) SPAMM_CUDA_TRY(cudaMemsetAsync(s.ptr, 0, want, stream));
+  if (zeroed) SPAMM_TRY(zero_async(s.ptr, want, stream, 1024));
   return SPAMM_OK;
 }
 
@@ -875,16 +897,41 @@ void free_tree_async(spamm_tree *t, cudaStream_t st) {
   delete t;
 }
 
+// zero every leaf block whose occupancy is clear (one warp per block)
+__global__ void zero_unoccupied_kernel(unsigned char *__restrict__ padded, int64_t N, int32_t leaf,
+                                       int64_t nb, int esz, const uint8_t *__restrict__ occ_leaf) {
+  const int lane = threadIdx.x & 31;
+  const int64_t G = nb * nb, row_bytes = (int64_t)leaf * esz;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < G;
+       g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if (occ_leaf[g]) continue;  // warp-uniform
+    const int64_t bi = g / nb, bj = g - bi * nb;
+    unsigned char *base = padded + (bi * leaf) * N * esz + bj * row_bytes;
+    if (row_bytes % 16 == 0) {
+      const int per_row = (int)(row_bytes / 16);
+      for (int e = lane; e < per_row * leaf; e += 32) {
+        const int r = e / per_row, c = e - r * per_row;
+        reinterpret_cast<uint4 *>(base + (int64_t)r * N * esz)[c] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    } else {
+      for (int64_t e = lane; e < row_bytes * leaf; e += 32) {
+        const int64_t r = e / row_bytes, c = e - r * row_bytes;
+        base[r * N * esz + c] = 0;
+      }
+    }
+  }
+}
+
 int materialize(DeviceContext *ctx, const spamm_tree *tc) {
   spamm_tree *t = const_cast<spamm_tree *>(tc);  // the values (zeros) do not change
-  if (t->valid_hi < 0) return SPAMM_OK;
-  const int64_t esz = t->elem_size(), row = t->N * esz;
-  const int64_t r0 = t->valid_lo * t->leaf, r1 = std::min<int64_t>(t->valid_hi * t->leaf, t->N);
-  if (r0 > 0) SPAMM_CUDA_TRY(cudaMemsetAsync(t->padded, 0, (size_t)(r0 * row), ctx->stream));
-  if (r1 < t->N)
-    SPAMM_CUDA_TRY(cudaMemsetAsync((char *)t->padded + r1 * row, 0, (size_t)((t->N - r1) * row),
-                                   ctx->stream));
-  t->valid_hi = -1;
+  if (!t->lazy_empty) return SPAMM_OK;
+  const int64_t G = t->nb * t->nb;
+  const unsigned grid = (unsigned)std::min<int64_t>((G + 7) / 8, (int64_t)ctx->num_sms * 8);
+  zero_unoccupied_kernel<<<grid, 256, 0, ctx->stream>>>((unsigned char *)t->padded, t->N, t->leaf,
+                                                        t->nb, (int)t->elem_size(),
+                                                        t->occ + level_offset(t->depth));
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  t->lazy_empty = false;
   return SPAMM_OK;
 }
 
@@ -1112,6 +1159,13 @@ int spamm_tree_recompute_norms(const spamm_tree *t, double *nsq_host) {
 
 int spamm_tree_device_ptrs(const spamm_tree *t, void **padded, double **nsq, uint8_t **occ) {
   if (!t) { set_error("null tree"); return SPAMM_ERR_VALUE; }
+  if (padded && t->lazy_empty) {  // the caller may read any of the storage
+    DeviceContext *ctx;
+    SPAMM_TRY(get_context(t->device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    SPAMM_TRY(materialize(ctx, t));
+    SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  }
   if (padded) *padded = t->padded;
   if (nsq) *nsq = t->nsq;
   if (occ) *occ = t->occ;

@@ -88,6 +88,31 @@ class InteriorNode:
                                                    self.norm_sq)
 
 
+class PendingBlocks:
+    """An in-flight ``nonzero_blocks(wait=False)`` copy.  ``wait()`` blocks
+    until the blocks are in host memory and returns ``(ids, blocks)``; an
+    unwaited transfer is waited for when the object is collected (the host
+    buffer must outlive the copy)."""
+
+    def __init__(self, handle, ids, blocks):
+        self._handle = handle
+        self.ids = ids
+        self.blocks = blocks
+
+    def wait(self):
+        h, self._handle = self._handle, None
+        if h is not None:
+            _lib.check(_lib.load().spamm_transfer_wait(h))
+        return self.ids, self.blocks
+
+    def __del__(self):
+        if getattr(self, "_handle", None) is not None:
+            try:
+                self.wait()
+            except Exception:  # interpreter shutdown
+                pass
+
+
 def _level_slices(depth):
     out, off = [], 0
     for k in range(depth + 1):
@@ -202,12 +227,16 @@ class QuadTreeMatrix:
         return self._occupied[self.depth]
 
     # -- queries --------------------------------------------------------------
-    def nonzero_blocks(self, out=None):
+    def nonzero_blocks(self, out=None, wait=True):
         """(ids, blocks): the tree's nonzero leaves -- the reference's
         ``_blocks[_leaf_nonzero]`` with their indices i * block_grid + j in
         ascending order -- read back in one transfer (extension: the product
         without its empty blocks).  ``out``: optional C-contiguous
-        (>= count, b, b) host array of the tree's dtype (e.g. pinned)."""
+        (>= count, b, b) host array of the tree's dtype (e.g. pinned).
+
+        ``wait=False`` returns a :class:`PendingBlocks` at once: the copy runs
+        on a separate copy-out stream and overlaps the caller's next calls
+        (pass pinned ``out`` for that); ``.wait()`` yields ``(ids, blocks)``."""
         occ = np.asarray(self._occupied[self.depth]).reshape(-1)
         ids = np.flatnonzero(occ).astype(np.int64)
         b = self.leaf_size
@@ -216,7 +245,14 @@ class QuadTreeMatrix:
         elif (out.dtype != self.dtype or out.ndim != 3 or out.shape[1:] != (b, b)
               or out.shape[0] < len(ids) or not out.flags.c_contiguous):
             raise ValueError("out must be a C-contiguous (>= count, b, b) array of the tree dtype")
-        _lib.check(_lib.load().spamm_tree_blocks_to_host(self._handle, ids.ctypes.data, len(ids),
+        # ids=NULL below: the device lists the nonzero leaves itself (the same
+        # ones as `ids`, both from the occupancy pyramid)
+        if not wait:
+            h = ctypes.c_void_p()
+            _lib.check(_lib.load().spamm_tree_blocks_to_host_async(
+                self._handle, None, len(ids), out.ctypes.data, ctypes.byref(h)))
+            return PendingBlocks(h, ids, out[:len(ids)])
+        _lib.check(_lib.load().spamm_tree_blocks_to_host(self._handle, None, len(ids),
                                                          out.ctypes.data))
         return ids, out[:len(ids)]
 

@@ -336,3 +336,43 @@ def test_nonzero_blocks_match_padded():
         i, j = divmod(int(g), nb)
         dense[i * leaf:(i + 1) * leaf, j * leaf:(j + 1) * leaf] = blk
     assert np.array_equal(dense, c._padded)
+
+
+@pytest.mark.gpu
+def test_nonzero_blocks_async_overlaps_later_calls():
+    """wait=False: the copies of several products are in flight together while
+    later multiplies run; every one lands bit-identical to the synchronous
+    read, and an unwaited transfer is completed when collected."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    n, leaf = 512, 32
+    d = np.abs(np.subtract.outer(np.arange(n), np.arange(n)))
+    x = rng.uniform(-1, 1, (n, n)) * 0.9 ** d
+    t = sp.from_dense(x, leaf_size=leaf)
+    taus = [1e-2, 1e-4, 1e-6, 1e-8]
+    G = t.block_grid ** 2
+    bufs = [torch.empty((G, leaf, leaf), dtype=torch.float64, pin_memory=True).numpy()
+            for _ in taus]
+    pend, prods = [], []
+    for q, tau in enumerate(taus):
+        c, _ = sp.spamm(t, t, sp.SpammConfig(tau=tau))
+        pend.append(c.nonzero_blocks(out=bufs[q], wait=False))
+        prods.append(c)
+    for c, p in zip(prods, pend):
+        ids, blocks = p.wait()
+        ids2, blocks2 = c.nonzero_blocks()
+        assert np.array_equal(ids, ids2)
+        assert np.array_equal(blocks.view(np.uint64), blocks2.view(np.uint64))
+        assert p.wait()[0] is ids  # waiting twice is a no-op
+    # the product may be released before its copy completes
+    c, _ = sp.spamm(t, t, sp.SpammConfig(tau=1e-8))
+    ref = c.nonzero_blocks()[1].copy()
+    p = c.nonzero_blocks(out=bufs[0], wait=False)
+    del c
+    _, blocks = p.wait()
+    assert np.array_equal(blocks.view(np.uint64), ref.view(np.uint64))
+    # an empty tree: nothing to copy
+    z = sp.from_dense(np.zeros((64, 64)), leaf_size=leaf)
+    ids, blocks = z.nonzero_blocks(wait=False).wait()
+    assert len(ids) == 0 and blocks.shape == (0, leaf, leaf)
