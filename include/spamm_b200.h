@@ -11,6 +11,7 @@
  *
  * Reference interfaces replaced (arxiv/paper_1011_3534, pkg/src/spamm):
  *   spamm_tree_from_host      <- quadtree.from_dense          quadtree.py:218-251
+ *   (+ _async / spamm_tree_wait: the same build overlapping queued work)
  *                                (+ QuadTreeMatrix.__init__    quadtree.py:116-151)
  *   spamm_tree_to_host        <- QuadTreeMatrix.to_dense      quadtree.py:184-187, :264-266
  *   spamm_tree_padded_to_host <- QuadTreeMatrix._padded       quadtree.py:145
@@ -122,6 +123,17 @@ SPAMM_API const char *spamm_version(void);
 /* -- trees ---------------------------------------------------------------- */
 SPAMM_API int spamm_tree_from_host(const void *host, int64_t n, int64_t ld, int32_t leaf_size,
                          int32_t dtype, int32_t device, spamm_tree **out);
+/* spamm_tree_from_host without waiting: the host->device copy and the norm
+ * pyramid run on a separate copy-in stream (overlapping work already queued,
+ * e.g. the previous matrix's multiplies) and the call returns at once.  Every
+ * later call on the tree is ordered after the build; `host` must stay valid
+ * (and should be pinned) until spamm_tree_wait(*out) or spamm_tree_free(*out)
+ * returns (free waits for a pending build).  spamm_tree_info_get reports
+ * root_norm_sq as NaN until spamm_tree_wait. */
+SPAMM_API int spamm_tree_from_host_async(const void *host, int64_t n, int64_t ld, int32_t leaf_size,
+                                         int32_t dtype, int32_t device, spamm_tree **out);
+/* Block until an asynchronous build is complete (no-op for other trees). */
+SPAMM_API int spamm_tree_wait(const spamm_tree *t);
 /* `dev` is a device pointer on `device`; n x n with leading dimension ld. */
 SPAMM_API int spamm_tree_from_device(const void *dev, int64_t n, int64_t ld, int32_t leaf_size,
                            int32_t dtype, int32_t device, spamm_tree **out);

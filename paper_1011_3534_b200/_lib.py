@@ -40,7 +40,8 @@ EXPORTED = (
     "spamm_tree_add", "spamm_tree_scale", "spamm_tree_filter_drop", "spamm_tree_diagonal",
     "spamm_tree_blocks_to_host", "spamm_boxes_morton_order", "spamm_tree_toeplitz",
     "spamm_tree_tridiagonal", "spamm_tree_recompute_norms",
-    "spamm_tree_blocks_to_host_async", "spamm_transfer_wait",
+    "spamm_tree_blocks_to_host_async", "spamm_transfer_wait", "spamm_tree_from_host_async",
+    "spamm_tree_wait",
 )
 
 
@@ -87,6 +88,8 @@ def load(path=LIB_PATH):
         L.spamm_version.restype = ctypes.c_char_p
         L.spamm_device_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
         L.spamm_tree_from_host.argtypes = [vp, i64, i64, i32, i32, i32, pp]
+        L.spamm_tree_from_host_async.argtypes = [vp, i64, i64, i32, i32, i32, pp]
+        L.spamm_tree_wait.argtypes = [vp]
         L.spamm_tree_from_device.argtypes = [vp, i64, i64, i32, i32, i32, pp]
         L.spamm_tree_from_padded_device.argtypes = [vp, i64, i64, i32, i32, i32, pp]
         L.spamm_tree_info_get.argtypes = [vp, ctypes.POINTER(TreeInfo)]

@@ -18,7 +18,8 @@
 
 namespace spamm {
 
-int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out);
+int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out,
+               cudaStream_t st = nullptr);
 void free_tree_async(spamm_tree *t, cudaStream_t st);
 int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap,
@@ -247,8 +248,10 @@ SPAMM_API int spamm_tree_filter_drop(const spamm_tree *m, double tau, spamm_tree
   drop_mark_kernel<<<(unsigned)std::min<int64_t>((G + 255) / 256, 4096), 256, 0, ctx->stream>>>(
       m->occ + level_offset(m->depth), m->nrm + level_offset(m->depth), G, tau, drop, count);
   unsigned *hc = (unsigned *)ctx->host_pinned;
-  SPAMM_CUDA_TRY(cudaMemcpyAsync(hc, count, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
-  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  {
+    const SmallRead r{hc, count, sizeof(unsigned)};
+    SPAMM_TRY(read_small_sync(ctx, ctx->stream, &r, 1));
+  }
   *dropped_any = *hc != 0;
   *out = nullptr;
   if (!*hc) return SPAMM_OK;  // nothing drops: the caller keeps the input tree
@@ -273,6 +276,7 @@ SPAMM_API int spamm_tree_blocks_to_host(const spamm_tree *m, const int64_t *ids,
   DeviceContext *ctx;
   SPAMM_TRY(get_context(m->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(tree_join(ctx, m));
   const int64_t esz = m->elem_size(), bytes = count * m->leaf * m->leaf * esz;
   SPAMM_TRY(ensure_scratch(ctx->reduce_tmp, (size_t)(bytes + count * 8 + 256), ctx->stream));
   int64_t *dids = (int64_t *)ctx->reduce_tmp.ptr;
@@ -320,6 +324,7 @@ SPAMM_API int spamm_tree_blocks_to_host_async(const spamm_tree *m, const int64_t
   DeviceContext *ctx;
   SPAMM_TRY(get_context(m->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(tree_join(ctx, m));
   auto *t = new spamm_transfer;
   t->device = m->device;
   const int64_t esz = m->elem_size(), bytes = count * m->leaf * m->leaf * esz;

@@ -86,6 +86,7 @@ struct DeviceContext {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;       // overlaps memory-bound fills with compute
   cudaStream_t copy_out = nullptr;   // device->host result transfers (overlap the next call)
+  cudaStream_t copy_in = nullptr;    // asynchronous builds: host->device copy + K1 (overlap compute)
   cudaEvent_t fork = nullptr, join = nullptr;
   cudaEvent_t ev[8] = {};
   std::mutex mu;
@@ -99,6 +100,7 @@ struct DeviceContext {
   Scratch reduce_tmp;     // misc reduction scratch
   Scratch pyr_tickets;    // pyramid hand-off counters (self-resetting, zero at rest)
   Scratch k1_ticket;      // K1's last-CTA ticket for the fused pyramid (zero at rest)
+  Scratch pyr_tickets_in, k1_ticket_in;  // the same, for builds on copy_in
   Scratch dn_masks;       // dense traversal: two work sets (zero at rest)
   size_t dn_set_words = 0;  // words per dense work set
   int dense_parity = 0;     // which dense work set the next dense call uses
@@ -113,6 +115,7 @@ struct DeviceContext {
   size_t cull_capacity = 0;   // survivor capacity per ping-pong buffer (items)
   size_t pruned_capacity = 0; // pruned capacity (items, all tiers)
   void *host_pinned = nullptr;  // small pinned staging for counters
+  Scratch host_stage;           // pinned staging of read_small_sync (grow-only)
   std::vector<Scratch> xfer_free;  // idle device staging buffers of async block transfers
 };
 
@@ -123,6 +126,18 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed = 
 // copy engine and so queues behind device->host copies in flight (an async
 // product read-back would otherwise stall the next multiply).
 int zero_async(void *p, size_t bytes, cudaStream_t st, int ctas);
+
+// Small device->host reads (statistics, root norms, pyramids) without the
+// copy engines: a kernel stores the bytes into pinned host memory, then the
+// stream is synchronised and the bytes are copied to their destinations.  A
+// cudaMemcpy would queue behind bulk device->host copies in flight on the
+// copy-out stream (same engine); these stores interleave with them on PCIe.
+struct SmallRead {
+  void *host;
+  const void *dev;
+  size_t bytes;
+};
+int read_small_sync(DeviceContext *ctx, cudaStream_t st, const SmallRead *r, int n);
 
 }  // namespace spamm
 
@@ -145,6 +160,11 @@ struct spamm_tree {
   // filled on the first whole-storage access (materialize()).  A row-sharded
   // product (band tree) is the same thing: blocks outside its rows are empty.
   bool lazy_empty = false;
+  // Asynchronous build (spamm_tree_from_host_async): copy + K1 run on the
+  // context's copy_in stream; every later use orders itself after `ready`
+  // (tree_join), and root_norm_sq is fetched on the first spamm_tree_wait.
+  cudaEvent_t ready = nullptr;
+  bool root_pending = false;
   int64_t elem_size() const { return dtype == SPAMM_DTYPE_F64 ? 8 : 4; }
 };
 
@@ -152,4 +172,6 @@ namespace spamm {
 struct DeviceContext;
 // zero-fill a lazy tree's empty blocks (stream-ordered on ctx->stream)
 int materialize(DeviceContext *ctx, const spamm_tree *t);
+// order ctx->stream after an asynchronous build of t (no-op otherwise)
+int tree_join(DeviceContext *ctx, const spamm_tree *t);
 }  // namespace spamm

@@ -17,7 +17,8 @@
 
 namespace spamm {
 
-int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out);
+int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out,
+               cudaStream_t st = nullptr);
 void free_tree_async(spamm_tree *t, cudaStream_t st);
 int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap,

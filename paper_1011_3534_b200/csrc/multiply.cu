@@ -25,7 +25,8 @@ struct spamm_product {
 
 namespace spamm {
 
-int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out);
+int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out,
+               cudaStream_t st = nullptr);
 void free_tree_async(spamm_tree *t, cudaStream_t st);
 int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap,
@@ -91,6 +92,8 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   SPAMM_TRY(get_context(a->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
   cudaStream_t st = ctx->stream;
+  SPAMM_TRY(tree_join(ctx, a));
+  SPAMM_TRY(tree_join(ctx, b));
   const int depth = a->depth;
   const int64_t nb = a->nb;
   const int64_t G = nb * nb;
@@ -271,9 +274,11 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     }
     ctx->last_overlapped = overlapped;
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
-    SPAMM_CUDA_BREAK(cudaMemcpyAsync(hc, dtc, sizeof(TraverseCounters), cudaMemcpyDeviceToHost, st));
-    SPAMM_CUDA_BREAK(cudaMemcpyAsync(&c->root_norm_sq, c->nsq, sizeof(double), cudaMemcpyDeviceToHost, st));
-    SPAMM_CUDA_BREAK(cudaStreamSynchronize(st));
+    {
+      const SmallRead r[2] = {{hc, dtc, sizeof(TraverseCounters)},
+                              {&c->root_norm_sq, c->nsq, sizeof(double)}};
+      if ((rc = read_small_sync(ctx, st, r, 2))) break;
+    }
     if (tv_timeline && ta.timeline) {
       std::vector<unsigned long long> tl(4 * 4096);
       cudaMemcpy(tl.data(), tv_tl, sizeof(unsigned long long) * 4 * 4096, cudaMemcpyDeviceToHost);

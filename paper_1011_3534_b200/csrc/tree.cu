@@ -7,6 +7,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -49,6 +50,7 @@ int get_context(int device, DeviceContext **out) {
     SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+    SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
     SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
     SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming));
     for (auto &e : ctx->ev) SPAMM_CUDA_TRY(cudaEventCreate(&e));
@@ -84,6 +86,53 @@ int zero_async(void *p, size_t bytes, cudaStream_t st, int ctas) {
   const unsigned grid = (unsigned)std::min<size_t>(want, (size_t)std::max(ctas, 1));
   zero_fill_kernel<<<grid, 256, 0, st>>>((unsigned char *)p, bytes);
   SPAMM_CUDA_TRY(cudaGetLastError());
+  return SPAMM_OK;
+}
+
+// dst: pinned host memory (device-visible through UVA)
+__global__ void store_to_host_kernel(unsigned char *__restrict__ dst,
+                                     const unsigned char *__restrict__ src, size_t bytes) {
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x,
+               stride = (size_t)gridDim.x * blockDim.x;
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const size_t q = bytes / 16;
+    for (size_t i = tid; i < q; i += stride)
+      reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+    for (size_t i = q * 16 + tid; i < bytes; i += stride) dst[i] = src[i];
+  } else {
+    for (size_t i = tid; i < bytes; i += stride) dst[i] = src[i];
+  }
+}
+
+int read_small_sync(DeviceContext *ctx, cudaStream_t st, const SmallRead *r, int n) {
+  size_t total = 0;
+  for (int q = 0; q < n; ++q) total += (r[q].bytes + 255) / 256 * 256;
+  if (ctx->host_stage.bytes < total) {
+    SPAMM_CUDA_TRY(cudaStreamSynchronize(st));  // the old stage may be in use by st
+    if (ctx->host_stage.ptr) SPAMM_CUDA_TRY(cudaFreeHost(ctx->host_stage.ptr));
+    ctx->host_stage.ptr = nullptr;
+    ctx->host_stage.bytes = 0;
+    const size_t want = std::max<size_t>(total + total / 4, 1 << 16);
+    SPAMM_CUDA_TRY(cudaMallocHost(&ctx->host_stage.ptr, want));
+    ctx->host_stage.bytes = want;
+  }
+  unsigned char *stage = (unsigned char *)ctx->host_stage.ptr;
+  size_t off = 0;
+  for (int q = 0; q < n; ++q) {
+    if (r[q].bytes) {
+      const unsigned grid = (unsigned)std::min<size_t>((r[q].bytes / 16 + 255) / 256 + 1, 64);
+      store_to_host_kernel<<<grid, 256, 0, st>>>(stage + off, (const unsigned char *)r[q].dev,
+                                                 r[q].bytes);
+    }
+    off += (r[q].bytes + 255) / 256 * 256;
+  }
+  SPAMM_CUDA_TRY(cudaGetLastError());
+  SPAMM_CUDA_TRY(cudaStreamSynchronize(st));
+  off = 0;
+  for (int q = 0; q < n; ++q) {
+    if (r[q].bytes && r[q].host != stage + off) memcpy(r[q].host, stage + off, r[q].bytes);
+    off += (r[q].bytes + 255) / 256 * 256;
+  }
   return SPAMM_OK;
 }
 
@@ -835,8 +884,11 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap,
                         unsigned *grp_done, unsigned grp_target, const int *overflow,
                         unsigned long long *t_end) {
-  SPAMM_TRY(ensure_scratch(ctx->k1_ticket, sizeof(unsigned), st, /*zeroed=*/true));
-  unsigned *ticket = (unsigned *)ctx->k1_ticket.ptr;
+  // builds on copy_in run concurrently with the main stream's: own tickets
+  Scratch &k1t = st == ctx->copy_in ? ctx->k1_ticket_in : ctx->k1_ticket;
+  Scratch &pyt = st == ctx->copy_in ? ctx->pyr_tickets_in : ctx->pyr_tickets;
+  SPAMM_TRY(ensure_scratch(k1t, sizeof(unsigned), st, /*zeroed=*/true));
+  unsigned *ticket = (unsigned *)k1t.ptr;
   bool fused = false;
   // list mode follows the leaf-product kernel: launch it programmatically so
   // its CTAs are resident (and waiting) as that kernel's CTAs retire
@@ -859,16 +911,18 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
   } else {
     // tickets start (and are left) at zero
     const size_t need = sizeof(unsigned) * (size_t)std::max<int64_t>(pl.n_counters, 1);
-    SPAMM_TRY(ensure_scratch(ctx->pyr_tickets, need, st, /*zeroed=*/true));
+    SPAMM_TRY(ensure_scratch(pyt, need, st, /*zeroed=*/true));
     pyramid_fused_kernel<<<(unsigned)(int64_t(1) << (2 * (pl.from[0] - pl.L[0]))), PYR_THREADS, 0,
-                           st>>>(t->nsq, t->occ, t->nrm, pl, (unsigned *)ctx->pyr_tickets.ptr);
+                           st>>>(t->nsq, t->occ, t->nrm, pl, (unsigned *)pyt.ptr);
   }
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (launches) ++*launches;
   return SPAMM_OK;
 }
 
-int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out) {
+int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out,
+               cudaStream_t st = nullptr) {
+  if (!st) st = ctx->stream;
   auto t = std::make_unique<spamm_tree>();
   t->n = n;
   t->leaf = leaf;
@@ -878,18 +932,27 @@ int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm
   t->dtype = dtype;
   t->device = ctx->device;
   const int64_t esz = t->elem_size();
-  SPAMM_CUDA_TRY(cudaMallocAsync(&t->padded, (size_t)(t->N * t->N * esz), ctx->stream));
+  SPAMM_CUDA_TRY(cudaMallocAsync(&t->padded, (size_t)(t->N * t->N * esz), st));
   SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->nsq, sizeof(double) * pyramid_size(t->depth),
-                                 ctx->stream));
-  SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->occ, pyramid_size(t->depth), ctx->stream));
+                                 st));
+  SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->occ, pyramid_size(t->depth), st));
   SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->nrm, sizeof(double) * pyramid_size(t->depth),
-                                 ctx->stream));
+                                 st));
   *out = t.release();
+  return SPAMM_OK;
+}
+
+int tree_join(DeviceContext *ctx, const spamm_tree *t) {
+  if (t && t->ready) SPAMM_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, t->ready, 0));
   return SPAMM_OK;
 }
 
 void free_tree_async(spamm_tree *t, cudaStream_t st) {
   if (!t) return;
+  if (t->ready) {  // (st is the library's stream, which may not have joined yet)
+    cudaStreamWaitEvent(st, t->ready, 0);
+    cudaEventDestroy(t->ready);
+  }
   if (t->padded) cudaFreeAsync(t->padded, st);
   if (t->nsq) cudaFreeAsync(t->nsq, st);
   if (t->occ) cudaFreeAsync(t->occ, st);
@@ -924,6 +987,7 @@ __global__ void zero_unoccupied_kernel(unsigned char *__restrict__ padded, int64
 
 int materialize(DeviceContext *ctx, const spamm_tree *tc) {
   spamm_tree *t = const_cast<spamm_tree *>(tc);  // the values (zeros) do not change
+  SPAMM_TRY(tree_join(ctx, t));
   if (!t->lazy_empty) return SPAMM_OK;
   const int64_t G = t->nb * t->nb;
   const unsigned grid = (unsigned)std::min<int64_t>((G + 7) / 8, (int64_t)ctx->num_sms * 8);
@@ -936,10 +1000,8 @@ int materialize(DeviceContext *ctx, const spamm_tree *tc) {
 }
 
 int finish_tree(DeviceContext *ctx, spamm_tree *t) {
-  SPAMM_CUDA_TRY(cudaMemcpyAsync(&t->root_norm_sq, t->nsq, sizeof(double), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
-  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  return SPAMM_OK;
+  const SmallRead r{&t->root_norm_sq, t->nsq, sizeof(double)};
+  return read_small_sync(ctx, ctx->stream, &r, 1);
 }
 
 static int validate_shape(int64_t n, int64_t ld, int32_t leaf, int32_t dtype) {
@@ -1051,6 +1113,66 @@ int spamm_tree_from_host(const void *host, int64_t n, int64_t ld, int32_t leaf, 
   return tree_from(host, true, n, ld, leaf, dtype, device, out);
 }
 
+int spamm_tree_from_host_async(const void *host, int64_t n, int64_t ld, int32_t leaf,
+                               int32_t dtype, int32_t device, spamm_tree **out) {
+  SPAMM_TRY(validate_shape(n, ld, leaf, dtype));
+  if (!out) {
+    set_error("null argument");
+    return SPAMM_ERR_VALUE;
+  }
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  // everything on copy_in: allocation, padding, copy, K1 + pyramid (its own
+  // tickets), then the `ready` event later uses wait on
+  cudaStream_t st = ctx->copy_in;
+  spamm_tree *t = nullptr;
+  SPAMM_TRY(alloc_tree(ctx, n, leaf, dtype, &t, st));
+  const int64_t esz = t->elem_size();
+  int rc = SPAMM_OK;
+  do {
+    if (t->N != n && (rc = zero_async(t->padded, (size_t)(t->N * t->N * esz), st, 4 * ctx->num_sms)))
+      break;
+    cudaError_t e = cudaMemcpy2DAsync(t->padded, (size_t)(t->N * esz), host, (size_t)(ld * esz),
+                                      (size_t)(n * esz), (size_t)n, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) { set_error("copy: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
+    rc = build_pyramid_async(ctx, t, st, nullptr, nullptr, nullptr, 0, nullptr, 0, nullptr, nullptr);
+    if (rc) break;
+    e = cudaEventCreateWithFlags(&t->ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(t->ready, st);
+    if (e != cudaSuccess) { set_error("event: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }
+    t->root_pending = true;
+  } while (0);
+  if (rc) {
+    cudaStreamSynchronize(st);
+    if (t->ready) {
+      cudaEventDestroy(t->ready);
+      t->ready = nullptr;
+    }
+    free_tree_async(t, st);
+    return rc;
+  }
+  *out = t;
+  return SPAMM_OK;
+}
+
+int spamm_tree_wait(const spamm_tree *tc) {
+  if (!tc) { set_error("null tree"); return SPAMM_ERR_VALUE; }
+  spamm_tree *t = const_cast<spamm_tree *>(tc);  // completes a pending build; values unchanged
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(t->device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (!t->ready) return SPAMM_OK;
+  SPAMM_CUDA_TRY(cudaEventSynchronize(t->ready));
+  if (t->root_pending) {
+    SPAMM_TRY(tree_join(ctx, t));
+    const SmallRead r{&t->root_norm_sq, t->nsq, sizeof(double)};
+    SPAMM_TRY(read_small_sync(ctx, ctx->stream, &r, 1));
+    t->root_pending = false;
+  }
+  return SPAMM_OK;
+}
+
 int spamm_tree_from_device(const void *dev, int64_t n, int64_t ld, int32_t leaf, int32_t dtype,
                            int32_t device, spamm_tree **out) {
   return tree_from(dev, false, n, ld, leaf, dtype, device, out);
@@ -1078,7 +1200,7 @@ int spamm_tree_info_get(const spamm_tree *t, spamm_tree_info *info) {
   info->depth = t->depth;
   info->dtype = t->dtype;
   info->device = t->device;
-  info->root_norm_sq = t->root_norm_sq;
+  info->root_norm_sq = t->root_pending ? NAN : t->root_norm_sq;  // (spamm_tree_wait fetches it)
   return SPAMM_OK;
 }
 
@@ -1113,12 +1235,11 @@ int spamm_tree_pyramid_to_host(const spamm_tree *t, double *nsq, uint8_t *occ) {
   DeviceContext *ctx;
   SPAMM_TRY(get_context(t->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_TRY(tree_join(ctx, t));
   const int64_t P = pyramid_size(t->depth);
-  if (nsq) SPAMM_CUDA_TRY(cudaMemcpyAsync(nsq, t->nsq, sizeof(double) * P, cudaMemcpyDeviceToHost,
-                                          ctx->stream));
-  if (occ) SPAMM_CUDA_TRY(cudaMemcpyAsync(occ, t->occ, P, cudaMemcpyDeviceToHost, ctx->stream));
-  SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  return SPAMM_OK;
+  const SmallRead r[2] = {{nsq, t->nsq, nsq ? sizeof(double) * P : 0},
+                         {occ, t->occ, occ ? (size_t)P : 0}};
+  return read_small_sync(ctx, ctx->stream, r, 2);
 }
 
 int spamm_tree_recompute_norms(const spamm_tree *t, double *nsq_host) {
@@ -1159,11 +1280,12 @@ int spamm_tree_recompute_norms(const spamm_tree *t, double *nsq_host) {
 
 int spamm_tree_device_ptrs(const spamm_tree *t, void **padded, double **nsq, uint8_t **occ) {
   if (!t) { set_error("null tree"); return SPAMM_ERR_VALUE; }
-  if (padded && t->lazy_empty) {  // the caller may read any of the storage
+  if ((padded && t->lazy_empty) || t->ready) {  // the caller may read any of the storage
     DeviceContext *ctx;
     SPAMM_TRY(get_context(t->device, &ctx));
     std::lock_guard<std::mutex> lk(ctx->mu);
-    SPAMM_TRY(materialize(ctx, t));
+    if (padded) SPAMM_TRY(materialize(ctx, t));
+    else SPAMM_TRY(tree_join(ctx, t));
     SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   }
   if (padded) *padded = t->padded;
@@ -1206,6 +1328,9 @@ void spamm_tree_free(spamm_tree *t) {
   DeviceContext *ctx;
   if (get_context(t->device, &ctx) != SPAMM_OK) return;
   std::lock_guard<std::mutex> lk(ctx->mu);
+  // an asynchronous build may still be reading the caller's host array: the
+  // caller may release that array once this returns
+  if (t->ready) cudaEventSynchronize(t->ready);
   free_tree_async(t, ctx->stream);
 }
 

@@ -142,15 +142,37 @@ class QuadTreeMatrix:
         self.padded_dim = int(info.padded_dim)
         self.dtype = _SUPPORTED_DTYPES[info.dtype]
         self.device = int(info.device)
-        self._root_norm_sq = float(info.root_norm_sq)
+        self._root_nsq = float(info.root_norm_sq)
+        self._pending = False  # an asynchronous build (from_dense(wait=False))
+        self._src = None       # ... and the host array it reads
         self._host_padded = None
         self._host_pyramid = None
         self._root = None
+
+    @property
+    def _root_norm_sq(self):
+        if self._pending:
+            self.wait()
+        return self._root_nsq
+
+    def wait(self):
+        """Block until an asynchronous build (``from_dense(wait=False)``) is
+        complete; returns the tree.  A no-op for every other tree."""
+        if self._pending:
+            L = _lib.load()
+            _lib.check(L.spamm_tree_wait(self._handle))
+            info = _lib.TreeInfo()
+            _lib.check(L.spamm_tree_info_get(self._handle, ctypes.byref(info)))
+            self._root_nsq = float(info.root_norm_sq)
+            self._pending = False
+            self._src = None
+        return self
 
     def __del__(self):
         h = getattr(self, "_handle", None)
         if h is not None and h.value:
             try:
+                # (a pending build is waited for inside: it may read _src)
                 _lib.load().spamm_tree_free(h)
             except Exception:  # interpreter shutdown
                 pass
@@ -304,11 +326,18 @@ def _wrap(handle):
     return QuadTreeMatrix(handle, _internal=True)
 
 
-def from_dense(dense, leaf_size=4, dtype=None, device=None):
+def from_dense(dense, leaf_size=4, dtype=None, device=None, wait=True):
     """Build a device quadtree from a dense square array (quadtree.py:218-251).
 
     Validation and exception types follow the reference; the padding, the
     leaf norms and the pyramid are computed on the GPU.
+
+    ``wait=False`` (extension): return at once; the host->device copy and
+    the pyramid run on a separate copy-in stream, overlapping work already
+    queued (e.g. the previous matrix's multiplies).  Every later call on the
+    tree is ordered after the build.  Pass pinned host memory for the copy to
+    be truly asynchronous; the tree keeps a reference to the array until
+    ``wait()`` (or its first host-side use of the root norm).
     """
     if leaf_size < 1 or (leaf_size & (leaf_size - 1)) != 0:
         raise ValueError(f"leaf_size must be a power of two >= 1, got {leaf_size}")
@@ -325,6 +354,13 @@ def from_dense(dense, leaf_size=4, dtype=None, device=None):
     h = ctypes.c_void_p()
     dev = get_device() if device is None else int(device)
     code = _lib.DTYPE_F64 if target == np.float64 else _lib.DTYPE_F32
+    if not wait:
+        _lib.check(_lib.load().spamm_tree_from_host_async(arr.ctypes.data, n, n, int(leaf_size),
+                                                          code, dev, ctypes.byref(h)))
+        t = _wrap(h.value)
+        t._pending = True
+        t._src = arr
+        return t
     _lib.check(_lib.load().spamm_tree_from_host(arr.ctypes.data, n, n, int(leaf_size), code,
                                                 dev, ctypes.byref(h)))
     return _wrap(h.value)

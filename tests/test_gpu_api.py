@@ -376,3 +376,40 @@ def test_nonzero_blocks_async_overlaps_later_calls():
     z = sp.from_dense(np.zeros((64, 64)), leaf_size=leaf)
     ids, blocks = z.nonzero_blocks(wait=False).wait()
     assert len(ids) == 0 and blocks.shape == (0, leaf, leaf)
+
+
+@pytest.mark.gpu
+def test_from_dense_async_matches_sync():
+    """from_dense(wait=False): the build overlaps queued multiplies; the tree,
+    its root norm and every product with it are identical to the synchronous
+    build's, and a pending tree may be dropped before its build completes."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    for n, leaf in ((300, 16), (1024, 64)):
+        d = np.abs(np.subtract.outer(np.arange(n), np.arange(n)))
+        x = rng.uniform(-1, 1, (n, n)) * 0.9 ** d
+        pin = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+        pin[...] = x
+        ref = sp.from_dense(x, leaf_size=leaf)
+        busy, _ = sp.spamm(ref, ref, sp.SpammConfig(tau=0.0))  # work queued ahead
+        t = sp.from_dense(pin, leaf_size=leaf, wait=False)
+        c_ref, st_ref = sp.spamm(ref, ref, sp.SpammConfig(tau=1e-6))
+        c, st = sp.spamm(t, t, sp.SpammConfig(tau=1e-6))  # ordered after the build
+        assert st.leaf_matmuls == st_ref.leaf_matmuls
+        assert np.array_equal(c._padded.view(np.uint64), c_ref._padded.view(np.uint64))
+        assert t.norm() == ref.norm()
+        for k in range(t.depth + 1):
+            assert np.array_equal(t._norm_sq[k].view(np.uint64), ref._norm_sq[k].view(np.uint64))
+            assert np.array_equal(t._occupied[k], ref._occupied[k])
+        assert np.array_equal(t.to_dense(), x)
+        assert t.wait() is t
+        p2 = sp.from_dense(pin, leaf_size=leaf, wait=False)
+        del p2  # dropped while (possibly) in flight
+        del busy
+    # dtype conversion and padding on the async path
+    y = rng.uniform(-1, 1, (70, 70))
+    a = sp.from_dense(y, leaf_size=8, dtype=np.float32, wait=False)
+    b = sp.from_dense(y, leaf_size=8, dtype=np.float32)
+    assert a.norm() == b.norm()
+    assert np.array_equal(a._padded, b._padded)
