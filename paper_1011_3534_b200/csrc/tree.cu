@@ -615,6 +615,239 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
   }
 }
 
+// ------------------------------------------------ K1, segmented chains
+// The reference's leaf norm is one sequential chain acc = rn(acc + s_i),
+// s_i = rn(x_i^2) >= 0, over the leaf in row-major order (quadtree.py:80-87):
+// b^2 dependent adds (4096 x ~8 cycles at b = 64).  For the C tree (a few
+// hundred to a few thousand leaves right after the products) that latency,
+// not bandwidth, bounds the multiply's tail.  This kernel gives each leaf a
+// warp, splits the chain into 64 row-major segments (two per lane) and still
+// reproduces the chain's bits exactly:
+//
+//  * While acc stays inside one binade [2^E, 2^(E+1)) every double there is
+//    a multiple of u = 2^(E-52), so rn(acc + s) = acc + rnd_u(s), rnd_u =
+//    nearest multiple of u -- unless s sits exactly half-way (a tie: its
+//    rounding depends on acc's last bit).  A segment that stays in one
+//    binade therefore adds D * u, D = sum of rnd_u(s_i) as an exact integer,
+//    wherever in that binade it starts.
+//  * Each lane predicts its segments' binades from a float prefix sum of the
+//    s_i (relative error ~1e-12, margin 2^-30) and forms D in integers,
+//    flagging ties.
+//  * The segments are applied in order.  A segment is applied as acc + D*u
+//    only if acc >= 2^E and acc + D*u < 2^(E+1) -- the exact condition for
+//    all its (monotone) partial sums to stay in the binade -- and it had no
+//    tie; otherwise (binade crossings, ties, tiny or non-finite values,
+//    segment 0) its lane runs the plain chain from the exact acc.  The
+//    result is the sequential chain's, bit for bit.  (On c2's products ~9 of
+//    64 segments take the plain chain: ~600 dependent adds instead of 4096.)
+// The leaf is staged in shared memory with coalesced 16-byte cp.async copies
+// (segments padded by 16 bytes; lane l starts its passes at element l, which
+// spreads the per-lane segment reads over distinct banks).  Lanes publish
+// (simple, E, D) per segment in a table; lane 0 then walks the 64 segments in
+// order, merging consecutive simple segments of one binade into a run
+// (integer D sums: no floating-point dependency), applying each run with one
+// exact add and running the plain chain over the other segments.
+constexpr int SEG_WARPS = 6;
+constexpr int SEG_PAD = 16;  // bytes after each staged segment
+
+template <typename T, int LEAF>
+__host__ __device__ constexpr int seg_stride() {  // bytes per staged segment
+  return LEAF * LEAF / 64 * (int)sizeof(T) + SEG_PAD;
+}
+template <typename T, int LEAF>
+__host__ __device__ constexpr int seg_warp_bytes() {
+  return 64 * seg_stride<T, LEAF>();
+}
+
+struct SegInfo {
+  long long D;  // sum of rnd_u(s_i) (simple segments)
+  int E;        // binade exponent (simple segments)
+  int simple;
+};
+
+template <typename T, int LEAF>
+__device__ __forceinline__ double seg_chain(const unsigned char *seg_base, double acc) {
+  constexpr int L = LEAF * LEAF / 64;
+  const T *x = reinterpret_cast<const T *>(seg_base);
+#pragma unroll 16
+  for (int i = 0; i < L; ++i) {
+    const double v = (double)x[i];
+    acc = __dadd_rn(acc, __dmul_rn(v, v));
+  }
+  return acc;
+}
+
+template <typename T, int LEAF>
+__global__ void __launch_bounds__(32 * SEG_WARPS) leaf_norm_seg_kernel(
+    T *__restrict__ padded, int64_t N, int64_t nb, double *__restrict__ nsq_leaf,
+    uint8_t *__restrict__ occ_leaf, const uint32_t *__restrict__ list, const unsigned *list_count,
+    PyrTail tail, unsigned smem_bytes) {
+  using U = typename Bits<T>::U;
+  constexpr int L = LEAF * LEAF / 64;  // segment length (elements), >= 16
+  constexpr int EPV = 16 / (int)sizeof(T);
+  constexpr int SS = seg_stride<T, LEAF>();
+  extern __shared__ __align__(16) unsigned char seg_smem[];
+  __shared__ SegInfo tbl[SEG_WARPS][64];
+  if (tail.pdl_wait) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char *wsm = seg_smem + (size_t)warp * seg_warp_bytes<T, LEAF>();
+  const int64_t n_leaves = list ? (int64_t)*list_count : nb * nb;
+  const int64_t gw = (int64_t)blockIdx.x * SEG_WARPS + warp;
+  const int64_t nw = (int64_t)gridDim.x * SEG_WARPS;
+  const bool check_flags = tail.grp_done && !*(volatile const int *)tail.overflow;
+  for (int64_t lx = gw; lx < n_leaves; lx += nw) {
+    const int64_t leaf = list ? (int64_t)list[lx] : lx;
+    const int64_t bi = leaf / nb, bj = leaf - bi * nb;
+    if (check_flags) {  // the leaf-product kernel has stored every tile of this block
+      const unsigned *flag = tail.grp_done + lx;
+      for (;;) {
+        unsigned v;
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v >= tail.grp_target) break;
+        __nanosleep(128);
+      }
+    }
+    T *base = padded + (bi * LEAF) * N + bj * LEAF;
+    __syncwarp();  // (the previous leaf's readers are done with the stage)
+#pragma unroll 8
+    for (int c = lane; c < LEAF * LEAF / EPV; c += 32) {
+      const int e = c * EPV;
+      const int sg = e / L, off = e % L;
+      cp_async16(wsm + sg * SS + off * (int)sizeof(T), base + (int64_t)(e / LEAF) * N + (e % LEAF));
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    // pass 1, segments lane and lane + 32: raw-bit OR, float sum estimates
+    U bits = 0;
+    bool finite[2];
+    double est[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const T *sx = reinterpret_cast<const T *>(wsm + (lane + 32 * h) * SS);
+      double p4[4] = {0.0, 0.0, 0.0, 0.0};
+      bool fin = true;
+#pragma unroll 16
+      for (int i = 0; i < L; ++i) {
+        const T x = sx[(i + lane) & (L - 1)];
+        bits |= Bits<T>::of(x);
+        const double sq = __dmul_rn((double)x, (double)x);
+        fin &= sq <= 1.79e308;  // false for inf and NaN
+        p4[i & 3] += sq;
+      }
+      finite[h] = fin;
+      est[h] = (p4[0] + p4[1]) + (p4[2] + p4[3]);
+    }
+    double pre0 = est[0], pre1 = est[1];  // inclusive scans in segment order
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y0 = __shfl_up_sync(0xffffffffu, pre0, o);
+      const double y1 = __shfl_up_sync(0xffffffffu, pre1, o);
+      if (lane >= o) {
+        pre0 += y0;
+        pre1 += y1;
+      }
+    }
+    pre1 += __shfl_sync(0xffffffffu, pre0, 31);
+    // predicted binade of each segment; D = sum of rnd_u(s_i) where it is one
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int seg = lane + 32 * h;
+      const double hi_est = h ? pre1 : pre0, lo_est = hi_est - est[h];
+      const double za = lo_est * (1.0 - 0x1p-30), zz = hi_est * (1.0 + 0x1p-30);
+      int ea = 0, ez = 0;
+      frexp(za, &ea);
+      frexp(zz, &ez);
+      bool simp = finite[h] && seg > 0 && za > 0x1p-900 && zz < 0x1p+1000 && ea == ez;
+      long long d = 0;
+      if (simp) {
+        const T *sx = reinterpret_cast<const T *>(wsm + seg * SS);
+        const double inv_u = ldexp(1.0, 53 - ea);  // 2^-(E-52), E = ea - 1: exact power of two
+        bool tie = false;
+#pragma unroll 16
+        for (int i = 0; i < L; ++i) {
+          const double x = (double)sx[(i + lane) & (L - 1)];
+          const double q = __dmul_rn(__dmul_rn(x, x), inv_u);  // exact scaling
+          const double fl = floor(q), fr = q - fl;               // both exact
+          tie |= fr == 0.5 || q >= 0x1p53;  // (q >= 2^53: the estimate was off)
+          d += (long long)fmin(fl, 0x1p53) + (fr > 0.5 ? 1 : 0);
+        }
+        simp = !tie;
+      }
+      tbl[warp][seg] = SegInfo{d, ea - 1, (int)simp};  // E: za in [2^E, 2^(E+1))
+    }
+    __syncwarp();
+    // lane 0: the segments in order -- runs of simple segments of one binade
+    // applied with one exact add each, everything else by the plain chain
+    if (lane == 0) {
+      double acc = 0.0;
+      int run0 = -1, runE = 0;
+      long long runD = 0;
+      auto close_run = [&](int end) {
+        if (run0 < 0) return;
+        const double lo = ldexp(1.0, runE);
+        const double v = acc + (double)runD * ldexp(1.0, runE - 52);  // exact when it applies
+        if (runD < (1ll << 52) && acc >= lo && v < 2.0 * lo) {
+          acc = v;  // every partial sum of the run stayed in [2^E, 2^(E+1))
+        } else {
+          for (int sg = run0; sg < end; ++sg) acc = seg_chain<T, LEAF>(wsm + sg * SS, acc);
+        }
+        run0 = -1;
+      };
+      for (int sg = 0; sg < 64; ++sg) {
+        const SegInfo si = tbl[warp][sg];
+        if (si.simple && run0 >= 0 && si.E == runE) {
+          runD += si.D;
+          continue;
+        }
+        close_run(sg);
+        if (si.simple) {
+          run0 = sg;
+          runE = si.E;
+          runD = si.D;
+        } else {
+          acc = seg_chain<T, LEAF>(wsm + sg * SS, acc);
+        }
+      }
+      close_run(64);
+      tbl[warp][0].D = __double_as_longlong(acc);
+    }
+    __syncwarp();
+    const double acc = __longlong_as_double(tbl[warp][0].D);
+    // occupancy / -0.0 (as the staged kernel): OR of every lane's raw bits
+    unsigned long long all = (unsigned long long)bits;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) all |= __shfl_xor_sync(0xffffffffu, all, o);
+    const bool nz = (U)((U)all << 1) != 0;
+    if (!nz && all) {  // all zero with some -0.0: canonicalise to +0.0
+      for (int e = lane; e < LEAF * LEAF; e += 32) base[(int64_t)(e / LEAF) * N + (e % LEAF)] = T(0);
+    }
+    if (lane == 0) {
+      nsq_leaf[leaf] = acc;
+      occ_leaf[leaf] = (uint8_t)nz;
+      tail.nrm[level_offset(tail.depth) + leaf] = __dsqrt_rn(acc);
+      if (tail.grp_done) tail.grp_done[lx] = 0u;  // zero at rest for the next product
+    }
+  }
+  if (tail.ticket) {  // the last CTA builds the pyramid
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(tail.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      pyramid_cta(tail, seg_smem, smem_bytes);
+      if (threadIdx.x == 0) {
+        *tail.ticket = 0u;
+        if (tail.t_end) *tail.t_end = k1_gt();
+      }
+    }
+  }
+}
+
 // Direct kernel for tiny leaves (b * b * sizeof(T) < 128): one thread per
 // leaf reads its b x b elements in row-major order straight from global.
 template <typename T>
@@ -894,7 +1127,54 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
   // its CTAs are resident (and waiting) as that kernel's CTAs retire
   K1Overlap ovs{grp_done, grp_target, overflow, t_end, list != nullptr && t_end != nullptr};
   const K1Overlap *ov = (grp_done || t_end) ? &ovs : nullptr;
-  if (t->dtype == SPAMM_DTYPE_F64)
+  // list mode (C's tree): the segmented-chain kernel, a warp per leaf
+  static const bool no_seg = getenv("SPAMM_NO_SEG_CHAIN") != nullptr;
+  if (list && !no_seg && (t->leaf == 32 || t->leaf == 64)) {
+    const bool f64 = t->dtype == SPAMM_DTYPE_F64;
+    PyrTail tail{};
+    tail.nsq = t->nsq;
+    tail.occ = t->occ;
+    tail.nrm = t->nrm;
+    tail.depth = t->depth;
+    tail.ticket = t->depth <= PYR_TAIL_MAX_DEPTH ? ticket : nullptr;
+    if (ov) {
+      tail.grp_done = ov->grp_done;
+      tail.grp_target = ov->grp_target;
+      tail.overflow = ov->overflow;
+      tail.t_end = ov->t_end;
+      tail.pdl_wait = ov->pdl && !ov->grp_done;
+    }
+    // shared memory: a staged leaf per warp (one CTA per SM)
+    const unsigned smem = (unsigned)(SEG_WARPS * (t->leaf == 64
+        ? (f64 ? seg_warp_bytes<double, 64>() : seg_warp_bytes<float, 64>())
+        : (f64 ? seg_warp_bytes<double, 32>() : seg_warp_bytes<float, 32>())));
+    const int64_t cap = std::min<int64_t>(list_cap, t->nb * t->nb);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((cap + SEG_WARPS - 1) / SEG_WARPS,
+                             (int64_t)ctx->num_sms)));
+    cfg.blockDim = dim3(32 * SEG_WARPS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    if (ov && (ov->grp_done || ov->pdl)) {
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+    }
+    auto launch = [&](auto kern, auto *data) -> int {
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SPAMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, data, t->N, t->nb, t->nsq + level_offset(t->depth),
+                                        t->occ + level_offset(t->depth), list, list_count, tail, smem));
+      return SPAMM_OK;
+    };
+    double *pd = (double *)t->padded;
+    float *pf = (float *)t->padded;
+    if (t->leaf == 64) SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 64>, pd) : launch(leaf_norm_seg_kernel<float, 64>, pf));
+    else SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 32>, pd) : launch(leaf_norm_seg_kernel<float, 32>, pf));
+    fused = tail.ticket != nullptr;
+  } else if (t->dtype == SPAMM_DTYPE_F64)
     SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap, ticket, ov, &fused));
   else
     SPAMM_TRY(launch_leaf_norms<float>(t, st, list, list_count, list_cap, ticket, ov, &fused));

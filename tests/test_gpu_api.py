@@ -413,3 +413,79 @@ def test_from_dense_async_matches_sync():
     b = sp.from_dense(y, leaf_size=8, dtype=np.float32)
     assert a.norm() == b.norm()
     assert np.array_equal(a._padded, b._padded)
+
+
+def _crafted_blocks(n, leaf, rng):
+    """A matrix whose leaves stress the segmented norm chains: rounding ties
+    (s exactly half an ulp of the running sum), binade crossings inside and
+    across segments, subnormal and overflowing squares, NaN, zero leaves."""
+    x = np.zeros((n, n))
+    nb = n // leaf
+    kinds = ["ties", "ties3", "range", "subnormal", "overflow", "nan", "zero", "ramp", "random"]
+    for q in range(nb * nb):
+        i, j = divmod(q, nb)
+        kind = kinds[q % len(kinds)]
+        blk = x[i * leaf:(i + 1) * leaf, j * leaf:(j + 1) * leaf]
+        if kind == "ties":       # acc in [2, 4): u = 2^-51, s = 2^-52 is a tie
+            blk[...] = 2.0 ** -26
+            blk[0, 0] = 1.5
+        elif kind == "ties3":    # s = 9 * 2^-52 = 4.5 u: ties again
+            blk[...] = 3 * 2.0 ** -26
+            blk[0, 0] = 1.5
+            blk[leaf // 2, 3] = 1.0
+        elif kind == "range":
+            blk[...] = rng.uniform(-1, 1, blk.shape) * 10.0 ** rng.integers(-150, 150, blk.shape)
+        elif kind == "subnormal":
+            blk[...] = rng.uniform(-1, 1, blk.shape) * 1e-160
+        elif kind == "overflow":
+            blk[...] = rng.uniform(-1, 1, blk.shape)
+            blk[leaf - 1, leaf // 3] = 1e200
+        elif kind == "nan":
+            blk[...] = rng.uniform(-1, 1, blk.shape)
+            blk[leaf // 2, leaf // 2] = np.nan
+        elif kind == "ramp":     # growing along the chain: many binade crossings
+            blk[...] = np.arange(1, leaf * leaf + 1).reshape(leaf, leaf) ** 3.0
+        elif kind == "random":
+            blk[...] = rng.uniform(-1, 1, blk.shape)
+    return x
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("leaf", [16, 32, 64])
+def test_product_norms_segmented_chain_edge_cases(leaf):
+    """C = A * I (tau = 0) carries A's crafted leaves into a product (NaN and
+    overflow spread along their block rows); C's norm pyramid, built by the
+    segmented-chain kernel, must equal the oracle's sequential chains bit for
+    bit on every leaf."""
+    rng = np.random.default_rng(21)
+    n = leaf * 6
+    x = _crafted_blocks(n, leaf, rng)
+    a = sp.from_dense(x, leaf_size=leaf)
+    eye = sp.from_dense(np.eye(n), leaf_size=leaf)
+    c, _ = sp.spamm(a, eye, sp.SpammConfig(tau=0.0))
+    cp = c._padded.copy()
+    assert np.isnan(cp).any() and np.array_equal(cp[:leaf, :leaf], a._padded[:leaf, :leaf])
+    nsq, occ = oracle.build_pyramid(cp, leaf)
+    got = np.concatenate([lv.reshape(-1) for lv in c._norm_sq])
+    goto = np.concatenate([lv.reshape(-1) for lv in c._occupied])
+    assert np.array_equal(got.view(np.uint64), nsq.view(np.uint64))
+    assert np.array_equal(goto, occ.astype(bool))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("leaf", [16, 32, 64])
+def test_product_f32_matches_oracle(leaf):
+    rng = np.random.default_rng(3)
+    n = leaf * 8 - 5
+    d = np.abs(np.subtract.outer(np.arange(n), np.arange(n)))
+    ad = (rng.uniform(-1, 1, (n, n)) * 0.8 ** d).astype(np.float32)
+    bd = (rng.uniform(-1, 1, (n, n)) * 0.8 ** d).astype(np.float32)
+    a = sp.from_dense(ad, leaf_size=leaf, dtype=np.float32)
+    b = sp.from_dense(bd, leaf_size=leaf, dtype=np.float32)
+    c, st = sp.spamm(a, b, sp.SpammConfig(tau=1e-4))
+    ref = oracle.spamm(ad, bd, leaf, 1e-4, dtype=np.float32)
+    assert st.leaf_matmuls == ref["stats"]["leaf_matmuls"]
+    assert np.array_equal(c._padded.view(np.uint32), ref["c_padded"].view(np.uint32))
+    nsq, _ = oracle.build_pyramid(ref["c_padded"].copy(), leaf)
+    got = np.concatenate([lv.reshape(-1) for lv in c._norm_sq])
+    assert np.array_equal(got.view(np.uint64), nsq.view(np.uint64))
