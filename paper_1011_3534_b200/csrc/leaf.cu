@@ -214,9 +214,9 @@ constexpr int STG_MERGE = 1, STG_END = 2, STG_DONE = 4;
 //               waits "full", runs its DMMAs, releases the stage ("empty"),
 //               then merges / stores as StageInfo says.  No block-wide
 //               barrier in the loop.
-template <int TILE>
+template <int TILE, int CW_ = 16, int WM_ = 4>
 struct WsCfg {
-  static constexpr int CWARPS = 16, WM = 4, WN = 4;
+  static constexpr int CWARPS = CW_, WM = WM_, WN = CW_ / WM_;
   static constexpr int THREADS = 32 * (1 + CWARPS);
   static constexpr int WTM = TILE / WM, WTN = TILE / WN;  // warp tile
   static constexpr int MT8 = WTM / 8, NT8 = WTN / 8;      // m8 / n8 tiles per warp
@@ -270,14 +270,46 @@ __device__ __forceinline__ void tmem_load<4>(uint32_t taddr, uint32_t (&r)[4]) {
                : "memory");
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
+template <>
+__device__ __forceinline__ void tmem_store<32>(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      R4(0), R4(4), R4(8), R4(12), R4(16), R4(20), R4(24), R4(28)
+      : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_load<32>(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : W4(0), W4(4), W4(8), W4(12), W4(16), W4(20), W4(24), W4(28)
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_store<64>(uint32_t taddr, const uint32_t (&r)[64]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63,%64};\n" ::"r"(taddr),
+      R4(0), R4(4), R4(8), R4(12), R4(16), R4(20), R4(24), R4(28), R4(32), R4(36), R4(40), R4(44), R4(48), R4(52), R4(56), R4(60)
+      : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_load<64>(uint32_t taddr, uint32_t (&r)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n"
+      : W4(0), W4(4), W4(8), W4(12), W4(16), W4(20), W4(24), W4(28), W4(32), W4(36), W4(40), W4(44), W4(48), W4(52), W4(56), W4(60)
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
 #undef R4
 #undef W4
 
-template <int TILE>
-__global__ void __launch_bounds__(WsCfg<TILE>::THREADS, 1)
+template <int TILE, int CW = 16, int WMv = 4>
+__global__ void __launch_bounds__(WsCfg<TILE, CW, WMv>::THREADS, 1)
     leaf_dmma_ws_kernel(LeafArgs args, const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB) {
-  using C = WsCfg<TILE>;
+  using C = WsCfg<TILE, CW, WMv>;
   extern __shared__ __align__(1024) unsigned char dsm_raw[];
   // TMA 128-byte swizzle needs 1024-byte aligned tiles
   double *dsm = reinterpret_cast<double *>(
@@ -590,15 +622,15 @@ static bool make_b_map5(CUtensorMap *map, const void *base, int64_t N) {
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int TILE>
+template <int TILE, int CW = 16, int WMv = 4>
 static int launch_dmma_ws(LeafArgs args, int num_sms, cudaStream_t st) {
-  using C = WsCfg<TILE>;
+  using C = WsCfg<TILE, CW, WMv>;
   CUtensorMap ma, mb;
   SPAMM_TRY(make_operand_map(&ma, args.a, args.N, 2, TILE));             // A: 32 k x TILE rows
   args.b_map5 = TILE == 64 && make_b_map5(&mb, args.b, args.N);
   if (!args.b_map5)
     SPAMM_TRY(make_operand_map(&mb, args.b, args.N, TILE / 16, DMMA_BK));  // B: TILE n x 32 k
-  auto kern = leaf_dmma_ws_kernel<TILE>;
+  auto kern = leaf_dmma_ws_kernel<TILE, CW, WMv>;
   SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(C::SMEM + 1024)));
   SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -674,11 +706,27 @@ __global__ void __launch_bounds__(SIMT_THREADS) leaf_simt_kernel(LeafArgs args) 
   }
 }
 
+// consumer-warp layout of the FP64 kernel at leaf >= 64 (SPAMM_K3_WARPS):
+// 16 = 4 x 4 warp tiles of 16 x 16 (default), 8 = 2 x 4 of 32 x 16,
+// 9 = 4 x 2 of 16 x 32, 4 = 2 x 2 of 32 x 32
+int k3_warps() {
+  static const int w = getenv("SPAMM_K3_WARPS") ? atoi(getenv("SPAMM_K3_WARPS")) : 16;
+  return w;
+}
+unsigned leaf_signals_per_tile(int leaf) {
+  if (leaf < 64) return 16;
+  const int w = k3_warps();
+  return w == 8 || w == 9 ? 8 : w == 4 ? 4 : 16;
+}
+
 int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches,
                 bool *signals) {
   if (signals) *signals = false;
   if (dtype == SPAMM_DTYPE_F64 && args.leaf >= 32) {
     if (args.leaf == 32) SPAMM_TRY((launch_dmma_ws<32>(args, num_sms, st)));
+    else if (k3_warps() == 8) SPAMM_TRY((launch_dmma_ws<64, 8, 2>(args, num_sms, st)));
+    else if (k3_warps() == 9) SPAMM_TRY((launch_dmma_ws<64, 8, 4>(args, num_sms, st)));
+    else if (k3_warps() == 4) SPAMM_TRY((launch_dmma_ws<64, 4, 2>(args, num_sms, st)));
     else SPAMM_TRY((launch_dmma_ws<64>(args, num_sms, st)));
     if (signals) *signals = args.grp_done != nullptr;
   } else {

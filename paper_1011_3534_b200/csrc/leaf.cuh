@@ -26,6 +26,7 @@ struct LeafArgs {
 // in args.grp_done (CWARPS per (sub-)tile) and lets dependents launch early.
 int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches,
                 bool *signals = nullptr);
-constexpr unsigned LEAF_SIGNALS_PER_TILE = 16;  // consumer warps of the warp-specialised kernel
+// consumer warps of the warp-specialised kernel per (sub-)tile at this leaf size
+unsigned leaf_signals_per_tile(int leaf);
 
 }  // namespace spamm

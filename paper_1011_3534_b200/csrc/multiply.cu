@@ -269,7 +269,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       const unsigned subs = (unsigned)((a->leaf / tile) * (a->leaf / tile));
       if ((rc = build_pyramid_async(ctx, c, st, &launches, ta.group_ids, &dtc->num_groups,
                                     (int64_t)gcap, overlapped ? la.grp_done : nullptr,
-                                    LEAF_SIGNALS_PER_TILE * subs, &dtc->overflow, &dtc->k1_t1)))
+                                    leaf_signals_per_tile(a->leaf) * subs, &dtc->overflow, &dtc->k1_t1)))
         break;
     }
     ctx->last_overlapped = overlapped;
