@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv>::THREADS, 1)
     atomicMax(&args.tc->k3_t0n, ~t_start);
   }
 
-  unsigned items = 0;
+  unsigned items = 0, stages_total = 0;
   if (warp == 0) {
     // ============================================================ producer
     if (lane == 0) {
@@ -411,6 +411,7 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv>::THREADS, 1)
           k = knext;
         }
       }
+      stages_total = (unsigned)gstep;
       // termination marker
       acquire();
       info[stage].flags = STG_DONE;
@@ -571,7 +572,7 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv>::THREADS, 1)
   if (args.timeline && tid == 0) {
     args.timeline[3 * blockIdx.x] = t_start;
     args.timeline[3 * blockIdx.x + 1] = gtimer();
-    args.timeline[3 * blockIdx.x + 2] = items;
+    args.timeline[3 * blockIdx.x + 2] = items | ((unsigned long long)stages_total << 16);
   }
 }
 

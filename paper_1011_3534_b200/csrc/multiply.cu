@@ -333,9 +333,15 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       if (tl[3 * q]) {
         ends.push_back((tl[3 * q + 1] - t0) * 1e-3);
         busy += (tl[3 * q + 1] - tl[3 * q]) * 1e-3;
-        items += (int)tl[3 * q + 2];
+        items += (int)(tl[3 * q + 2] & 0xffff);
         ++n;
       }
+    if (getenv("SPAMM_GEMM_TIMELINE_RAW"))
+      for (int q = 0; q < 4096; ++q)
+        if (tl[3 * q])
+          fprintf(stderr, "[gemm cta] %d start=%.1f end=%.1f items=%llu stages=%llu\n", q,
+                  (tl[3 * q] - t0) * 1e-3, (tl[3 * q + 1] - t0) * 1e-3, tl[3 * q + 2] & 0xffff,
+                  tl[3 * q + 2] >> 16);
     std::sort(ends.begin(), ends.end());
     if (n)
       fprintf(stderr, "[gemm timeline] ctas=%d items=%d span=%.1fus end min/med/p90/max=%.1f/%.1f/%.1f/%.1f busy_avg=%.1fus\n",

@@ -17,4 +17,7 @@ for it in range(3):
             print(f"tau={tau:g} retained={st.leaf_matmuls} groups={det.n_groups} gemm={det.ms_gemm*1e3:.1f}us "
                   f"ctree={det.ms_ctree*1e3:.1f}us cull={det.ms_cull*1e3:.1f}us total={det.ms_total*1e3:.1f}us",
                   file=sys.stderr, flush=True)
+            ph = det.traverse_phase_us
+            print("   traverse phases (us from class. end; [0]=launch->class.): " +
+                  " ".join(f"{i}:{v:.1f}" for i, v in enumerate(ph) if v), file=sys.stderr, flush=True)
         del c
