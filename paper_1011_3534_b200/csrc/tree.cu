@@ -1129,7 +1129,11 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
   const K1Overlap *ov = (grp_done || t_end) ? &ovs : nullptr;
   // list mode (C's tree): the segmented-chain kernel, a warp per leaf
   static const bool no_seg = getenv("SPAMM_NO_SEG_CHAIN") != nullptr;
-  if (list && !no_seg && (t->leaf == 32 || t->leaf == 64)) {
+  // (only where K1 overlaps K3's tail -- small block grids: per leaf the
+  // segmented kernel is latency-short, but for 10^4-10^6 C blocks the staged
+  // kernel's 32-leaf CTAs stream them faster: c3 C tree 0.13 vs 0.35 ms, c5
+  // 0.30 vs 0.81 ms)
+  if (list && !no_seg && grp_done && (t->leaf == 32 || t->leaf == 64)) {
     const bool f64 = t->dtype == SPAMM_DTYPE_F64;
     PyrTail tail{};
     tail.nsq = t->nsq;
