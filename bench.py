@@ -198,6 +198,17 @@ def fp64_peak():
     return peak, "profiles/fp64_peaks.json (DMMA mma.sync f64 microbenchmark, this pool's B200)"
 
 
+def fp32_peak():
+    """FP32 FMA (CUDA-core) roofline for the f32 leaf kernels."""
+    path = os.path.join(ROOT, "profiles", "fp64_peaks.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        if "ffma_tflops" in p:
+            return p["ffma_tflops"], "profiles/fp64_peaks.json (FFMA microbenchmark, this pool's B200)"
+    return 148 * 128 * 2 * 1.965e9 / 1e12, "nominal: 148 SMs x 128 FMA/clk x 2 x 1965 MHz"
+
+
 def k3_traffic():
     path = os.path.join(ROOT, "profiles", "k3_traffic.json")
     if os.path.exists(path):
@@ -294,18 +305,21 @@ def run_b200(args, cfg_name):
               "tflops": leaf_flops(leaf, r) / (m * 1e-3) / 1e12}
              for (t, r, m, g, cu, ct, ng) in per_tau_all[-1]]
 
-    peak, peak_src = fp64_peak()
+    f64_tensor = args.dtype == "f64" and leaf >= 32
+    peak, peak_src = fp64_peak() if f64_tensor else fp32_peak()
     # K3 roofline from this rank's own flops and K3 event time
     local_f = sum(leaf_flops(leaf, x[1]) for step in per_tau_all for x in step)
     local_gemm = sum(x[3] for step in per_tau_all for x in step)
     achieved = local_f / (local_gemm * 1e-3) / 1e12 if local_gemm > 0 else 0.0
     traffic = k3_traffic()
-    kname = ("leaf_dmma_ws_kernel<%d> (K3)" % min(leaf, 64) if args.dtype == "f64" and leaf >= 32
+    kname = ("leaf_dmma_ws_kernel<%d> (K3)" % min(leaf, 64) if f64_tensor
+             else "leaf_sgemm_kernel (K3, FP32 FMA pipe)" if args.dtype == "f32" and leaf >= 64
              else "leaf_simt_kernel (K3, FMA pipe)")
-    roofline = {"bound": "tensor", "kernel": kname, "achieved": achieved,
+    roofline = {"bound": "tensor" if f64_tensor else "fma", "kernel": kname, "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": peak_src,
-                "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                "traffic": (traffic.get("bytes_per_launch") if traffic and cfg_name == "c2"
+                            and f64_tensor else None),
                 "algorithmic": "2*b^3 flop per retained leaf triple / K3 event time"}
 
     line = {

@@ -720,6 +720,113 @@ unsigned leaf_signals_per_tile(int leaf) {
   return w == 8 || w == 9 ? 8 : w == 4 ? 4 : 16;
 }
 
+// ----------------------------------------------------- FP32 tiled path
+// FP32 leaves of 64 (and multiples): np.matmul's order on this data is one
+// sequential FMA chain per output over the inner index from zero -- the same
+// as the SIMT kernel -- but here a CTA of 256 threads owns a 64 x 64 C tile,
+// each thread a 4 x 4 register micro-tile, and the operand tiles are staged in
+// shared memory (A transposed, so a thread's four rows at one inner index are
+// one 16-byte load), double-buffered through registers: 2 shared loads per
+// 16 FMAs instead of 2 global loads per FMA.  Products are merged with the
+// same LCA-keyed stack (per element, in f32).
+constexpr int SG_THREADS = 256;
+constexpr int SG_APAD = 4;                       // floats of padding per transposed A row
+constexpr int SG_A_FLOATS = 64 * (64 + SG_APAD);  // As[q][r]
+constexpr int SG_B_FLOATS = 64 * 64;              // Bs[q][c]
+constexpr size_t SG_SMEM = sizeof(float) * 2 * (SG_A_FLOATS + SG_B_FLOATS);
+
+__global__ void __launch_bounds__(SG_THREADS) leaf_sgemm_kernel(LeafArgs args) {
+  extern __shared__ __align__(16) float sg_smem[];
+  __shared__ int s_work;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int b = args.leaf;
+  const int subs_side = b / 64, kchunks = b / 64;
+  const int64_t N = args.N;
+  const float *__restrict__ A = (const float *)args.a;
+  const float *__restrict__ B = (const float *)args.b;
+  float *__restrict__ Cm = (float *)args.c;
+  float stk[MAXD][16];
+  int ops[MAXD];
+  WorkItem w;
+  while (fetch_work(args, subs_side, &s_work, w)) {
+    const int64_t nk = w.end - w.start;
+    const int64_t steps = nk * kchunks;  // (product, inner chunk) pairs, in order
+    const int64_t arow0 = (int64_t)w.i * b + w.si * 64, bcol0 = (int64_t)w.j * b + w.sj * 64;
+    float4 ra[4], rb[4];
+    auto load = [&](int64_t step) {  // global -> registers
+      const int64_t s = step / kchunks;
+      const int kc = (int)(step - s * kchunks);
+      const int64_t kcol = (int64_t)args.ks[w.start + s] * b + kc * 64;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int f = tid + SG_THREADS * u, r = f >> 4, c4 = (f & 15) * 4;
+        ra[u] = __ldg(reinterpret_cast<const float4 *>(A + (arow0 + r) * N + kcol + c4));
+        rb[u] = __ldg(reinterpret_cast<const float4 *>(B + (kcol + r) * N + bcol0 + c4));
+      }
+    };
+    auto store = [&](int buf) {  // registers -> shared (A transposed)
+      float *As = sg_smem + buf * (SG_A_FLOATS + SG_B_FLOATS), *Bs = As + SG_A_FLOATS;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int f = tid + SG_THREADS * u, r = f >> 4, c4 = (f & 15) * 4;
+        As[(c4 + 0) * (64 + SG_APAD) + r] = ra[u].x;
+        As[(c4 + 1) * (64 + SG_APAD) + r] = ra[u].y;
+        As[(c4 + 2) * (64 + SG_APAD) + r] = ra[u].z;
+        As[(c4 + 3) * (64 + SG_APAD) + r] = ra[u].w;
+        *reinterpret_cast<float4 *>(Bs + r * 64 + c4) = rb[u];
+      }
+    };
+    float acc[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+    int sp = 0;
+    load(0);
+    store(0);
+    __syncthreads();
+    for (int64_t step = 0; step < steps; ++step) {
+      const int cur = (int)(step & 1);
+      if (step + 1 < steps) load(step + 1);
+      const float *As = sg_smem + cur * (SG_A_FLOATS + SG_B_FLOATS), *Bs = As + SG_A_FLOATS;
+#pragma unroll 16
+      for (int q = 0; q < 64; ++q) {
+        const float4 a = *reinterpret_cast<const float4 *>(As + q * (64 + SG_APAD) + ty * 4);
+        const float4 bv = *reinterpret_cast<const float4 *>(Bs + q * 64 + tx * 4);
+        const float av[4] = {a.x, a.y, a.z, a.w}, bw[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(av[i], bw[j], acc[i * 4 + j]);
+      }
+      if (step + 1 < steps) store(cur ^ 1);
+      __syncthreads();
+      const int64_t s = step / kchunks;
+      if (step - s * kchunks == kchunks - 1) {  // product P_k complete: merge in tree order
+        const uint32_t k = args.ks[w.start + s];
+        int h = 99;
+        if (s + 1 < nk) h = merge_level(k, args.ks[w.start + s + 1]);
+        while (sp > 0 && ops[sp - 1] < h) {
+          --sp;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc[e] = stk[sp][e] + acc[e];
+        }
+        if (s + 1 < nk) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            stk[sp][e] = acc[e];
+            acc[e] = 0.f;
+          }
+          ops[sp] = h;
+          ++sp;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      *reinterpret_cast<float4 *>(Cm + (arow0 + ty * 4 + i) * N + bcol0 + tx * 4) =
+          make_float4(acc[i * 4], acc[i * 4 + 1], acc[i * 4 + 2], acc[i * 4 + 3]);
+  }
+}
+
 int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches,
                 bool *signals) {
   if (signals) *signals = false;
@@ -734,8 +841,16 @@ int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, i
     LeafArgs a2 = args;
     a2.grp_done = nullptr;
     a2.order = nullptr;
-    if (dtype == SPAMM_DTYPE_F64) leaf_simt_kernel<double><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
-    else leaf_simt_kernel<float><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
+    static const bool no_sgemm = getenv("SPAMM_NO_SGEMM") != nullptr;
+    if (dtype == SPAMM_DTYPE_F64) {
+      leaf_simt_kernel<double><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
+    } else if (args.leaf >= 64 && !no_sgemm) {
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_sgemm_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SG_SMEM));
+      leaf_sgemm_kernel<<<num_sms * 3, SG_THREADS, SG_SMEM, st>>>(a2);
+    } else {
+      leaf_simt_kernel<float><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
+    }
   }
   SPAMM_CUDA_TRY(cudaGetLastError());
   if (launches) ++*launches;

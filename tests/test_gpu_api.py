@@ -473,7 +473,7 @@ def test_product_norms_segmented_chain_edge_cases(leaf):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("leaf", [16, 32, 64])
+@pytest.mark.parametrize("leaf", [16, 32, 64, 128])
 def test_product_f32_matches_oracle(leaf):
     rng = np.random.default_rng(3)
     n = leaf * 8 - 5

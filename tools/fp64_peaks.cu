@@ -64,6 +64,21 @@ __global__ void dfma_tp(double* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void ffma_tp(float* out, int iters) {
+  float x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = threadIdx.x + i;
+  const float m = 0.999999f, c = 1e-9f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = fmaf(x[i], m, c);
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void dadd_chain(double* out, int iters, long long* cyc) {
   double acc = threadIdx.x, e = 1e-7 * (threadIdx.x + 1);
   long long t0 = clock64();
@@ -106,6 +121,9 @@ int main() {
     float ms = timeit([&] { dfma_tp<<<blocks, threads>>>(out, iters); });
     double flops = 2.0 * 8 * iters * (double)blocks * threads;
     printf(", \"dfma_tflops\": %.3f", flops / ms / 1e9);
+    ms = timeit([&] { ffma_tp<<<blocks, threads>>>((float *)out, iters); });
+    flops = 2.0 * 16 * iters * (double)blocks * threads;
+    printf(", \"ffma_tflops\": %.3f", flops / ms / 1e9);
   }
   {
     dadd_chain<<<1, 32>>>(out, 1024, cyc); CK(cudaDeviceSynchronize());
