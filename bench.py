@@ -248,8 +248,8 @@ def run_b200(args, cfg_name):
             a_host = a_host.astype(np.float32)
             b_host = a_host if b_host is None or b_host is a_host else b_host.astype(np.float32)
         n = a_host.shape[0]
-        a = sp.from_dense(a_host, leaf_size=leaf)
-        b = a if b_host is a_host else sp.from_dense(b_host, leaf_size=leaf)
+        a = sp.from_dense(a_host, leaf_size=leaf, dtype=a_host.dtype)
+        b = a if b_host is a_host else sp.from_dense(b_host, leaf_size=leaf, dtype=b_host.dtype)
     shard = spd.row_shard(rank, world, n, leaf) if use_dist else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -409,8 +409,9 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
     def inputs(it):
         """from_dense of step it's operands, returning before the copy is done:
         host->device copy + pyramid on the library's copy-in stream."""
-        at = sp.from_dense(pin_a[it % 2], leaf_size=leaf, wait=False)
-        bt = at if same else sp.from_dense(pin_b[it % 2], leaf_size=leaf, wait=False)
+        at = sp.from_dense(pin_a[it % 2], leaf_size=leaf, dtype=pin_a[0].dtype, wait=False)
+        bt = at if same else sp.from_dense(pin_b[it % 2], leaf_size=leaf, dtype=pin_b[0].dtype,
+                                           wait=False)
         return at, bt
     # the product comes back as its nonzero leaf blocks (the tree's content;
     # empty blocks are implicit zeros), in one transfer per multiply; with row

@@ -753,27 +753,41 @@ __global__ void __launch_bounds__(SG_THREADS) leaf_sgemm_kernel(LeafArgs args) {
     const int64_t steps = nk * kchunks;  // (product, inner chunk) pairs, in order
     const int64_t arow0 = (int64_t)w.i * b + w.si * 64, bcol0 = (int64_t)w.j * b + w.sj * 64;
     float4 ra[4], rb[4];
+    // A pieces: warp task t = 8u + warp covers rows 8 (t & 7) .. +7 and float4
+    // columns 4 (t >> 3) .. +3; lane l takes row l & 7, column l >> 3 -- whole
+    // 64-byte row segments from global, and transposed stores that hit at most
+    // two lanes per bank (row-major lane order would put eight on one)
+    const int warp = tid >> 5, lane = tid & 31;
+    auto a_rc = [&](int u, int &r, int &c4) {
+      const int t = 8 * u + warp;
+      r = 8 * (t & 7) + (lane & 7);
+      c4 = 4 * (4 * (t >> 3) + (lane >> 3));
+    };
     auto load = [&](int64_t step) {  // global -> registers
       const int64_t s = step / kchunks;
       const int kc = (int)(step - s * kchunks);
       const int64_t kcol = (int64_t)args.ks[w.start + s] * b + kc * 64;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int f = tid + SG_THREADS * u, r = f >> 4, c4 = (f & 15) * 4;
+        int r, c4;
+        a_rc(u, r, c4);
         ra[u] = __ldg(reinterpret_cast<const float4 *>(A + (arow0 + r) * N + kcol + c4));
-        rb[u] = __ldg(reinterpret_cast<const float4 *>(B + (kcol + r) * N + bcol0 + c4));
+        const int f = tid + SG_THREADS * u, rr = f >> 4, cc4 = (f & 15) * 4;
+        rb[u] = __ldg(reinterpret_cast<const float4 *>(B + (kcol + rr) * N + bcol0 + cc4));
       }
     };
     auto store = [&](int buf) {  // registers -> shared (A transposed)
       float *As = sg_smem + buf * (SG_A_FLOATS + SG_B_FLOATS), *Bs = As + SG_A_FLOATS;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int f = tid + SG_THREADS * u, r = f >> 4, c4 = (f & 15) * 4;
+        int r, c4;
+        a_rc(u, r, c4);
         As[(c4 + 0) * (64 + SG_APAD) + r] = ra[u].x;
         As[(c4 + 1) * (64 + SG_APAD) + r] = ra[u].y;
         As[(c4 + 2) * (64 + SG_APAD) + r] = ra[u].z;
         As[(c4 + 3) * (64 + SG_APAD) + r] = ra[u].w;
-        *reinterpret_cast<float4 *>(Bs + r * 64 + c4) = rb[u];
+        const int f = tid + SG_THREADS * u, rr = f >> 4, cc4 = (f & 15) * 4;
+        *reinterpret_cast<float4 *>(Bs + rr * 64 + cc4) = rb[u];
       }
     };
     float acc[16];
