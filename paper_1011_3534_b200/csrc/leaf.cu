@@ -554,10 +554,9 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv>::THREADS, 1)
           top_dirty = false;
           if (args.grp_done) {  // this warp's part of the group is in C
             __syncwarp();
-            if (lane == 0) {
-              __threadfence();
-              atomicAdd(&args.grp_done[si.grp], 1u);
-            }
+            if (lane == 0)  // release reduction: no full fence stalling the warp
+              asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(&args.grp_done[si.grp])
+                           : "memory");
           }
         }
       }
