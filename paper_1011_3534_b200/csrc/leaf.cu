@@ -728,70 +728,71 @@ unsigned leaf_signals_per_tile(int leaf) {
 // one 16-byte load), double-buffered through registers: 2 shared loads per
 // 16 FMAs instead of 2 global loads per FMA.  Products are merged with the
 // same LCA-keyed stack (per element, in f32).
-constexpr int SG_THREADS = 256;
 constexpr int SG_APAD = 4;                       // floats of padding per transposed A row
 constexpr int SG_A_FLOATS = 64 * (64 + SG_APAD);  // As[q][r]
 constexpr int SG_B_FLOATS = 64 * 64;              // Bs[q][c]
 constexpr size_t SG_SMEM = sizeof(float) * 2 * (SG_A_FLOATS + SG_B_FLOATS);
 
-__global__ void __launch_bounds__(SG_THREADS) leaf_sgemm_kernel(LeafArgs args) {
+// TM x TN outputs per thread (64 / TN threads across, 64 / TM down).
+template <int TM, int TN>
+__global__ void __launch_bounds__(4096 / (TM * TN)) leaf_sgemm_kernel(LeafArgs args) {
+  constexpr int THREADS = 4096 / (TM * TN), NX = 64 / TN;
+  constexpr int PER = 1024 / THREADS;  // float4 pieces per thread per operand tile
   extern __shared__ __align__(16) float sg_smem[];
   __shared__ int s_work;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, tx = tid % NX, ty = tid / NX;
   const int b = args.leaf;
   const int subs_side = b / 64, kchunks = b / 64;
   const int64_t N = args.N;
   const float *__restrict__ A = (const float *)args.a;
   const float *__restrict__ B = (const float *)args.b;
   float *__restrict__ Cm = (float *)args.c;
-  float stk[MAXD][16];
+  float stk[MAXD][TM * TN];
   int ops[MAXD];
   WorkItem w;
   while (fetch_work(args, subs_side, &s_work, w)) {
     const int64_t nk = w.end - w.start;
     const int64_t steps = nk * kchunks;  // (product, inner chunk) pairs, in order
     const int64_t arow0 = (int64_t)w.i * b + w.si * 64, bcol0 = (int64_t)w.j * b + w.sj * 64;
-    float4 ra[4], rb[4];
-    // A pieces: warp task t = 8u + warp covers rows 8 (t & 7) .. +7 and float4
-    // columns 4 (t >> 3) .. +3; lane l takes row l & 7, column l >> 3 -- whole
-    // 64-byte row segments from global, and transposed stores that hit at most
-    // two lanes per bank (row-major lane order would put eight on one)
-    const int warp = tid >> 5, lane = tid & 31;
+    float4 ra[PER], rb[PER];
+    // A piece u of this thread: row r, float4 column c4 -- lanes run down 8
+    // rows, then across 4 columns: whole 64-byte row segments from global and
+    // transposed shared stores with at most two lanes per bank
     auto a_rc = [&](int u, int &r, int &c4) {
-      const int t = 8 * u + warp;
-      r = 8 * (t & 7) + (lane & 7);
-      c4 = 4 * (4 * (t >> 3) + (lane >> 3));
+      const int f = tid + THREADS * u, t = f >> 5, l = f & 31;
+      r = 8 * (t & 7) + (l & 7);
+      c4 = 4 * (4 * (t >> 3) + (l >> 3));
     };
     auto load = [&](int64_t step) {  // global -> registers
       const int64_t s = step / kchunks;
       const int kc = (int)(step - s * kchunks);
       const int64_t kcol = (int64_t)args.ks[w.start + s] * b + kc * 64;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < PER; ++u) {
         int r, c4;
         a_rc(u, r, c4);
         ra[u] = __ldg(reinterpret_cast<const float4 *>(A + (arow0 + r) * N + kcol + c4));
-        const int f = tid + SG_THREADS * u, rr = f >> 4, cc4 = (f & 15) * 4;
+        const int f = tid + THREADS * u, rr = f >> 4, cc4 = (f & 15) * 4;
         rb[u] = __ldg(reinterpret_cast<const float4 *>(B + (kcol + rr) * N + bcol0 + cc4));
       }
     };
     auto store = [&](int buf) {  // registers -> shared (A transposed)
       float *As = sg_smem + buf * (SG_A_FLOATS + SG_B_FLOATS), *Bs = As + SG_A_FLOATS;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < PER; ++u) {
         int r, c4;
         a_rc(u, r, c4);
         As[(c4 + 0) * (64 + SG_APAD) + r] = ra[u].x;
         As[(c4 + 1) * (64 + SG_APAD) + r] = ra[u].y;
         As[(c4 + 2) * (64 + SG_APAD) + r] = ra[u].z;
         As[(c4 + 3) * (64 + SG_APAD) + r] = ra[u].w;
-        const int f = tid + SG_THREADS * u, rr = f >> 4, cc4 = (f & 15) * 4;
+        const int f = tid + THREADS * u, rr = f >> 4, cc4 = (f & 15) * 4;
         *reinterpret_cast<float4 *>(Bs + rr * 64 + cc4) = rb[u];
       }
     };
-    float acc[16];
+    float acc[TM * TN];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+    for (int e = 0; e < TM * TN; ++e) acc[e] = 0.f;
     int sp = 0;
     load(0);
     store(0);
@@ -800,15 +801,29 @@ __global__ void __launch_bounds__(SG_THREADS) leaf_sgemm_kernel(LeafArgs args) {
       const int cur = (int)(step & 1);
       if (step + 1 < steps) load(step + 1);
       const float *As = sg_smem + cur * (SG_A_FLOATS + SG_B_FLOATS), *Bs = As + SG_A_FLOATS;
-#pragma unroll 16
+#pragma unroll 8
       for (int q = 0; q < 64; ++q) {
-        const float4 a = *reinterpret_cast<const float4 *>(As + q * (64 + SG_APAD) + ty * 4);
-        const float4 bv = *reinterpret_cast<const float4 *>(Bs + q * 64 + tx * 4);
-        const float av[4] = {a.x, a.y, a.z, a.w}, bw[4] = {bv.x, bv.y, bv.z, bv.w};
+        float av[TM], bw[TN];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < TM; i += 4) {
+          const float4 a = *reinterpret_cast<const float4 *>(As + q * (64 + SG_APAD) + ty * TM + i);
+          av[i] = a.x;
+          av[i + 1] = a.y;
+          av[i + 2] = a.z;
+          av[i + 3] = a.w;
+        }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fmaf(av[i], bw[j], acc[i * 4 + j]);
+        for (int j = 0; j < TN; j += 4) {
+          const float4 bv = *reinterpret_cast<const float4 *>(Bs + q * 64 + tx * TN + j);
+          bw[j] = bv.x;
+          bw[j + 1] = bv.y;
+          bw[j + 2] = bv.z;
+          bw[j + 3] = bv.w;
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i * TN + j] = fmaf(av[i], bw[j], acc[i * TN + j]);
       }
       if (step + 1 < steps) store(cur ^ 1);
       __syncthreads();
@@ -820,11 +835,11 @@ __global__ void __launch_bounds__(SG_THREADS) leaf_sgemm_kernel(LeafArgs args) {
         while (sp > 0 && ops[sp - 1] < h) {
           --sp;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) acc[e] = stk[sp][e] + acc[e];
+          for (int e = 0; e < TM * TN; ++e) acc[e] = stk[sp][e] + acc[e];
         }
         if (s + 1 < nk) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
+          for (int e = 0; e < TM * TN; ++e) {
             stk[sp][e] = acc[e];
             acc[e] = 0.f;
           }
@@ -834,9 +849,12 @@ __global__ void __launch_bounds__(SG_THREADS) leaf_sgemm_kernel(LeafArgs args) {
       }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      *reinterpret_cast<float4 *>(Cm + (arow0 + ty * 4 + i) * N + bcol0 + tx * 4) =
-          make_float4(acc[i * 4], acc[i * 4 + 1], acc[i * 4 + 2], acc[i * 4 + 3]);
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; j += 4)
+        *reinterpret_cast<float4 *>(Cm + (arow0 + ty * TM + i) * N + bcol0 + tx * TN + j) =
+            make_float4(acc[i * TN + j], acc[i * TN + j + 1], acc[i * TN + j + 2],
+                        acc[i * TN + j + 3]);
   }
 }
 
@@ -858,9 +876,18 @@ int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, i
     if (dtype == SPAMM_DTYPE_F64) {
       leaf_simt_kernel<double><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
     } else if (args.leaf >= 64 && !no_sgemm) {
-      SPAMM_CUDA_TRY(cudaFuncSetAttribute(leaf_sgemm_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SG_SMEM));
-      leaf_sgemm_kernel<<<num_sms * 3, SG_THREADS, SG_SMEM, st>>>(a2);
+      // micro-tile shape (SPAMM_SGEMM_SHAPE): 84 = 8 x 4 per thread (128 threads,
+      // default), 44 = 4 x 4 (256), 88 = 8 x 8 (64)
+      static const int shape = getenv("SPAMM_SGEMM_SHAPE") ? atoi(getenv("SPAMM_SGEMM_SHAPE")) : 84;
+      auto go = [&](auto kern, int threads) -> int {
+        SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SG_SMEM));
+        kern<<<num_sms * 3, threads, SG_SMEM, st>>>(a2);
+        return SPAMM_OK;
+      };
+      if (shape == 44) SPAMM_TRY(go(leaf_sgemm_kernel<4, 4>, 256));
+      else if (shape == 88) SPAMM_TRY(go(leaf_sgemm_kernel<8, 8>, 64));
+      else SPAMM_TRY(go(leaf_sgemm_kernel<8, 4>, 128));
     } else {
       leaf_simt_kernel<float><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
     }
