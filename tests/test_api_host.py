@@ -81,6 +81,8 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("a GPU is present")
     with pytest.raises((RuntimeError, ValueError)):
         sp.from_dense(np.eye(8), leaf_size=4)
+    with pytest.raises((RuntimeError, ValueError)):
+        sp.from_dense(np.eye(8), leaf_size=4, wait=False)  # the asynchronous build too
 
 
 def test_public_surface_matches_reference_names():
@@ -92,3 +94,23 @@ def test_public_surface_matches_reference_names():
         assert hasattr(sp, name), name
     assert sp.EMPTY.kind == "empty" and sp.EMPTY.norm_sq == 0.0
     assert math.isclose(sp.LeafNode(None, 4.0).norm_sq, 4.0)
+
+
+def test_async_build_validates_like_from_dense():
+    """from_dense(wait=False) validates on the host exactly like the
+    synchronous call (reference exception types, before any device work)."""
+    with pytest.raises(ValueError):
+        sp.from_dense(np.eye(8), leaf_size=3, wait=False)
+    with pytest.raises(sp.DimensionMismatchError):
+        sp.from_dense(np.ones((4, 5)), leaf_size=4, wait=False)
+    with pytest.raises(ValueError):
+        sp.from_dense(np.eye(8), leaf_size=4, dtype=np.int32, wait=False)
+
+
+def test_pending_blocks_wait_is_idempotent_without_a_handle():
+    """PendingBlocks.wait() returns its (ids, blocks) and is a no-op once done."""
+    from paper_1011_3534_b200.quadtree import PendingBlocks
+    ids = np.arange(3)
+    blocks = np.zeros((3, 2, 2))
+    p = PendingBlocks(None, ids, blocks)
+    assert p.wait()[0] is ids and p.wait()[1] is blocks
