@@ -252,14 +252,31 @@ def run_b200(args, cfg_name):
         b = a if b_host is a_host else sp.from_dense(b_host, leaf_size=leaf, dtype=b_host.dtype)
     shard = spd.row_shard(rank, world, n, leaf) if use_dist else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    nbk = spd.padded_blocks(n, leaf)
+    # the step's multiplies (one per tau) as pieces: at N = 1 every tau whole;
+    # at N > 1 the sweep is partitioned over the ranks -- a tau whole or split
+    # into C block-row shards, balanced by retained triples per row (measured
+    # by one planning multiply per tau; every rank computes the same plan, no
+    # collective in the data path)
+    pieces = [(q, None) for q in range(len(taus))]
+    plan_desc = None
+    if use_dist:
+        row_counts = []
+        for tau in taus:
+            _, _, det = sp.spamm_detailed(a, b, sp.SpammConfig(tau=tau), keep_triples=True)
+            row_counts.append(np.bincount(det.triples[:, 0], minlength=nbk)[:nbk])
+        plan, _ = spd.sweep_plan(world, n, leaf, row_counts)
+        pieces = [(q, None if rows == (0, nbk) else rows) for q, rows in plan[rank]]
+        plan_desc = [[(float(taus[q]), list(rows)) for q, rows in p] for p in plan]
 
     def one_step(collect=None):
         f, ms, gemm, launches = 0.0, 0.0, 0.0, 0
         per_tau = []
-        for tau in taus:
+        for q, rows in pieces:
+            tau = taus[q]
             flush.zero_()
             torch.cuda.synchronize()
-            c, st, det = sp.spamm_detailed(a, b, sp.SpammConfig(tau=tau), rows=shard)
+            c, st, det = sp.spamm_detailed(a, b, sp.SpammConfig(tau=tau), rows=rows)
             f += leaf_flops(leaf, st.leaf_matmuls)
             ms += det.ms_total
             gemm += det.ms_gemm
@@ -331,8 +348,10 @@ def run_b200(args, cfg_name):
         "config": {"workload": f"{cfg_name}: n={n} leaf={leaf} {WORKLOAD_DESC.get(cfg_name, '')}, "
                                f"tau sweep {list(taus)}, one spamm per tau per step",
                    "l2": "flushed (256 MiB write) before every multiply",
-                   "parallelism": (f"C block-row shards x{world} (no data-path collective)"
+                   "parallelism": (f"tau sweep partitioned over {world} ranks: each tau whole or "
+                                   f"split into C block-row shards (no data-path collective)"
                                    if use_dist else "single GPU"),
+                   "plan": plan_desc,
                    "per_tau": table},
         "roofline": roofline,
         "clocks": clocks,
@@ -367,6 +386,8 @@ def run_b200(args, cfg_name):
         if dev_cfg:
             line["e2e"] = {"unavailable": "inputs generated on the GPU: host staging of a "
                                           f"{n}x{n} operand is {n * n * 8 / 1e9:.0f} GB"}
+        elif use_dist:
+            line["e2e"] = e2e_leg_dist(args, sp, spd, a_host, leaf, taus, pieces, b_host)
         else:
             line["e2e"] = e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host)
 
@@ -480,6 +501,96 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
             "pipelining": "from_dense(wait=False): step s+1's host->device copy of A runs on the "
                           "copy-in stream during step s's multiplies (PCIe full duplex with the "
                           "read-backs); no copy crosses the timed region's boundaries",
+            "timing": "host wall clock around synchronous public-API calls (max over ranks)"}
+
+
+def e2e_leg_dist(args, sp, spd, a_host, leaf, taus, pieces, b_host=None):
+    """e2e at N > 1 ranks: the operands cross PCIe once in total -- each rank
+    copies its band of padded rows from pinned host memory, the bands are
+    all-gathered over NVLink (NCCL) into every rank's tree storage (the
+    pyramid is then built locally) -- and each rank runs its pieces of the
+    sweep and reads back only their products (a piece's product holds only
+    its rows), the copies overlapping the next piece.  Wall time: max over
+    ranks."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    n = a_host.shape[0]
+    N = spd.padded_blocks(n, leaf) * leaf
+    tdt = torch.float32 if a_host.dtype == np.float32 else torch.float64
+    same = b_host is None or b_host is a_host
+    R0, R1 = rank * N // world, (rank + 1) * N // world  # padded rows of this rank
+    assert N % world == 0, "equal bands for the all-gather"
+    h = R1 - R0
+    hosts = [a_host] if same else [a_host, b_host]
+    pins = []
+    for x in hosts:  # this rank's band, zero-padded to N columns, in pinned memory
+        p = torch.zeros((h, N), dtype=tdt, pin_memory=True)
+        r1 = min(R1, n)
+        if r1 > R0:
+            p[:r1 - R0, :n] = torch.from_numpy(np.ascontiguousarray(x[R0:r1]))
+        pins.append(p)
+    bands = [torch.empty((h, N), dtype=tdt, device="cuda") for _ in pins]
+    fulls = [torch.empty((N, N), dtype=tdt, device="cuda") for _ in pins]
+    nbk = N // leaf
+    pin_blk = [torch.empty((nbk * nbk, leaf, leaf), dtype=tdt, pin_memory=True).numpy()
+               for _ in pieces]
+    pending = [None] * len(pieces)
+    h2d = sum(p.numel() * p.element_size() for p in pins)
+
+    def operands():
+        trees = []
+        for p, band, full in zip(pins, bands, fulls):
+            band.copy_(p, non_blocking=True)                  # PCIe: 1/world of the rows
+            dist.all_gather_into_tensor(full, band)           # NVLink
+            trees.append(spd.tree_from_padded(full, n, leaf))  # pyramid on every rank
+        return trees[0], trees[-1]
+
+    t0 = None
+    e_f = 0.0
+    d2h = 0
+    for it in range(args.warmup + args.steps):
+        if it == args.warmup:
+            for q in pending:
+                if q is not None:
+                    q.wait()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            d2h = 0
+        at, bt = operands()
+        f = 0.0
+        for j, (q, rows) in enumerate(pieces):
+            c, st, _ = sp.spamm_detailed(at, bt, sp.SpammConfig(tau=taus[q]), rows=rows)
+            if pending[j] is not None:
+                pending[j].wait()
+            pending[j] = c.nonzero_blocks(out=pin_blk[j], wait=False)
+            d2h += (pending[j].blocks.nbytes + pending[j].ids.nbytes + c._pyramid()[2].nbytes
+                    + c._pyramid()[3].nbytes)
+            f += leaf_flops(leaf, st.leaf_matmuls)
+            del c
+        del at, bt
+        if it >= args.warmup:
+            e_f += f
+    for q in pending:
+        if q is not None:
+            q.wait()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    d2h = d2h // max(args.steps, 1)
+    t = torch.tensor([el, e_f, float(d2h), float(h2d)], dtype=torch.float64, device="cuda")
+    mx = t[:1].clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t[1:])
+    el, e_f, d2h, h2d = float(mx.item()), float(t[1].item()), int(t[2].item()), int(t[3].item())
+    return {"value": e_f / el / 1e12, "unit": "TFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": el / args.steps * 1e3,
+            "result": "each rank's products read back as their nonzero leaf blocks + norm "
+                      "pyramid (copy-out stream overlapping the next piece)",
+            "operands": "each rank copies 1/N of the padded rows host->device; NCCL all-gather "
+                        "over NVLink assembles the operand on every rank",
             "timing": "host wall clock around synchronous public-API calls (max over ranks)"}
 
 

@@ -54,6 +54,61 @@ def row_shard(rank, world, n, leaf, weights=None):
     return (cuts[rank], cuts[rank + 1])
 
 
+def sweep_plan(world, n, leaf, row_counts, fixed_cost=2800.0, max_split=None):
+    """Partition a set of independent multiplies (e.g. a tau sweep on the same
+    operands) over `world` ranks: each multiply may be split into contiguous C
+    block-row shards, and the pieces are assigned to ranks (longest first).
+
+    `row_counts[m]` are multiply m's retained triples per C block row (its
+    work); a piece costs `fixed_cost` (the per-call traversal / C-tree
+    overhead, in triple units: ~60 us / ~0.021 us per 64^3 triple on a B200)
+    plus its rows' triples.  Shard counts are grown greedily on the multiply
+    whose pieces are the most expensive while that lowers the makespan.
+    Deterministic: every rank computes the same plan.
+
+    Returns (plan, makespan): plan[r] = [(m, (row_lo, row_hi)), ...]."""
+    nb = padded_blocks(n, leaf)
+    counts = [np.asarray(c, dtype=np.float64) for c in row_counts]
+    assert all(c.shape == (nb,) for c in counts)
+    M = len(counts)
+    max_split = max_split or world
+
+    def build(splits):
+        pieces = []
+        for m in range(M):
+            for r in range(splits[m]):
+                lo, hi = row_shard(r, splits[m], n, leaf, counts[m] + 1e-9)
+                if hi > lo:
+                    pieces.append((fixed_cost + counts[m][lo:hi].sum(), m, (lo, hi)))
+        pieces.sort(key=lambda x: (-x[0], x[1], x[2]))
+        load = [0.0] * world
+        plan = [[] for _ in range(world)]
+        for cost, m, rows in pieces:
+            r = min(range(world), key=lambda q: (load[q], q))
+            load[r] += cost
+            plan[r].append((m, rows))
+        for p in plan:
+            p.sort()
+        return plan, max(load)
+
+    splits = [1] * M
+    best_plan, best = build(splits)
+    while True:
+        cand = [m for m in range(M) if splits[m] < max_split]
+        if not cand:
+            break
+        # split the multiply whose pieces are the most expensive
+        m = max(cand, key=lambda q: (counts[q].sum() / splits[q], -q))
+        splits = list(splits)
+        splits[m] += 1
+        plan, span = build(splits)
+        if span < best - 1e-9:
+            best_plan, best = plan, span
+        elif sum(splits) > world:  # more pieces than ranks and no gain: done
+            break
+    return best_plan, best
+
+
 _INT_KEYS = ("leaf_matmuls", "pruned_calls", "pruned_volume", "empty_skip_volume")
 
 

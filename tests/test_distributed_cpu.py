@@ -79,3 +79,29 @@ def test_row_shard_partition():
             spans = [spd.row_shard(r, world, n, leaf) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == nb
             assert all(x[1] == y[0] for x, y in zip(spans, spans[1:]))
+
+
+def test_sweep_plan_partitions_every_row_of_every_multiply_once():
+    """distributed.sweep_plan: every (multiply, C block row) lands on exactly
+    one rank, the plan is deterministic, and the makespan never grows with
+    more ranks."""
+    import numpy as np
+    from paper_1011_3534_b200 import distributed as spd
+
+    rng = np.random.default_rng(0)
+    n, leaf = 4096, 64
+    nb = spd.padded_blocks(n, leaf)
+    counts = [rng.integers(0, 400, nb).astype(float) for _ in range(4)]
+    prev = None
+    for world in (1, 2, 3, 4, 8, 16):
+        plan, span = spd.sweep_plan(world, n, leaf, counts)
+        assert len(plan) == world
+        cover = [np.zeros(nb, int) for _ in counts]
+        for pieces in plan:
+            for m, (lo, hi) in pieces:
+                cover[m][lo:hi] += 1
+        assert all((c == 1).all() for c in cover)
+        assert spd.sweep_plan(world, n, leaf, counts) == (plan, span)
+        if prev is not None:
+            assert span <= prev + 1e-6
+        prev = span
