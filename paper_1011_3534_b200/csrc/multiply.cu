@@ -198,6 +198,11 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     }
     // device timing starts at the first kernel (host-side setup excluded)
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[0], st));
+    if (dense) {
+      ta.c_nsq_leaf = c->nsq + level_offset(depth);
+      ta.c_nrm_leaf = c->nrm + level_offset(depth);
+      ta.c_occ_leaf = c->occ + level_offset(depth);
+    }
     if ((rc = dense ? launch_traverse_dense(ta, ctx->num_sms, st)
                     : launch_traverse(ta, ctx->num_sms, st)))
       break;
@@ -214,13 +219,17 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     // zeroed on the side stream under the traversal (only blocks that receive
     // products are recomputed below).
     c->lazy_empty = true;
-    SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));  // (fork: before the traversal)
-    if ((rc = zero_async(c->nsq + level_offset(depth), sizeof(double) * G, ctx->side, 64))) break;
-    if ((rc = zero_async(c->occ + level_offset(depth), G, ctx->side, 64))) break;
-    if ((rc = zero_async(c->nrm + level_offset(depth), sizeof(double) * G, ctx->side, 64))) break;
-    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));
-    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
-    SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));
+    if (dense) {  // (zeroed by the traversal kernel itself)
+      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
+    } else {
+      SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));  // (fork: before the traversal)
+      if ((rc = zero_async(c->nsq + level_offset(depth), sizeof(double) * G, ctx->side, 64))) break;
+      if ((rc = zero_async(c->occ + level_offset(depth), G, ctx->side, 64))) break;
+      if ((rc = zero_async(c->nrm + level_offset(depth), sizeof(double) * G, ctx->side, 64))) break;
+      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->join, ctx->side));
+      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
+      SPAMM_CUDA_BREAK(cudaStreamWaitEvent(st, ctx->join, 0));
+    }
 
     // ------------------------------------------------ K3 leaf products -> C
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[2], st));

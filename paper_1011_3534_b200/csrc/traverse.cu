@@ -844,6 +844,14 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   const unsigned nblocks = gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned long long t_entry = globaltimer();
+  if (a.c_nsq_leaf) {  // the product's leaf-level norms start at zero
+    for (uint64_t e = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x; e < G;
+         e += (uint64_t)nblocks * DN_THREADS) {
+      a.c_nsq_leaf[e] = 0.0;
+      a.c_nrm_leaf[e] = 0.0;
+      a.c_occ_leaf[e] = 0;
+    }
+  }
   uint32_t *ws = a.dn_masks;                     // this call's work set
   uint32_t *pm = ws + LY::PM, *ptc = ws + LY::PTC, *qtc = ws + LY::QTC, *ne = ws + LY::NE,
            *tdn = ws + LY::TDN;

@@ -72,6 +72,10 @@ struct TraverseArgs {
   unsigned long long *timeline;     // optional per-CTA %globaltimer stamps (4 per CTA)
   uint32_t *lpt_order;              // optional: groups by decreasing size (K3's work order)
   double *pw_part;                  // budget: per-tier top-of-recursion partial sums
+  // dense traversal: zero the product's leaf-level norms (nb^2 entries each)
+  // while classifying -- only the C blocks that receive products get norms
+  double *c_nsq_leaf, *c_nrm_leaf;
+  uint8_t *c_occ_leaf;
 };
 
 // Launch the cooperative traversal kernel (one launch per multiply).
