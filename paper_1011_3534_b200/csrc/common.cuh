@@ -109,6 +109,7 @@ struct DeviceContext {
   Scratch dn_status;      // dense traversal: look-back state (zero at rest)
   int counter_parity = 0; // which traversal counter set the next call uses
   bool last_overlapped = false;  // the last product's C tree overlapped K3
+  bool last_k3_pdl = false;      // the last product's K3 followed the traversal programmatically
   Scratch grp_done;       // per-group finished-tile counters (zero at rest)
   Scratch lpt_order;      // groups by decreasing size (K3's work order)
   Scratch pw_part;        // budget: per-tier partial sums of the split recursion

@@ -342,10 +342,7 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv>::THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   // every CTA is resident: a programmatic dependent (C's norm kernel, which
   // waits on args.grp_done) may start now and overlap this kernel
-  if (tid == 0) {
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-    atomicMax(&args.tc->k3_t0n, ~t_start);
-  }
+  if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
   unsigned items = 0, stages_total = 0;
   if (warp == 0) {
@@ -353,6 +350,13 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv>::THREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmA) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmB) : "memory");
+      // launched as a programmatic dependent of the traversal: its outputs
+      // (group lists, counts) are complete and visible after this (a no-op
+      // for a plain launch)
+      asm volatile("griddepcontrol.wait;\n" ::: "memory");
+      // K3's span starts when its inputs are ready (its prologue may have
+      // overlapped the traversal's tail)
+      atomicMax(&args.tc->k3_t0n, ~gtimer());
       unsigned long long m = *args.n_codes;
       if (m > args.capacity) m = args.capacity;
       const int ng = args.tc->overflow ? 0 : (int)args.tc->num_groups;  // overflow: result discarded, re-run
@@ -634,7 +638,19 @@ static int launch_dmma_ws(LeafArgs args, int num_sms, cudaStream_t st) {
   SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(C::SMEM + 1024)));
   SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  kern<<<num_sms, C::THREADS, C::SMEM + 1024, st>>>(args, ma, mb);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(num_sms);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM + 1024;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (args.pdl) {  // CTAs become resident (prologue done) as the traversal's CTAs retire
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  SPAMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args, ma, mb));
   return SPAMM_OK;
 }
 

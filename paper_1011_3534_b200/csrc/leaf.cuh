@@ -20,6 +20,7 @@ struct LeafArgs {
   int b_map5;                         // B streamed as the conflict-free 5-D TMA box
   unsigned *grp_done;                 // optional: per-group count of finished warp tiles
   const uint32_t *order;              // optional: work order over the groups (longest first)
+  int pdl;                            // launch as a programmatic dependent of the previous kernel
 };
 
 // Returns through *signals whether the launched kernel reports finished groups

@@ -219,8 +219,14 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     // zeroed on the side stream under the traversal (only blocks that receive
     // products are recomputed below).
     c->lazy_empty = true;
-    if (dense) {  // (zeroed by the traversal kernel itself)
-      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
+    // dense path: C's leaf-level norms are zeroed by the traversal kernel
+    // itself, and K3 follows it as a programmatic dependent (no event or
+    // stream wait may sit between them; the traversal's time is then the
+    // multiply's remainder after K3 and the C tree)
+    static const bool no_pdl = getenv("SPAMM_NO_K3_PDL") != nullptr;
+    const bool k3_pdl = dense && !no_pdl;
+    if (dense) {
+      if (!k3_pdl) SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[1], st));
     } else {
       SPAMM_CUDA_BREAK(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));  // (fork: before the traversal)
       if ((rc = zero_async(c->nsq + level_offset(depth), sizeof(double) * G, ctx->side, 64))) break;
@@ -232,7 +238,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     }
 
     // ------------------------------------------------ K3 leaf products -> C
-    SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[2], st));
+    if (!k3_pdl) SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[2], st));
     LeafArgs la{};
     la.a = a->padded;
     la.b = b->padded;
@@ -248,6 +254,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     la.group_starts = ta.group_starts;
     la.order = ta.lpt_order;
     la.tc = dtc;
+    la.pdl = k3_pdl;
     static const bool want_timeline = getenv("SPAMM_GEMM_TIMELINE") != nullptr;
     if (want_timeline) {
       if ((rc = ensure_scratch(ctx->reduce_tmp, sizeof(unsigned long long) * 3 * 4096, st))) break;
@@ -282,6 +289,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
         break;
     }
     ctx->last_overlapped = overlapped;
+    ctx->last_k3_pdl = k3_pdl;
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
     {
       const SmallRead r[2] = {{hc, dtc, sizeof(TraverseCounters)},
@@ -389,8 +397,8 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     s.traverse_phase_us[q] = cc.phase_ns[q] ? (float)((double)(cc.phase_ns[q] - cc.phase_ns[0]) * 1e-3) : 0.f;
   // slot 0: kernel entry -> phase 0 (negative offset of the prologue)
   s.traverse_phase_us[0] = cc.phase_ns[15] ? (float)((double)(cc.phase_ns[0] - cc.phase_ns[15]) * 1e-3) : 0.f;
-  cudaEventElapsedTime(&s.ms_cull, ctx->ev[0], ctx->ev[1]);
   cudaEventElapsedTime(&s.ms_total, ctx->ev[0], ctx->ev[4]);
+  if (!ctx->last_k3_pdl) cudaEventElapsedTime(&s.ms_cull, ctx->ev[0], ctx->ev[1]);
   static const bool tail_dbg = getenv("SPAMM_TAIL_DEBUG") != nullptr;
   if (tail_dbg && cc.k3_t1 && cc.k1_t1)
     fprintf(stderr, "[tail] k3 span %.1f us, C tree done %.1f us after K3\n",
@@ -405,11 +413,18 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       s.ms_ctree = (float)((double)(cc.k1_t1 - cc.k3_t1) * 1e-6);
     else
       s.ms_ctree = std::max(0.f, s.ms_total - s.ms_cull - s.ms_gemm);
+  } else if (ctx->last_k3_pdl && cc.k3_t0n && cc.k3_t1) {
+    s.ms_gemm = (float)((double)(cc.k3_t1 - ~cc.k3_t0n) * 1e-6);
+    s.ms_leaf = s.ms_gemm;
+    cudaEventElapsedTime(&s.ms_ctree, ctx->ev[3], ctx->ev[4]);
   } else {
     cudaEventElapsedTime(&s.ms_leaf, ctx->ev[1], ctx->ev[3]);
     cudaEventElapsedTime(&s.ms_gemm, ctx->ev[2], ctx->ev[3]);
     cudaEventElapsedTime(&s.ms_ctree, ctx->ev[3], ctx->ev[4]);
   }
+  // K3 launched programmatically behind the traversal: no event between
+  // them; the traversal's share is the multiply's remainder
+  if (ctx->last_k3_pdl) s.ms_cull = std::max(0.f, s.ms_total - s.ms_gemm - s.ms_ctree);
   (void)cudaGetLastError();  // (timing queries must not leave an error for the next call)
 
   // ------------------------------------------------------- product records

@@ -844,6 +844,9 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   const unsigned nblocks = gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned long long t_entry = globaltimer();
+  // the leaf-product kernel may launch now: its CTAs take SMs as this grid's
+  // CTAs retire and wait (griddepcontrol.wait) for this grid's results
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (a.c_nsq_leaf) {  // the product's leaf-level norms start at zero
     for (uint64_t e = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x; e < G;
          e += (uint64_t)nblocks * DN_THREADS) {
