@@ -214,7 +214,7 @@ constexpr int STG_MERGE = 1, STG_END = 2, STG_DONE = 4;
 //               waits "full", runs its DMMAs, releases the stage ("empty"),
 //               then merges / stores as StageInfo says.  No block-wide
 //               barrier in the loop.
-template <int TILE, int CW_ = 16, int WM_ = 4>
+template <int TILE, int CW_ = 16, int WM_ = 4, int ST_ = 0>
 struct WsCfg {
   static constexpr int CWARPS = CW_, WM = WM_, WN = CW_ / WM_;
   static constexpr int THREADS = 32 * (1 + CWARPS);
@@ -224,7 +224,7 @@ struct WsCfg {
   static constexpr int NREG = 2 * NACC;                   // ... as b32 registers
   static constexpr int A_ELEMS = TILE * DMMA_BK, B_ELEMS = DMMA_BK * TILE;
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-  static constexpr int STAGES = TILE == 64 ? 6 : 10;
+  static constexpr int STAGES = ST_ ? ST_ : TILE == 64 ? 6 : 10;
   static constexpr size_t SMEM = sizeof(double) * STAGES * STAGE_ELEMS;
   static constexpr int SLOT_COLS = NREG * (CWARPS / 4);   // TMEM columns per stack slot
   static constexpr int TM_COLS = 512;
@@ -305,11 +305,11 @@ __device__ __forceinline__ void tmem_load<64>(uint32_t taddr, uint32_t (&r)[64])
 #undef R4
 #undef W4
 
-template <int TILE, int CW = 16, int WMv = 4>
-__global__ void __launch_bounds__(WsCfg<TILE, CW, WMv>::THREADS, 1)
+template <int TILE, int CW = 16, int WMv = 4, int ST = 0>
+__global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
     leaf_dmma_ws_kernel(LeafArgs args, const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB) {
-  using C = WsCfg<TILE, CW, WMv>;
+  using C = WsCfg<TILE, CW, WMv, ST>;
   extern __shared__ __align__(1024) unsigned char dsm_raw[];
   // TMA 128-byte swizzle needs 1024-byte aligned tiles
   double *dsm = reinterpret_cast<double *>(
@@ -626,15 +626,15 @@ static bool make_b_map5(CUtensorMap *map, const void *base, int64_t N) {
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int TILE, int CW = 16, int WMv = 4>
+template <int TILE, int CW = 16, int WMv = 4, int ST = 0>
 static int launch_dmma_ws(LeafArgs args, int num_sms, cudaStream_t st) {
-  using C = WsCfg<TILE, CW, WMv>;
+  using C = WsCfg<TILE, CW, WMv, ST>;
   CUtensorMap ma, mb;
   SPAMM_TRY(make_operand_map(&ma, args.a, args.N, 2, TILE));             // A: 32 k x TILE rows
   args.b_map5 = TILE == 64 && make_b_map5(&mb, args.b, args.N);
   if (!args.b_map5)
     SPAMM_TRY(make_operand_map(&mb, args.b, args.N, TILE / 16, DMMA_BK));  // B: TILE n x 32 k
-  auto kern = leaf_dmma_ws_kernel<TILE, CW, WMv>;
+  auto kern = leaf_dmma_ws_kernel<TILE, CW, WMv, ST>;
   SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(C::SMEM + 1024)));
   SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -882,6 +882,8 @@ int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, i
     else if (k3_warps() == 8) SPAMM_TRY((launch_dmma_ws<64, 8, 2>(args, num_sms, st)));
     else if (k3_warps() == 9) SPAMM_TRY((launch_dmma_ws<64, 8, 4>(args, num_sms, st)));
     else if (k3_warps() == 4) SPAMM_TRY((launch_dmma_ws<64, 4, 2>(args, num_sms, st)));
+    else if (k3_warps() == 5) SPAMM_TRY((launch_dmma_ws<64, 16, 4, 5>(args, num_sms, st)));
+    else if (k3_warps() == 3) SPAMM_TRY((launch_dmma_ws<64, 16, 4, 4>(args, num_sms, st)));
     else SPAMM_TRY((launch_dmma_ws<64>(args, num_sms, st)));
     if (signals) *signals = args.grp_done != nullptr;
   } else {
