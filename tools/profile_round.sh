@@ -2,7 +2,7 @@
 # Round profile on one B200: bench lines, ncu launch list, ncu full capture of
 # the timed step's kernels.  Usage (under gpurun): bash tools/profile_round.sh TAG
 set -u
-TAG=${1:-r01e}
+TAG=${1:-r01f}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/smi.txt 2>&1
