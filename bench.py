@@ -511,6 +511,9 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
         del at, bt
         if it >= args.warmup:
             e_f += f
+        if os.environ.get("SPAMM_E2E_DEBUG"):
+            print(f"[e2e] step {it} t={(time.perf_counter() - (t0 or 0)) * 1e3:.3f} ms",
+                  file=sys.stderr, flush=True)
     for p in pending:
         p.wait()
     torch.cuda.synchronize()

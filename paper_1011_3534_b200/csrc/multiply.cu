@@ -295,6 +295,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       const SmallRead r[2] = {{hc, dtc, sizeof(TraverseCounters)},
                               {&c->root_norm_sq, c->nsq, sizeof(double)}};
       if ((rc = read_small_sync(ctx, st, r, 2))) break;
+      launches += 2;  // (the two store-to-host kernels of the read)
     }
     if (tv_timeline && ta.timeline) {
       std::vector<unsigned long long> tl(4 * 4096);
