@@ -809,6 +809,13 @@ static int launch_staged(spamm_tree *t, cudaStream_t st, const uint32_t *list,
   return SPAMM_OK;
 }
 
+// ring depth of the 32-leaf K1 for large trees (SPAMM_K1_STAGES; 3 by default: four CTAs
+// per SM instead of two -- c5 K1 8.73 -> 8.08 ms, 3.94 -> 4.25 TB/s)
+static int k1_big_stages() {
+  static const int v = getenv("SPAMM_K1_STAGES") ? atoi(getenv("SPAMM_K1_STAGES")) : 3;
+  return v;
+}
+
 template <typename T>
 static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *list,
                              const unsigned *list_count, int64_t list_cap, unsigned *ticket,
@@ -826,6 +833,10 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
     if (ov && ov->grp_done)
       SPAMM_TRY((launch_staged<T, 12, 8>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
+    else if (n_leaves >= (int64_t)64 * sms && k1_big_stages() == 4)
+      SPAMM_TRY((launch_staged<T, 4, 32>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
+    else if (n_leaves >= (int64_t)64 * sms && k1_big_stages() == 3)
+      SPAMM_TRY((launch_staged<T, 3, 32>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
     else if (n_leaves >= (int64_t)64 * sms)
       SPAMM_TRY((launch_staged<T, 6, 32>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
     else
