@@ -420,7 +420,10 @@ class NumaLocal:
             import pynvml
             pynvml.nvmlInit()
             self.saved = os.sched_getaffinity(0)
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            import torch
+            # NVML numbers all GPUs, CUDA only the visible ones: match by UUID
+            uuid = "GPU-" + str(torch.cuda.get_device_properties(self.device).uuid)
+            h = pynvml.nvmlDeviceGetHandleByUUID(uuid.encode())
             pynvml.nvmlDeviceSetCpuAffinity(h)
         except Exception:  # no NVML / no affinity support: leave as is
             self.saved = None
