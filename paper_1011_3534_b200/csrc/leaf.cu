@@ -817,7 +817,7 @@ __global__ void __launch_bounds__(4096 / (TM * TN)) leaf_sgemm_kernel(LeafArgs a
       const int cur = (int)(step & 1);
       if (step + 1 < steps) load(step + 1);
       const float *As = sg_smem + cur * (SG_A_FLOATS + SG_B_FLOATS), *Bs = As + SG_A_FLOATS;
-#pragma unroll 8
+#pragma unroll 16
       for (int q = 0; q < 64; ++q) {
         float av[TM], bw[TN];
 #pragma unroll
