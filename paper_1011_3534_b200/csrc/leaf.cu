@@ -340,9 +340,6 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
-  // every CTA is resident: a programmatic dependent (C's norm kernel, which
-  // waits on args.grp_done) may start now and overlap this kernel
-  if (tid == 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
   unsigned items = 0, stages_total = 0;
   if (warp == 0) {
@@ -354,6 +351,10 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
       // (group lists, counts) are complete and visible after this (a no-op
       // for a plain launch)
       asm volatile("griddepcontrol.wait;\n" ::: "memory");
+      // the traversal is complete: a programmatic dependent (C's norm kernel,
+      // which waits on args.grp_done) may start now and overlap this kernel.
+      // Not earlier: it reads the traversal's group list and count.
+      asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
       // K3's span starts when its inputs are ready (its prologue may have
       // overlapped the traversal's tail)
       atomicMax(&args.tc->k3_t0n, ~gtimer());
