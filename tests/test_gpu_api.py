@@ -489,3 +489,28 @@ def test_product_f32_matches_oracle(leaf):
     nsq, _ = oracle.build_pyramid(ref["c_padded"].copy(), leaf)
     got = np.concatenate([lv.reshape(-1) for lv in c._norm_sq])
     assert np.array_equal(got.view(np.uint64), nsq.view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_chained_launch_path_is_deterministic():
+    """The c2-shaped path chains three kernels programmatically (traversal ->
+    leaf products -> C's norms, each launched before its predecessor ends).
+    Repeated multiplies must give bit-identical products and C pyramids (a
+    dependent reading its predecessor's outputs too early shows up here)."""
+    rng = np.random.default_rng(17)
+    n, leaf = 4096, 64
+    d = np.abs(np.subtract.outer(np.arange(n), np.arange(n)))
+    u = rng.uniform(-1, 1, (n, n)) * 0.95 ** d
+    a = sp.from_dense(0.5 * (u + u.T), leaf_size=leaf)
+    ref = None
+    for _ in range(12):
+        c, st = sp.spamm(a, a, sp.SpammConfig(tau=1e-6))
+        pyr = np.concatenate([lv.reshape(-1) for lv in c._norm_sq]).view(np.uint64)
+        ids, blocks = c.nonzero_blocks()
+        got = (st.leaf_matmuls, pyr.copy(), ids.copy(), blocks.view(np.uint64).copy())
+        if ref is None:
+            ref = got
+            continue
+        assert got[0] == ref[0]
+        assert np.array_equal(got[1], ref[1])
+        assert np.array_equal(got[2], ref[2]) and np.array_equal(got[3], ref[3])
