@@ -1,11 +1,14 @@
 /*
  * leaf_gemm.c -- TEST INFRASTRUCTURE ONLY.  The per-leaf product the
  * reference delegates to np.matmul / OpenBLAS (multiply.py:255).  OpenBLAS's
- * internal FMA/blocking order is not part of the reference (it is a
- * third-party dependency, pinned only as numpy>=1.24, pyproject.toml:10), so
- * C is compared by tolerance (1e-13 relative Frobenius vs the reference's
- * own C in tests/golden), never bit-for-bit.  Compiled with FMA contraction
- * allowed and AVX2 vectorisation, row-axpy (i-t-j) loop order.
+ * internal FMA/blocking order is not part of the reference (a third-party
+ * dependency, pinned only as numpy>=1.24, pyproject.toml:10).  For these leaf
+ * sizes the build container's OpenBLAS 0.3.30 (SkylakeX kernels) accumulates
+ * each output element as one sequential FMA chain over the inner index from
+ * zero; this row-axpy (i-t-j) loop, compiled with FMA contraction, forms the
+ * same chain, so C matches the reference's own C in tests/golden bit for bit
+ * (tests/test_oracle.py).  A different BLAS build could order its FMAs
+ * differently -- the contract bar is 1e-12 relative Frobenius.
  */
 #include <stdint.h>
 #include <string.h>

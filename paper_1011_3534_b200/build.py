@@ -52,7 +52,7 @@ def build(force=False, verbose=False):
             print(out)
     tmp = LIB + ".tmp"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-                           "-o", tmp, *objs, "-lcudart_static" if False else "-lcudart"])
+                           "-o", tmp, *objs, "-lcudart"])
     os.replace(tmp, LIB)
     return LIB
 

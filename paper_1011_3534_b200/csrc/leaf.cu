@@ -15,8 +15,9 @@
 // order), and the products are merged in the reference's tree order with a
 // shunting-yard stack keyed by the level of the lowest common ancestor of
 // consecutive k (32 - clz(k_prev ^ k_next)).  Operand tiles stream through a
-// 3-stage cp.async pipeline with padded shared-memory rows (conflict-free
-// fragment loads); CTAs are persistent and take work items from a ticket.
+// 6-stage TMA ring (mbarrier completion; swizzled A boxes, a 5-D B box laid
+// out for conflict-free fragment loads) filled by a producer warp; CTAs are
+// persistent and take work items from a ticket.
 #include <cstdio>
 #include <cstdlib>
 

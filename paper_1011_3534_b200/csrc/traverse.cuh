@@ -60,7 +60,7 @@ struct TraverseArgs {
   uint32_t *group_ids;              // non-empty buckets, ascending i*nb + j
   uint32_t *group_starts;           // their offsets into ks
   uint32_t *ks;                     // inner indices, bucket-major, ascending per bucket
-  // dense traversal (depth <= 7)
+  // dense traversal (depth <= 6; the layouts are instantiated up to 7)
   uint32_t *dn_masks;               // this call's work set (DnLayout; zero at entry)
   uint32_t *dn_masks_clear;         // the previous call's work set, zeroed by this call
   unsigned long long dn_work_words; // words per work set

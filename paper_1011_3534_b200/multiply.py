@@ -3,7 +3,7 @@
 ``spamm(a, b, config)`` keeps the reference's signature, return value and
 exceptions (multiply.py:144-221); the work runs in the CUDA library:
 
-* K2 level-synchronous culling (csrc/cull.cu) -- the retained leaf-triple
+* K2 level-synchronous culling (csrc/traverse.cu) -- the retained leaf-triple
   set, the pruned boxes and every ProductStats integer are identical to the
   reference's, and ``omitted_budget`` is summed with numpy's pairwise order;
 * K3 leaf products on the FP64 tensor-core path (csrc/leaf.cu) merged in the
