@@ -56,6 +56,10 @@ def lib():
         L.oracle_leaf_stage.argtypes = [vp, vp, ctypes.c_int, i64, i32, vp, i64, vp]
         L.oracle_leaf_stage.restype = ctypes.c_int
         L.oracle_free.argtypes = [vp]
+        L.oracle_leaf_norms.argtypes = [vp, ctypes.c_int, i64, i32, vp, vp]
+        L.oracle_pyramid_from_leaves.argtypes = [vp, vp, ctypes.c_int]
+        L.oracle_group_product.argtypes = [vp, vp, ctypes.c_int, i32, vp, i64, ctypes.c_int, vp]
+        L.oracle_group_product.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -154,3 +158,46 @@ def spamm(ad, bd, leaf, tau, dtype=np.float64, tier_tau_decay=False, collect_box
     return dict(a_padded=pa, b_padded=pb, nsq_a=na, occ_a=oa, nsq_b=nb, occ_b=ob,
                 stats=stats, triples=trip, boxes=boxes, tiers=tiers,
                 c_padded=c, nsq_c=nc, occ_c=oc, depth=depth, N=N)
+
+
+# ----------------------------------- pieces for trees too large to hold densely
+def leaf_norms(blocks):
+    """(nsq, occ) of contiguous (count, b, b) leaf blocks (quadtree.py:74-87, :126)."""
+    blocks = np.ascontiguousarray(blocks)
+    count, leaf = blocks.shape[0], blocks.shape[1]
+    nsq = np.zeros(count, np.float64)
+    occ = np.zeros(count, np.uint8)
+    dt = 0 if blocks.dtype == np.float64 else 1
+    if count:
+        lib().oracle_leaf_norms(blocks.ctypes.data, dt, count, leaf, nsq.ctypes.data,
+                                occ.ctypes.data)
+    return nsq, occ
+
+
+def pyramid_from_leaves(nsq_leaf, occ_leaf, depth):
+    """Concatenated (nsq, occ) pyramids from the leaf level (row-major nb x nb)
+    by the reference's parent sums and occupancy OR (quadtree.py:90-92, :135-138)."""
+    nsq = np.zeros(pyramid_size(depth), np.float64)
+    occ = np.zeros(pyramid_size(depth), np.uint8)
+    lv = level_slices(depth)[depth]
+    nsq[lv] = np.asarray(nsq_leaf, np.float64).ravel()
+    occ[lv] = np.asarray(occ_leaf, np.uint8).ravel()
+    lib().oracle_pyramid_from_leaves(nsq.ctypes.data, occ.ctypes.data, depth)
+    return nsq, occ
+
+
+def group_product(a_blocks, b_blocks, ks, depth):
+    """One C block of _leaf_stage (multiply.py:224-257): A(i, k) B(k, j) over the
+    ascending retained ks, merged in the reference's binary-interval order over
+    [0, 2^depth) (multiply.py:119-141).  a_blocks / b_blocks: (len(ks), b, b)."""
+    a_blocks = np.ascontiguousarray(a_blocks)
+    b_blocks = np.ascontiguousarray(b_blocks, dtype=a_blocks.dtype)
+    ks = np.ascontiguousarray(ks, dtype=np.int32)
+    leaf = a_blocks.shape[1]
+    out = np.zeros((leaf, leaf), a_blocks.dtype)
+    dt = 0 if a_blocks.dtype == np.float64 else 1
+    rc = lib().oracle_group_product(a_blocks.ctypes.data, b_blocks.ctypes.data, dt, leaf,
+                                    ks.ctypes.data, len(ks), depth, out.ctypes.data)
+    if rc != 0:
+        raise MemoryError("oracle_group_product failed")
+    return out

@@ -362,3 +362,99 @@ int oracle_leaf_stage(const void *a_padded, const void *b_padded, int dtype, int
   free(starts);
   return status;
 }
+
+/*
+ * Pieces of the above for trees too large to hold densely on the host (the
+ * c5 / c4 checks pull only pyramids and selected blocks off the GPU):
+ *
+ * oracle_leaf_norms: _leaf_norm_sq (quadtree.py:74-87) and the occupancy
+ * test (:126) of `count` contiguous leaf blocks ([count][leaf][leaf]).
+ */
+void oracle_leaf_norms(const void *blocks, int dtype, int64_t count, int32_t leaf, double *nsq,
+                       uint8_t *occ) {
+  const int64_t bb = (int64_t)leaf * leaf;
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < count; ++q) {
+    double acc = 0.0;
+    int nz = 0;
+    for (int64_t e = 0; e < bb; ++e) {
+      const double x = dtype == DT_F64 ? ((const double *)blocks)[q * bb + e]
+                                       : (double)((const float *)blocks)[q * bb + e];
+      nz |= (x != 0.0);
+      acc = acc + x * x;
+    }
+    nsq[q] = acc;
+    occ[q] = (uint8_t)nz;
+  }
+}
+
+/* The levels above the leaves (_aggregate_norm_sq, quadtree.py:90-92, and the
+ * occupancy OR, :135-138) from a filled leaf level, concatenated layout. */
+void oracle_pyramid_from_leaves(double *nsq, uint8_t *occ, int depth) {
+  for (int k = depth - 1; k >= 0; --k) {
+    const int64_t s = (int64_t)1 << k, f = s * 2;
+    const double *fine = nsq + level_offset(k + 1);
+    const uint8_t *ofine = occ + level_offset(k + 1);
+    double *coarse = nsq + level_offset(k);
+    uint8_t *ocoarse = occ + level_offset(k);
+    for (int64_t i = 0; i < s; ++i)
+      for (int64_t j = 0; j < s; ++j) {
+        const int64_t r0 = (2 * i) * f + 2 * j, r1 = r0 + f;
+        coarse[i * s + j] = ((fine[r0] + fine[r0 + 1]) + fine[r1]) + fine[r1 + 1];
+        ocoarse[i * s + j] = ofine[r0] | ofine[r0 + 1] | ofine[r1] | ofine[r1 + 1];
+      }
+  }
+}
+
+/* One C block of _leaf_stage (multiply.py:224-257) from its operand blocks:
+ * a_blocks[q] = A(i, ks[q]), b_blocks[q] = B(ks[q], j), contiguous leaf x
+ * leaf, ks ascending; the products merged over the aligned binary intervals
+ * of [0, 2^depth) (_merge_contributions, :119-141).  Same arithmetic as
+ * oracle_leaf_stage, with the blocks gathered (lda = leaf). */
+static void merge_blocks_f64(const double *A, const double *B, int32_t leaf, const int32_t *ks,
+                             int64_t nk, int64_t lo, int64_t hi, double *out, double *scratch) {
+  const int64_t bb = (int64_t)leaf * leaf;
+  if (nk == 1) {
+    oracle_leaf_gemm_f64(A, B, leaf, leaf, out);
+    return;
+  }
+  const int64_t mid = lo + (hi - lo) / 2;
+  int64_t nl = 0;
+  while (nl < nk && ks[nl] < mid) ++nl;
+  if (nl == 0) { merge_blocks_f64(A, B, leaf, ks, nk, mid, hi, out, scratch); return; }
+  if (nl == nk) { merge_blocks_f64(A, B, leaf, ks, nk, lo, mid, out, scratch); return; }
+  merge_blocks_f64(A, B, leaf, ks, nl, lo, mid, out, scratch + bb);
+  merge_blocks_f64(A + nl * bb, B + nl * bb, leaf, ks + nl, nk - nl, mid, hi, scratch, scratch + bb);
+  for (int64_t q = 0; q < bb; ++q) out[q] = out[q] + scratch[q];
+}
+static void merge_blocks_f32(const float *A, const float *B, int32_t leaf, const int32_t *ks,
+                             int64_t nk, int64_t lo, int64_t hi, float *out, float *scratch) {
+  const int64_t bb = (int64_t)leaf * leaf;
+  if (nk == 1) {
+    oracle_leaf_gemm_f32(A, B, leaf, leaf, out);
+    return;
+  }
+  const int64_t mid = lo + (hi - lo) / 2;
+  int64_t nl = 0;
+  while (nl < nk && ks[nl] < mid) ++nl;
+  if (nl == 0) { merge_blocks_f32(A, B, leaf, ks, nk, mid, hi, out, scratch); return; }
+  if (nl == nk) { merge_blocks_f32(A, B, leaf, ks, nk, lo, mid, out, scratch); return; }
+  merge_blocks_f32(A, B, leaf, ks, nl, lo, mid, out, scratch + bb);
+  merge_blocks_f32(A + nl * bb, B + nl * bb, leaf, ks + nl, nk - nl, mid, hi, scratch, scratch + bb);
+  for (int64_t q = 0; q < bb; ++q) out[q] = out[q] + scratch[q];
+}
+int oracle_group_product(const void *a_blocks, const void *b_blocks, int dtype, int32_t leaf,
+                         const int32_t *ks, int64_t nk, int depth, void *out) {
+  if (nk <= 0) return -1;
+  const size_t esz = dtype == DT_F64 ? sizeof(double) : sizeof(float);
+  void *scratch = malloc(esz * (size_t)leaf * leaf * (depth + 2));
+  if (!scratch) return -1;
+  if (dtype == DT_F64)
+    merge_blocks_f64((const double *)a_blocks, (const double *)b_blocks, leaf, ks, nk, 0,
+                     (int64_t)1 << depth, (double *)out, (double *)scratch);
+  else
+    merge_blocks_f32((const float *)a_blocks, (const float *)b_blocks, leaf, ks, nk, 0,
+                     (int64_t)1 << depth, (float *)out, (float *)scratch);
+  free(scratch);
+  return 0;
+}

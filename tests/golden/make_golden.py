@@ -13,8 +13,12 @@ For every case it imports the reference `spamm` package, builds trees with
   otherwise expose them,
 * ProductStats (integers exact, budget as the exact float) and the pruned
   boxes in the reference's order,
-* C (full padded array for small cases; per-leaf norms plus sample blocks
-  for large ones) and the SpAMM-vs-exact error ``multiply_error``.
+* C (full padded array for small cases; for large ones a 64-bit hash of
+  every nonzero block -- ``block_hash`` -- plus eight blocks as stored) and
+  the SpAMM-vs-exact error ``multiply_error``.
+
+``GOLDEN_ONLY=c1,c3_l2_tau1e-08 python tests/golden/make_golden.py``
+regenerates just the named large cases and merges them into golden.json.
 
 Inputs are regenerated from seeds at test time (numpy PCG64 is
 bit-reproducible), so only the small-case inputs are stored.
@@ -57,6 +61,37 @@ def pyramid(t):
     return nsq, occ
 
 
+HASH_SEED = 77
+
+
+def hash_keys(leaf):
+    """Odd 64-bit multipliers, one per element of a leaf block."""
+    rng = np.random.default_rng(HASH_SEED)
+    return rng.integers(0, 2 ** 63, size=leaf * leaf, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+
+
+def block_hash(blocks):
+    """h = sum_e bits(x_e) * K_e mod 2^64 per block ((m, b, b) array): any
+    change of any element's bits changes h (K_e odd)."""
+    m, b = blocks.shape[0], blocks.shape[1]
+    bits = np.ascontiguousarray(blocks).view(np.uint32 if blocks.dtype == np.float32
+                                             else np.uint64).reshape(m, b * b).astype(np.uint64)
+    with np.errstate(over="ignore"):
+        return (bits * hash_keys(b)[None, :]).sum(axis=1, dtype=np.uint64)
+
+
+def c_block_hashes(c):
+    """(leaf ids i * nb + j, hashes) of every nonzero leaf of the reference's C."""
+    nz = np.argwhere(np.asarray(c._leaf_nonzero))
+    nbk = c.block_grid
+    ids = (nz[:, 0] * nbk + nz[:, 1]).astype(np.int64)
+    out = np.empty(len(ids), np.uint64)
+    for s in range(0, len(ids), 4096):
+        blk = np.stack([np.asarray(c._blocks[i, j]) for i, j in nz[s:s + 4096]])
+        out[s:s + 4096] = block_hash(blk)
+    return ids, out
+
+
 def run_case(name, ad, bd, leaf, tau, dtype=None, tier_tau_decay=False, store_inputs=False,
              store_c="full", recipe=None):
     a = from_dense(ad, leaf_size=leaf, dtype=dtype)
@@ -86,7 +121,11 @@ def run_case(name, ad, bd, leaf, tau, dtype=None, tier_tau_decay=False, store_in
     if store_c == "full":
         arrays["c_padded"] = np.asarray(c._padded)
     else:
-        # a handful of retained C blocks, bit patterns kept as stored
+        # every nonzero C block pinned by a 64-bit linear hash of its bits
+        # (block_hash below), plus a handful of blocks kept as stored
+        ids, hashes = c_block_hashes(c)
+        arrays["c_block_ids"] = ids
+        arrays["c_block_hash"] = hashes
         nbk = a.block_grid
         rng = np.random.default_rng(123)
         occ_leaf = np.argwhere(np.asarray(c._leaf_nonzero))
@@ -113,6 +152,9 @@ def run_case(name, ad, bd, leaf, tau, dtype=None, tier_tau_decay=False, store_in
 
 
 def main():
+    only = [x for x in os.environ.get("GOLDEN_ONLY", "").split(",") if x]
+    if only:  # regenerate just these cases, keeping the others' records
+        return main_only(only)
     metas = []
     rng = np.random.default_rng(20261020)
     # -- small white-box cases (inputs stored): padding, leaf sizes, zeros, -0.0, f32
@@ -162,13 +204,42 @@ def main():
                                   recipe="workloads:c3_l3"))
             print(metas[-1]["name"], metas[-1]["stats"])
         a, b, leaf, taus = workloads.make_config("c3_l2")
-        metas.append(run_case("c3_l2_tau1e-06", a, b, leaf, 1e-6, store_c="sample",
-                              recipe="workloads:c3_l2"))
-        print(metas[-1]["name"], metas[-1]["stats"])
+        for tau in taus:
+            metas.append(run_case(f"c3_l2_tau{tau:.0e}", a, b, leaf, tau, store_c="sample",
+                                  recipe="workloads:c3_l2"))
+            print(metas[-1]["name"], metas[-1]["stats"])
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(dict(generator="tests/golden/make_golden.py",
                        reference="arxiv/paper_1011_3534 spamm 0.1.0 (pkg/src/spamm)",
                        numpy=np.__version__, cases=metas), fh, indent=1)
+
+
+def large_case(name):
+    """(inputs, leaf, tau, recipe) of a seeded BASELINE-config case by name."""
+    if name == "refpair_n512_b4":
+        d = np.abs(np.arange(512)[:, None] - np.arange(512)[None, :])
+        return np.exp(-1.0 * d), np.exp(-2.0 * d), 4, 1e-8, "exp(-alpha*|i-j|), alpha=1.0 / 2.0"
+    cfg = name.split("_tau")[0]
+    a, b, leaf, taus = workloads.make_config(cfg)
+    tau = float(name.split("_tau")[1]) if "_tau" in name else taus[0]
+    return a, (a if cfg == "c2" else b), leaf, tau, f"workloads:{cfg}"
+
+
+def main_only(names):
+    path = os.path.join(HERE, "golden.json")
+    with open(path) as fh:
+        doc = json.load(fh)
+    by_name = {c["name"]: c for c in doc["cases"]}
+    for name in names:
+        a, b, leaf, tau, recipe = large_case(name)
+        meta = run_case(name, a, b, leaf, tau, store_c="sample", recipe=recipe)
+        print(meta["name"], meta["stats"], flush=True)
+        if name in by_name:
+            doc["cases"][[c["name"] for c in doc["cases"]].index(name)] = meta
+        else:
+            doc["cases"].append(meta)
+    with open(path, "w") as fh:
+        json.dump(doc, fh, indent=1)
 
 
 if __name__ == "__main__":

@@ -114,3 +114,23 @@ def test_pending_blocks_wait_is_idempotent_without_a_handle():
     blocks = np.zeros((3, 2, 2))
     p = PendingBlocks(None, ids, blocks)
     assert p.wait()[0] is ids and p.wait()[1] is blocks
+
+
+def test_shim_aliases_every_submodule():
+    """The shim maps the reference's module names onto this package's."""
+    import sys
+
+    from paper_1011_3534_b200 import compat
+
+    pkg = compat.install()
+    try:
+        import spamm
+
+        assert spamm is pkg
+        for m in compat.SUBMODULES:
+            assert sys.modules[f"spamm.{m}"].__name__ == f"paper_1011_3534_b200.{m}"
+        from spamm.multiply import SpammConfig, spamm as fn  # noqa: F401
+        from spamm.quadtree import from_dense, to_dense  # noqa: F401
+    finally:
+        compat.uninstall()
+    assert "spamm" not in sys.modules or sys.modules["spamm"] is not pkg

@@ -6,7 +6,9 @@ the B200 and compared:
 * retained leaf-triple set and pruned boxes (in reference order): exact
 * ProductStats integers: exact; omitted_budget: bit-exact (numpy pairwise)
 * C: bit-exact vs the reference (DMMA == the BLAS FMA chain, same merge
-  tree); the contract bar, 1e-12 relative Frobenius, is asserted as well.
+  tree) -- whole for small cases; for the large ones every nonzero block
+  through a 64-bit hash of its bits plus eight blocks byte for byte; the
+  contract bar, 1e-12 relative Frobenius, is asserted as well.
 """
 
 import numpy as np
@@ -64,10 +66,17 @@ def _check(name, traversal="auto"):
         assert np.linalg.norm(got.astype(np.float64) - ref) / den <= 1e-12
         assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), "C bit-exact"
     else:
-        pad = c._padded
+        nbk = c.block_grid
         for (i, j), blk in zip(z["c_sample_ij"], z["c_sample"]):
-            mine = pad[i * L:(i + 1) * L, j * L:(j + 1) * L]
+            mine = gc.tree_blocks(c, [int(i) * nbk + int(j)])[0]
             assert np.array_equal(mine.view(np.uint8), blk.view(np.uint8)), ("C block", i, j)
+        if "c_block_ids" in z:  # every nonzero block of C, pinned by its hash
+            ids, want = z["c_block_ids"], z["c_block_hash"]
+            mine_ids = np.flatnonzero(np.asarray(c._leaf_nonzero).reshape(-1))
+            assert np.array_equal(mine_ids, ids), "C's nonzero blocks"
+            got = gc.tree_block_hashes(c, ids)
+            bad = np.flatnonzero(got != want)
+            assert bad.size == 0, f"{bad.size} of {len(ids)} C blocks differ, first id {ids[bad[0]]}"
     nc, oc = _pyr(c)
     assert np.array_equal(oc, z["occ_c"]), "C occupancy"
     assert np.array_equal(nc.view(np.uint64), z["nsq_c"].view(np.uint64)), "C norms"

@@ -78,3 +78,31 @@ def test_row_shards_sum_to_whole():
         assert abs(tot["omitted_budget"] - full["omitted_budget"]) <= 1e-12 * full["omitted_budget"]
         assert np.array_equal(np.concatenate(parts), trip)
         assert nbox == len(boxes)
+
+
+def test_oracle_pieces_reassemble_the_whole_multiply():
+    """oracle.leaf_norms + pyramid_from_leaves rebuild C's pyramid and
+    oracle.group_product rebuilds every C block from gathered operand blocks
+    (the pieces the full-size GPU checks use) -- bit for bit vs the dense
+    oracle on config 1."""
+    from oracle import oracle
+    from paper_1011_3534_b200 import workloads
+
+    a, b, leaf, taus = workloads.make_config("c1")
+    r = oracle.spamm(a, b, leaf, taus[0])
+    N, depth = r["N"], r["depth"]
+    nb = N // leaf
+    blk = r["c_padded"].reshape(nb, leaf, nb, leaf).swapaxes(1, 2).reshape(-1, leaf, leaf)
+    nsq, occ = oracle.pyramid_from_leaves(*oracle.leaf_norms(blk), depth)
+    assert np.array_equal(nsq.view(np.uint64), r["nsq_c"].view(np.uint64))
+    assert np.array_equal(occ, r["occ_c"])
+    t, pa, pb = r["triples"], r["a_padded"], r["b_padded"]
+    gid = t[:, 0].astype(np.int64) * nb + t[:, 1]
+    starts = np.flatnonzero(np.r_[True, gid[1:] != gid[:-1]])
+    for s0, s1 in zip(starts, np.r_[starts[1:], len(t)]):
+        i, j, ks = t[s0, 0], t[s0, 1], t[s0:s1, 2]
+        A = np.stack([pa[i * leaf:(i + 1) * leaf, k * leaf:(k + 1) * leaf] for k in ks])
+        B = np.stack([pb[k * leaf:(k + 1) * leaf, j * leaf:(j + 1) * leaf] for k in ks])
+        got = oracle.group_product(A, B, ks, depth)
+        want = r["c_padded"][i * leaf:(i + 1) * leaf, j * leaf:(j + 1) * leaf]
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (i, j)
