@@ -37,6 +37,9 @@
  *   spamm_tree_tridiagonal    <- generators.gen_model_hamiltonian generators.py:76-88
  *   spamm_multiply_rows       <- (new) output block-row shard of spamm for multi-GPU
  *                                partitioning; the reference is single-process.
+ *   spamm_tc2_update          <- the add/scale pair of tc2_step  purification.py:123-133
+ *   spamm_tree_band_* , spamm_tree_pyramid_rebuild, spamm_tree_blocks_*_device,
+ *   spamm_tree_diagonal_rows  <- (new) row bands of distributed matrices
  */
 #ifndef SPAMM_B200_H
 #define SPAMM_B200_H
@@ -74,6 +77,14 @@ extern "C" {
  * trees (depth <= 6) default to the dense single-pass kernel; this flag
  * forces the tiered breadth-first kernel (testing / comparison). */
 #define SPAMM_TIERED_TRAVERSAL 0x10u
+/* Traversal only (the multi-GPU plan: which operand blocks a row shard's
+ * retained triples touch): no leaf products and no C; *c is set to NULL.
+ * Combine with SPAMM_KEEP_TRIPLES. */
+#define SPAMM_TRAVERSE_ONLY 0x20u
+/* Keep every tau-pruned call's (tier, i, j, k) and norm product, in reference
+ * order (spamm_product_pruned): the multi-GPU budget merges the shards' lists
+ * into the single-GPU order and sums them with the reference's pairwise sum. */
+#define SPAMM_KEEP_PRUNED 0x40u
 
 typedef struct spamm_tree spamm_tree;
 typedef struct spamm_product spamm_product;
@@ -214,7 +225,48 @@ SPAMM_API int spamm_multiply_rows(const spamm_tree *a, const spamm_tree *b, doub
 SPAMM_API int spamm_product_boxes(const spamm_product *p, int64_t *out, int64_t capacity);
 /* triples: 3 int32 per retained leaf product (i, j, k), sorted by (i, j, k). */
 SPAMM_API int spamm_product_triples(const spamm_product *p, int32_t *out, int64_t capacity);
+/* pruned calls (SPAMM_KEEP_PRUNED): 4 int32 per call (tier, i, j, k) and its
+ * norm product, reference order; count = spamm_product_pruned_count(p). */
+SPAMM_API int spamm_product_pruned(const spamm_product *p, int32_t *tier_ijk, double *np_out,
+                                   int64_t capacity);
+SPAMM_API int64_t spamm_product_pruned_count(const spamm_product *p);
 SPAMM_API void spamm_product_free(spamm_product *p);
+
+/* -- row bands of distributed matrices (multi-GPU; csrc/shard.cu) ------------
+ * A distributed matrix is one tree per rank: the element storage of the
+ * rank's C block rows [row_lo, row_hi) plus operand blocks fetched from other
+ * ranks, and the WHOLE matrix's pyramid, whose leaf level the caller
+ * all-gathers (NCCL) before spamm_tree_pyramid_rebuild.  Whole-storage reads
+ * of a band tree fail (status 1): gather the bands first.  The reference is
+ * single-process; these replace nothing in it. */
+/* band rows (device pointer to logical row row_lo*leaf, leading dimension ld)
+ * -> band tree whose pyramid is that of the band alone until rebuilt */
+SPAMM_API int spamm_tree_band_from_device(const void *rows, int64_t n, int64_t ld, int32_t leaf,
+                                          int32_t dtype, int64_t row_lo, int64_t row_hi,
+                                          int32_t device, spamm_tree **out);
+/* declare a tree (e.g. a spamm_multiply_rows product) the band [row_lo, row_hi) */
+SPAMM_API int spamm_tree_band_set(spamm_tree *t, int64_t row_lo, int64_t row_hi);
+/* the levels above the leaves and every nrm from the (gathered) leaf level */
+SPAMM_API int spamm_tree_pyramid_rebuild(spamm_tree *t);
+/* listed leaves (device ids i*block_grid+j) <-> contiguous device buffer */
+SPAMM_API int spamm_tree_blocks_gather_device(const spamm_tree *t, const int64_t *ids, int64_t count,
+                                              void *dev_out);
+SPAMM_API int spamm_tree_blocks_scatter_device(spamm_tree *t, const int64_t *ids, int64_t count,
+                                               const void *dev_in);
+/* the logical diagonal of block rows [row_lo, row_hi) to host memory */
+SPAMM_API int spamm_tree_diagonal_rows(const spamm_tree *t, int64_t row_lo, int64_t row_hi,
+                                       void *host_out);
+/* One TC2 sweep's element-wise work (purification.py:123-133 and the driver's
+ * sweep displacement, :190-199) on block rows [row_lo, row_hi) in one pass:
+ * *d_out = norms of D = add(X2, scale(X,-1)) (a norms-only tree: the
+ * fixed-point gap); if make_y also *y_out = Y = add(scale(X,2), scale(X2,-1))
+ * and *e_out = norms of add(Y, scale(X,-1)) -- with the reference's
+ * pass-through of blocks nonzero in one operand only (quadtree.py:280-299),
+ * bit-identical to those tree operations.  roots[0], roots[1]: the root
+ * squared norms of D and E. */
+SPAMM_API int spamm_tc2_update(const spamm_tree *x, const spamm_tree *x2, int32_t make_y,
+                               int64_t row_lo, int64_t row_hi, spamm_tree **y_out,
+                               spamm_tree **d_out, spamm_tree **e_out, double *roots);
 
 /* -- box log ordering ------------------------------------------------------- */
 /* order[r] = index of the box written r-th in a box log: boxes (5 int64 each,

@@ -28,6 +28,8 @@ COUNT_STATS = 0x2
 TIER_TAU_DECAY = 0x4
 KEEP_TRIPLES = 0x8
 TIERED_TRAVERSAL = 0x10
+TRAVERSE_ONLY = 0x20
+KEEP_PRUNED = 0x40
 
 # every symbol include/spamm_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
@@ -41,7 +43,10 @@ EXPORTED = (
     "spamm_tree_blocks_to_host", "spamm_boxes_morton_order", "spamm_tree_toeplitz",
     "spamm_tree_tridiagonal", "spamm_tree_recompute_norms",
     "spamm_tree_blocks_to_host_async", "spamm_transfer_wait", "spamm_tree_from_host_async",
-    "spamm_tree_wait",
+    "spamm_tree_wait", "spamm_product_pruned", "spamm_product_pruned_count",
+    "spamm_tree_band_from_device", "spamm_tree_band_set", "spamm_tree_pyramid_rebuild",
+    "spamm_tree_blocks_gather_device", "spamm_tree_blocks_scatter_device",
+    "spamm_tree_diagonal_rows", "spamm_tc2_update",
 )
 
 
@@ -118,6 +123,16 @@ def load(path=LIB_PATH):
         L.spamm_tree_recompute_norms.argtypes = [vp, vp]
         L.spamm_tree_toeplitz.argtypes = [vp, i64, i32, i32, i32, pp]
         L.spamm_tree_tridiagonal.argtypes = [vp, vp, i64, i32, i32, i32, pp]
+        L.spamm_product_pruned.argtypes = [vp, vp, vp, i64]
+        L.spamm_product_pruned_count.argtypes = [vp]
+        L.spamm_product_pruned_count.restype = i64
+        L.spamm_tree_band_from_device.argtypes = [vp, i64, i64, i32, i32, i64, i64, i32, pp]
+        L.spamm_tree_band_set.argtypes = [vp, i64, i64]
+        L.spamm_tree_pyramid_rebuild.argtypes = [vp]
+        L.spamm_tree_blocks_gather_device.argtypes = [vp, vp, i64, vp]
+        L.spamm_tree_blocks_scatter_device.argtypes = [vp, vp, i64, vp]
+        L.spamm_tree_diagonal_rows.argtypes = [vp, i64, i64, vp]
+        L.spamm_tc2_update.argtypes = [vp, vp, i32, i64, i64, pp, pp, pp, vp]
         _lib = L
         return L
 

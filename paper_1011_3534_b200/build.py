@@ -15,7 +15,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libspamm_b200.so")
-SOURCES = ["tree.cu", "traverse.cu", "leaf.cu", "multiply.cu", "algebra.cu", "boxes.cu", "generate.cu"]
+SOURCES = ["tree.cu", "traverse.cu", "leaf.cu", "multiply.cu", "algebra.cu", "boxes.cu", "generate.cu",
+           "shard.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

@@ -166,6 +166,12 @@ struct spamm_tree {
   // (tree_join), and root_norm_sq is fetched on the first spamm_tree_wait.
   cudaEvent_t ready = nullptr;
   bool root_pending = false;
+  // Row band of a distributed matrix (multi-GPU layout, csrc/shard.cu): the
+  // element storage holds block rows [band_lo, band_hi) plus any blocks
+  // fetched from other ranks (halo), while the pyramid is the whole matrix's
+  // (its leaf level all-gathered).  Whole-storage reads are refused.
+  bool distributed = false;
+  int64_t band_lo = 0, band_hi = 0;
   int64_t elem_size() const { return dtype == SPAMM_DTYPE_F64 ? 8 : 4; }
 };
 
@@ -173,6 +179,8 @@ namespace spamm {
 struct DeviceContext;
 // zero-fill a lazy tree's empty blocks (stream-ordered on ctx->stream)
 int materialize(DeviceContext *ctx, const spamm_tree *t);
+// upper pyramid levels + interior nrm from the leaf level (tree.cu)
+int pyramid_upper_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches = nullptr);
 // order ctx->stream after an asynchronous build of t (no-op otherwise)
 int tree_join(DeviceContext *ctx, const spamm_tree *t);
 }  // namespace spamm

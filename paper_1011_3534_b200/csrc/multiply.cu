@@ -21,6 +21,8 @@
 struct spamm_product {
   std::vector<int64_t> boxes;    // 5 per box: i_lo, j_lo, k_lo, edge, tier
   std::vector<int32_t> triples;  // 3 per retained leaf product: i, j, k
+  std::vector<int32_t> pruned;   // 4 per tau-pruned call: tier, i, j, k (SPAMM_KEEP_PRUNED)
+  std::vector<double> pruned_np; // its norm product rn(rn(sqrt a) rn(sqrt b))
 };
 
 namespace spamm {
@@ -83,6 +85,15 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
               (long long)row_hi, (long long)a->nb);
     return SPAMM_ERR_VALUE;
   }
+  if (a->distributed && (row_lo < a->band_lo || row_hi > a->band_hi)) {
+    set_error("rows [%lld, %lld) are not in A's band [%lld, %lld) (distributed operand)",
+              (long long)row_lo, (long long)row_hi, (long long)a->band_lo, (long long)a->band_hi);
+    return SPAMM_ERR_VALUE;
+  }
+  if (!a->padded || !b->padded) {
+    set_error("norms-only tree as a multiply operand");
+    return SPAMM_ERR_VALUE;
+  }
   if (a->depth > 21 || a->nb * a->nb >= (int64_t(1) << 31)) {
     set_error("quadtree depth %d / block grid %lld exceeds the supported range", a->depth,
               (long long)a->nb);
@@ -101,8 +112,11 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   if (ctx->cull_capacity == 0) ctx->cull_capacity = std::max<size_t>(1 << 16, 2 * G);
   if (ctx->pruned_capacity == 0) ctx->pruned_capacity = std::max<size_t>(1 << 16, 2 * G);
   TraverseCounters *hc = (TraverseCounters *)ctx->host_pinned;
+  // traversal only (the multi-GPU plan: which operand blocks a shard needs):
+  // no product, no leaf products, no C tree
+  const bool trav_only = (flags & SPAMM_TRAVERSE_ONLY) != 0;
   spamm_tree *c = nullptr;
-  SPAMM_TRY(alloc_tree(ctx, a->n, a->leaf, a->dtype, &c));
+  if (!trav_only) SPAMM_TRY(alloc_tree(ctx, a->n, a->leaf, a->dtype, &c));
   int rc = SPAMM_OK;
   int launches = 0;
   for (int attempt = 0;; ++attempt) {
@@ -198,7 +212,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     }
     // device timing starts at the first kernel (host-side setup excluded)
     SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[0], st));
-    if (dense) {
+    if (dense && c) {
       ta.c_nsq_leaf = c->nsq + level_offset(depth);
       ta.c_nrm_leaf = c->nrm + level_offset(depth);
       ta.c_occ_leaf = c->occ + level_offset(depth);
@@ -209,6 +223,27 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     ctx->counter_parity ^= 1;
     if (dense) ctx->dense_parity ^= 1;
     ++launches;
+    if (trav_only) {
+      SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
+      const SmallRead r{hc, dtc, sizeof(TraverseCounters)};
+      if ((rc = read_small_sync(ctx, st, &r, 1))) break;
+      ++launches;
+      ctx->last_overlapped = ctx->last_k3_pdl = false;
+      if (!hc->overflow) break;
+      unsigned long long need = 0, pneed = 0;
+      for (int t = 0; t <= depth; ++t) {
+        need = std::max(need, hc->n_active[t]);
+        pneed += hc->n_pruned[t];
+      }
+      ctx->cull_capacity = std::max<size_t>(2 * cap, need + need / 8);
+      ctx->pruned_capacity = std::max<size_t>(need > cap ? pcap : 2 * pcap, pneed + pneed / 8);
+      if (attempt > 40) {
+        set_error("culling capacity did not converge");
+        rc = SPAMM_ERR_INTERNAL;
+        break;
+      }
+      continue;
+    }
     // C's block storage is not zero-filled: a product is a lazy tree whose
     // empty blocks (no retained triple; the same as occupancy clear) are
     // zero by definition and never read by a multiply, a norm build or a
@@ -337,7 +372,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     free_tree_async(c, st);
     return rc;
   }
-  if (getenv("SPAMM_GEMM_TIMELINE")) {
+  if (getenv("SPAMM_GEMM_TIMELINE") && !trav_only) {
     std::vector<unsigned long long> tl(3 * 4096);
     cudaMemcpy(tl.data(), ctx->reduce_tmp.ptr, sizeof(unsigned long long) * 3 * 4096,
                cudaMemcpyDeviceToHost);
@@ -399,7 +434,8 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   // slot 0: kernel entry -> phase 0 (negative offset of the prologue)
   s.traverse_phase_us[0] = cc.phase_ns[15] ? (float)((double)(cc.phase_ns[0] - cc.phase_ns[15]) * 1e-3) : 0.f;
   cudaEventElapsedTime(&s.ms_total, ctx->ev[0], ctx->ev[4]);
-  if (!ctx->last_k3_pdl) cudaEventElapsedTime(&s.ms_cull, ctx->ev[0], ctx->ev[1]);
+  if (trav_only) s.ms_cull = s.ms_total;
+  else if (!ctx->last_k3_pdl) cudaEventElapsedTime(&s.ms_cull, ctx->ev[0], ctx->ev[1]);
   static const bool tail_dbg = getenv("SPAMM_TAIL_DEBUG") != nullptr;
   if (tail_dbg && cc.k3_t1 && cc.k1_t1)
     fprintf(stderr, "[tail] k3 span %.1f us, C tree done %.1f us after K3\n",
@@ -414,6 +450,8 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       s.ms_ctree = (float)((double)(cc.k1_t1 - cc.k3_t1) * 1e-6);
     else
       s.ms_ctree = std::max(0.f, s.ms_total - s.ms_cull - s.ms_gemm);
+  } else if (trav_only) {
+    // (no leaf products, no C tree)
   } else if (ctx->last_k3_pdl && cc.k3_t0n && cc.k3_t1) {
     s.ms_gemm = (float)((double)(cc.k3_t1 - ~cc.k3_t0n) * 1e-6);
     s.ms_leaf = s.ms_gemm;
@@ -425,13 +463,14 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   }
   // K3 launched programmatically behind the traversal: no event between
   // them; the traversal's share is the multiply's remainder
-  if (ctx->last_k3_pdl) s.ms_cull = std::max(0.f, s.ms_total - s.ms_gemm - s.ms_ctree);
+  if (ctx->last_k3_pdl && !trav_only) s.ms_cull = std::max(0.f, s.ms_total - s.ms_gemm - s.ms_ctree);
   (void)cudaGetLastError();  // (timing queries must not leave an error for the next call)
 
   // ------------------------------------------------------- product records
   if (product) {
     auto p = std::make_unique<spamm_product>();
     cudaError_t e = cudaSuccess;
+    const bool keep_pruned = (flags & SPAMM_KEEP_PRUNED) && (flags & SPAMM_COUNT_STATS);
     if ((flags & SPAMM_COLLECT_BOXES) && total_pruned) {
       std::vector<uint64_t> codes(total_pruned);
       e = cudaMemcpy(codes.data(), ctx->pruned_codes.ptr, total_pruned * sizeof(uint64_t),
@@ -447,6 +486,25 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
                           {int64_t(i) * edge, int64_t(j) * edge, int64_t(k) * edge, edge, t});
         }
       }
+    }
+    if (keep_pruned && total_pruned && e == cudaSuccess) {
+      // the pruned calls' norm products in reference order (tier-major; the
+      // multi-GPU budget merges the shards' lists into this order)
+      std::vector<uint64_t> codes(total_pruned);
+      p->pruned_np.resize(total_pruned);
+      e = cudaMemcpy(codes.data(), ctx->pruned_codes.ptr, total_pruned * sizeof(uint64_t),
+                     cudaMemcpyDeviceToHost);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(p->pruned_np.data(), ctx->pruned_vals.ptr, total_pruned * sizeof(double),
+                       cudaMemcpyDeviceToHost);
+      p->pruned.reserve(4 * total_pruned);
+      int64_t pos = 0;
+      for (int t = 0; t <= depth && e == cudaSuccess; ++t)
+        for (unsigned long long q = 0; q < cc.n_pruned[t]; ++q, ++pos) {
+          uint32_t i, j, k;
+          unpack_triple(codes[pos], i, j, k);
+          p->pruned.insert(p->pruned.end(), {(int32_t)t, (int32_t)i, (int32_t)j, (int32_t)k});
+        }
     }
     if ((flags & SPAMM_KEEP_TRIPLES) && m && e == cudaSuccess) {
       const int64_t ng = s.n_groups;
@@ -475,6 +533,11 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     *product = p.release();
   }
   if (stats) *stats = s;
+  if (c && a->distributed) {  // a row band of a distributed product
+    c->distributed = true;
+    c->band_lo = row_lo;
+    c->band_hi = row_hi;
+  }
   *c_out = c;
   return SPAMM_OK;
 }
@@ -513,6 +576,19 @@ int spamm_product_triples(const spamm_product *p, int32_t *out, int64_t capacity
   if (capacity < n) { set_error("triple buffer too small"); return SPAMM_ERR_VALUE; }
   std::copy(p->triples.begin(), p->triples.end(), out);
   return SPAMM_OK;
+}
+
+int spamm_product_pruned(const spamm_product *p, int32_t *tier_ijk, double *np_out, int64_t capacity) {
+  if (!p) { set_error("null product"); return SPAMM_ERR_VALUE; }
+  const int64_t n = (int64_t)p->pruned_np.size();
+  if (capacity < n) { set_error("pruned buffer too small"); return SPAMM_ERR_VALUE; }
+  std::copy(p->pruned.begin(), p->pruned.end(), tier_ijk);
+  std::copy(p->pruned_np.begin(), p->pruned_np.end(), np_out);
+  return SPAMM_OK;
+}
+
+int64_t spamm_product_pruned_count(const spamm_product *p) {
+  return p ? (int64_t)p->pruned_np.size() : 0;
 }
 
 void spamm_product_free(spamm_product *p) { delete p; }

@@ -885,7 +885,6 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
                         unsigned long long *t_end) {
   // builds on copy_in run concurrently with the main stream's: own tickets
   Scratch &k1t = st == ctx->copy_in ? ctx->k1_ticket_in : ctx->k1_ticket;
-  Scratch &pyt = st == ctx->copy_in ? ctx->pyr_tickets_in : ctx->pyr_tickets;
   SPAMM_TRY(ensure_scratch(k1t, sizeof(unsigned), st, /*zeroed=*/true));
   unsigned *ticket = (unsigned *)k1t.ptr;
   bool fused = false;
@@ -950,6 +949,14 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
     SPAMM_TRY(launch_leaf_norms<float>(t, st, list, list_count, list_cap, ticket, ov, &fused));
   if (launches) ++*launches;
   if (fused) return SPAMM_OK;  // the last K1 CTA built the pyramid
+  return pyramid_upper_async(ctx, t, st, launches);
+}
+
+// The levels above the leaves (and every interior nrm) from t's leaf level:
+// parents ((c11 + c12) + c21) + c22 and occupancy OR (quadtree.py:90-92,
+// :135-138).  Stream-ordered.
+int pyramid_upper_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches) {
+  Scratch &pyt = st == ctx->copy_in ? ctx->pyr_tickets_in : ctx->pyr_tickets;
   static bool carve = false;
   if (!carve) {
     cudaFuncSetAttribute(pyramid_fused_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1038,6 +1045,13 @@ __global__ void zero_unoccupied_kernel(unsigned char *__restrict__ padded, int64
 int materialize(DeviceContext *ctx, const spamm_tree *tc) {
   spamm_tree *t = const_cast<spamm_tree *>(tc);  // the values (zeros) do not change
   SPAMM_TRY(tree_join(ctx, t));
+  if (t->distributed || !t->padded) {
+    set_error(t->distributed ? "row band [%lld, %lld) of a distributed tree: only its rows are held "
+                               "here (gather the bands first)"
+                             : "norms-only tree (no element storage)",
+              (long long)t->band_lo, (long long)t->band_hi);
+    return SPAMM_ERR_VALUE;
+  }
   if (!t->lazy_empty) return SPAMM_OK;
   const int64_t G = t->nb * t->nb;
   const unsigned grid = (unsigned)std::min<int64_t>((G + 7) / 8, (int64_t)ctx->num_sms * 8);
@@ -1330,13 +1344,15 @@ int spamm_tree_recompute_norms(const spamm_tree *t, double *nsq_host) {
 
 int spamm_tree_device_ptrs(const spamm_tree *t, void **padded, double **nsq, uint8_t **occ) {
   if (!t) { set_error("null tree"); return SPAMM_ERR_VALUE; }
-  if ((padded && t->lazy_empty) || t->ready) {  // the caller may read any of the storage
+  {
+    // the caller may read any of the storage (a distributed band hands out
+    // its raw storage: only its own rows and fetched blocks are defined)
     DeviceContext *ctx;
     SPAMM_TRY(get_context(t->device, &ctx));
     std::lock_guard<std::mutex> lk(ctx->mu);
-    if (padded) SPAMM_TRY(materialize(ctx, t));
+    if (padded && t->lazy_empty && !t->distributed) SPAMM_TRY(materialize(ctx, t));
     else SPAMM_TRY(tree_join(ctx, t));
-    SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    SPAMM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // (every queued write is visible)
   }
   if (padded) *padded = t->padded;
   if (nsq) *nsq = t->nsq;

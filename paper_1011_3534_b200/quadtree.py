@@ -445,6 +445,27 @@ def filter_drop(m, tau):
     return _wrap(h.value)
 
 
+def tc2_update(x, x2, make_y, rows=None):
+    """One TC2 sweep's element-wise work in one device pass (extension;
+    spamm_tc2_update in the C ABI): the root squared norms of
+    D = add(x2, scale(x, -1)) and, if ``make_y``, of E = add(Y, scale(x, -1)),
+    plus Y = add(scale(x, 2), scale(x2, -1)) itself -- bit-identical to those
+    tree operations (quadtree.py:280-299), without building D or E.
+    ``rows=(lo, hi)`` restricts it to block rows [lo, hi) (a row band).
+
+    Returns (y or None, d, e or None, d_root_nsq, e_root_nsq); d and e are
+    norms-only trees (their pyramids; no element storage)."""
+    _require_conformable(x, x2)
+    lo, hi = (0, x.block_grid) if rows is None else rows
+    y, d, e = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    roots = np.zeros(2, np.float64)
+    _lib.check(_lib.load().spamm_tc2_update(x._handle, x2._handle, int(bool(make_y)), int(lo),
+                                            int(hi), ctypes.byref(y), ctypes.byref(d),
+                                            ctypes.byref(e), roots.ctypes.data))
+    return (_wrap(y.value) if y.value else None, _wrap(d.value),
+            _wrap(e.value) if e.value else None, float(roots[0]), float(roots[1]))
+
+
 def node_norm(m):
     """Frobenius norm from the root's cached norm (quadtree.py:269-271)."""
     return m.norm()
