@@ -27,7 +27,8 @@ class _CullResult(ctypes.Structure):
                 ("n_triples", ctypes.c_int64), ("triples", ctypes.POINTER(ctypes.c_int32)),
                 ("n_boxes", ctypes.c_int64), ("boxes", ctypes.POINTER(ctypes.c_int64)),
                 ("tier_candidates", ctypes.c_int64 * 32),
-                ("tier_survivors", ctypes.c_int64 * 32)]
+                ("tier_survivors", ctypes.c_int64 * 32),
+                ("box_np", ctypes.POINTER(ctypes.c_double))]
 
 
 def build():
@@ -121,13 +122,16 @@ def cull(nsq_a, occ_a, nsq_b, occ_b, depth, N, tau, tier_tau_decay=False, count_
         else np.zeros((0, 3), np.int32)
     boxes = np.ctypeslib.as_array(r.boxes, shape=(r.n_boxes, 5)).copy() if r.n_boxes \
         else np.zeros((0, 5), np.int64)
+    box_np = np.ctypeslib.as_array(r.box_np, shape=(r.n_boxes,)).copy() if r.n_boxes \
+        else np.zeros(0)
     L.oracle_free(ctypes.cast(r.triples, ctypes.c_void_p))
     L.oracle_free(ctypes.cast(r.boxes, ctypes.c_void_p))
+    L.oracle_free(ctypes.cast(r.box_np, ctypes.c_void_p))
     stats = dict(leaf_matmuls=r.leaf_matmuls, pruned_calls=r.pruned_calls,
                  omitted_budget=r.omitted_budget, max_depth_reached=r.max_depth_reached,
                  pruned_volume=r.pruned_volume, empty_skip_volume=r.empty_skip_volume)
     tiers = dict(candidates=list(r.tier_candidates[:depth + 1]),
-                 survivors=list(r.tier_survivors[:depth + 1]))
+                 survivors=list(r.tier_survivors[:depth + 1]), box_np=box_np)
     return stats, trip, boxes, tiers
 
 

@@ -127,6 +127,7 @@ typedef struct {
   int64_t n_boxes;     /* tau-pruned boxes, tier-major then candidate order  */
   int64_t *boxes;      /* 5 * n_boxes: i_lo, j_lo, k_lo, edge, tier          */
   int64_t tier_candidates[32], tier_survivors[32];
+  double *box_np;      /* n_boxes: each box's norm product (multiply.py:185)  */
 } oracle_cull_result;
 
 void oracle_free(void *p) { free(p); }
@@ -209,8 +210,10 @@ int oracle_cull_rows(const double *nsq_a, const uint8_t *occ_a, const double *ns
           if (res->n_boxes == box_cap) {
             box_cap = box_cap ? 2 * box_cap : 1024;
             res->boxes = (int64_t *)realloc(res->boxes, sizeof(int64_t) * 5 * box_cap);
-            if (!res->boxes) return -1;
+            res->box_np = (double *)realloc(res->box_np, sizeof(double) * box_cap);
+            if (!res->boxes || !res->box_np) return -1;
           }
+          res->box_np[res->n_boxes] = np_;
           int64_t *bx = res->boxes + 5 * res->n_boxes++;
           bx[0] = (int64_t)i * edge; bx[1] = (int64_t)j * edge; bx[2] = (int64_t)k * edge;
           bx[3] = edge; bx[4] = tier;

@@ -92,12 +92,19 @@ class MultiplyDetail:
     ms_gemm: float = 0.0
     kernel_launches: int = 0
     traverse_phase_us: list = field(default_factory=list)
+    pruned: np.ndarray | None = None        # (p, 4) int32 (tier, i, j, k), keep_pruned
+    pruned_np: np.ndarray | None = None     # (p,) their norm products, reference order
+    halo_bytes: int = 0                     # operand bytes fetched (distributed multiply)
 
 
-def _flags(config, keep_triples, traversal="auto"):
+def _flags(config, keep_triples, traversal="auto", traverse_only=False, keep_pruned=False):
     if traversal not in ("auto", "tiered"):
         raise ValueError(f"traversal must be 'auto' or 'tiered', got {traversal!r}")
     f = _lib.TIERED_TRAVERSAL if traversal == "tiered" else 0
+    if traverse_only:
+        f |= _lib.TRAVERSE_ONLY
+    if keep_pruned:
+        f |= _lib.KEEP_PRUNED
     if config.collect_boxes:
         f |= _lib.COLLECT_BOXES
     if config.count_stats:
@@ -109,12 +116,16 @@ def _flags(config, keep_triples, traversal="auto"):
     return f
 
 
-def spamm_detailed(a, b, config=None, keep_triples=False, rows=None, traversal="auto"):
+def spamm_detailed(a, b, config=None, keep_triples=False, rows=None, traversal="auto",
+                   traverse_only=False, keep_pruned=False):
     """spamm() plus a MultiplyDetail (retained triples, per-tier counts,
     device timings).  ``rows=(lo, hi)`` restricts the product to C leaf block
     rows [lo, hi) -- the shard of one rank in the multi-GPU layout.
     ``traversal="tiered"`` forces the breadth-first tier kernel even where
-    the dense single-pass kernel applies (depth <= 6); results are identical."""
+    the dense single-pass kernel applies (depth <= 6); results are identical.
+    ``traverse_only``: the traversal alone (no product; C is None) -- the
+    multi-GPU plan.  ``keep_pruned``: the pruned calls and their norm
+    products in reference order (detail.pruned / pruned_np)."""
     _require_conformable(a, b)
     if config is None:
         config = SpammConfig()
@@ -122,7 +133,7 @@ def spamm_detailed(a, b, config=None, keep_triples=False, rows=None, traversal="
     c = ctypes.c_void_p()
     prod = ctypes.c_void_p()
     st = _lib.Stats()
-    flags = _flags(config, keep_triples, traversal)
+    flags = _flags(config, keep_triples, traversal, traverse_only, keep_pruned)
     if rows is None:
         _lib.check(L.spamm_multiply(a._handle, b._handle, float(config.tau), flags,
                                     ctypes.byref(c), ctypes.byref(st), ctypes.byref(prod)))
@@ -156,10 +167,17 @@ def spamm_detailed(a, b, config=None, keep_triples=False, rows=None, traversal="
             if st.n_triples:
                 _lib.check(L.spamm_product_triples(prod, trip.ctypes.data, int(st.n_triples)))
             detail.triples = trip
+        if keep_pruned:
+            m = int(L.spamm_product_pruned_count(prod))
+            detail.pruned = np.empty((m, 4), np.int32)
+            detail.pruned_np = np.empty(m, np.float64)
+            if m:
+                _lib.check(L.spamm_product_pruned(prod, detail.pruned.ctypes.data,
+                                                  detail.pruned_np.ctypes.data, m))
     finally:
         if prod.value:
             L.spamm_product_free(prod)
-    return _wrap(c.value), stats, detail
+    return (_wrap(c.value) if c.value else None), stats, detail
 
 
 def spamm(a, b, config=None):

@@ -105,3 +105,76 @@ def test_sweep_plan_partitions_every_row_of_every_multiply_once():
         if prev is not None:
             assert span <= prev + 1e-6
         prev = span
+
+
+def test_row_shard_every_rank_nonempty_when_rows_suffice():
+    """no rank gets an empty range while there are at least as
+    many block rows as ranks -- with or without (skewed) weights; with fewer
+    rows the trailing ranks get empty ranges, still covering every row once."""
+    from paper_1011_3534_b200 import distributed as spd
+
+    rng = np.random.default_rng(1)
+    for n, leaf in ((1024, 32), (5, 4), (40, 4), (64, 8)):
+        nb = spd.padded_blocks(n, leaf)
+        for world in (1, 2, 3, 4, 8):
+            for w in (None, rng.random(nb), np.r_[1.0, np.zeros(nb - 1)], np.r_[np.zeros(nb - 1), 1.0]):
+                spans = [spd.row_shard(r, world, n, leaf, w) for r in range(world)]
+                assert spans[0][0] == 0 and spans[-1][1] == nb
+                assert all(x[1] == y[0] for x, y in zip(spans, spans[1:]))
+                assert all(hi >= lo for lo, hi in spans)
+                if nb >= world:
+                    assert all(hi > lo for lo, hi in spans), (n, leaf, world, spans)
+
+
+def _budget_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle
+        from paper_1011_3534_b200 import distributed as spd
+        from paper_1011_3534_b200 import workloads
+
+        a, _, leaf, taus = workloads.make_config("c2")
+        pa = oracle.pad(a, leaf)
+        N = pa.shape[0]
+        depth = oracle.depth_for(N, leaf)
+        na, oa = oracle.build_pyramid(pa, leaf)
+        comm = spd.Comm()
+        lo, hi = spd.row_shard(rank, world, a.shape[0], leaf)
+        st, _, boxes, tiers = oracle.cull(na, oa, na, oa, depth, N, taus[2], rows=(lo, hi))
+        # this rank's pruned calls as (tier, i, j, k) + norm product, gathered
+        tijk = np.stack([boxes[:, 4], boxes[:, 0] // boxes[:, 3], boxes[:, 1] // boxes[:, 3],
+                         boxes[:, 2] // boxes[:, 3]], axis=1) if len(boxes) else np.zeros((0, 4))
+        parts_t = comm.all_gather_var(torch.from_numpy(np.ascontiguousarray(tijk, np.int64)))
+        parts_v = comm.all_gather_var(torch.from_numpy(np.ascontiguousarray(tiers["box_np"])))
+        tij, _, budget = spd.merge_pruned([(x.numpy(), y.numpy()) for x, y in zip(parts_t, parts_v)])
+        bands = comm.bands(lo, hi)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "merged.npy"), tij)
+            np.save(os.path.join(out_dir, "budget.npy"), np.array([budget]))
+            np.save(os.path.join(out_dir, "bands.npy"), np.array(bands))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_budget_is_bit_identical(tmp_path, world):
+    """Per-rank pruned calls (each counted once, by the rank owning its first
+    row), merged by distributed.merge_pruned into tier-major Morton order and
+    pairwise-summed per tier, reproduce the single-process budget bit for bit
+    and the boxes in reference order (c2 at tau = 1e-8, gloo)."""
+    from oracle import oracle
+    from paper_1011_3534_b200 import workloads
+
+    port = _free_port()
+    mp.start_processes(_budget_worker, args=(world, port, str(tmp_path)), nprocs=world,
+                       start_method="spawn")
+    a, _, leaf, taus = workloads.make_config("c2")
+    ref = oracle.spamm(a, a, leaf, taus[2])
+    budget = float(np.load(tmp_path / "budget.npy")[0])
+    assert budget == ref["stats"]["omitted_budget"]
+    b = ref["boxes"]
+    want = np.stack([b[:, 4], b[:, 0] // b[:, 3], b[:, 1] // b[:, 3], b[:, 2] // b[:, 3]], axis=1)
+    assert np.array_equal(np.load(tmp_path / "merged.npy"), want)
+    bands = np.load(tmp_path / "bands.npy")
+    assert bands[0][0] == 0 and bands[-1][1] == 64

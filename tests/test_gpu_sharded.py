@@ -45,29 +45,3 @@ def test_row_shards_partition_the_product(world):
     assert abs(budget - full_st.omitted_budget) <= 1e-12 * full_st.omitted_budget
     assert nbox == len(full_st.boxes)
     assert np.array_equal(np.concatenate(trips), full_det.triples)
-
-
-def test_spamm_sharded_world1_nccl():
-    import torch
-    import torch.distributed as dist
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)
-    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-    try:
-        a_d = workloads.exponential_decay(1024, 0.9, 0)
-        b_d = workloads.exponential_decay(1024, 0.9, 1)
-        a, b = sp.from_dense(a_d, leaf_size=32), sp.from_dense(b_d, leaf_size=32)
-        c, st, _ = spd.spamm_sharded(a, b, sp.SpammConfig(tau=1e-6))
-        ref_c, ref_st = sp.spamm(a, b, sp.SpammConfig(tau=1e-6))
-        assert c.structurally_equal(ref_c)
-        assert st["leaf_matmuls"] == ref_st.leaf_matmuls == 2400
-        assert st["omitted_budget"] == ref_st.omitted_budget
-        band = torch.from_numpy(np.array(a._padded)).cuda()
-        again = spd.allgather_tree(band, 1024, 32)
-        assert again.structurally_equal(a)
-    finally:
-        dist.destroy_process_group()
