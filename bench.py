@@ -51,6 +51,12 @@ WORKLOAD_DESC = {
 METRIC = "SpAMM time & retained-leaf FP64 TFLOP/s vs tau, n=4096-65536, 1/2/4/8 B200"
 
 
+def workload_string(cfg_name, n, leaf, taus):
+    """config.workload -- the same string on the B200 arm and the reference arm."""
+    return (f"{cfg_name}: n={n} leaf={leaf} {WORKLOAD_DESC.get(cfg_name, '')}, "
+            f"tau sweep {list(taus)}, one spamm per tau per step")
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -65,6 +71,8 @@ def parse():
                    help="storage/compute precision (c5's FP32 variant: f32)")
     p.add_argument("--dist", action="store_true",
                    help="use the torch.distributed (NCCL) path even at world size 1")
+    p.add_argument("--no-extra", action="store_true",
+                   help="skip the per-config lines and the same-run FP64 peak")
     return p.parse_args()
 
 
@@ -179,7 +187,7 @@ def run_reference(args, cfg_name):
         "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": sec_per_step * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))",
-        "config": {"workload": f"{cfg_name}: n={a.shape[0]} leaf={leaf} taus={list(taus)}",
+        "config": {"workload": workload_string(cfg_name, a.shape[0], leaf, taus),
                    "l2": "n/a (CPU)"},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                          "sample": f"full {cfg_name} tau sweep per step"},
@@ -215,6 +223,73 @@ def k3_traffic():
         with open(path) as fh:
             return json.load(fh)
     return None
+
+
+def fp64_peak_same_run():
+    """The FP64 DMMA / DFMA microbenchmark (tools/fp64_peaks.cu, built by
+    __graft_entry__.build()) run inside this bench run: the roofline
+    denominator measured on this box, now."""
+    exe = os.path.join(ROOT, "tools", "bin", "fp64_peaks")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = json.loads(subprocess.check_output([exe], timeout=120).decode())
+    except Exception:
+        return None
+    dmma = max(v for k, v in out.items() if k.startswith("dmma_") and k.endswith("_tflops"))
+    return {"dmma_tflops": dmma, "dfma_tflops": out.get("dfma_tflops"),
+            "ffma_tflops": out.get("ffma_tflops"), "source": "tools/bin/fp64_peaks, this run"}
+
+
+def measure_config(sp, cfg_name, dtype, flush, steps=3, warmup=1):
+    """One BASELINE config device-timed exactly like `value` (L2 flushed,
+    CUDA events on the library's stream around every multiply): retained-leaf
+    TFLOP/s and the leaf-product kernel's roofline fraction."""
+    import torch
+
+    from paper_1011_3534_b200 import workloads
+
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    if cfg_name in workloads.DEVICE_CONFIGS:
+        at, _, leaf, taus = workloads.make_config_device(cfg_name, "cuda", tdt)
+        n = at.shape[0]
+        a = sp.from_device_pointer(at.data_ptr(), n, leaf_size=leaf,
+                                   dtype=np.float32 if dtype == "f32" else np.float64)
+        del at
+        torch.cuda.empty_cache()
+        b = a
+    else:
+        ah, bh, leaf, taus = workloads.make_config(cfg_name)
+        n = ah.shape[0]
+        npdt = np.float32 if dtype == "f32" else np.float64
+        a = sp.from_dense(ah, leaf_size=leaf, dtype=npdt)
+        b = a if bh is ah else sp.from_dense(bh, leaf_size=leaf, dtype=npdt)
+    f = ms = gemm = 0.0
+    per_tau = {}
+    for step in range(warmup + steps):
+        for tau in taus:
+            flush.zero_()
+            torch.cuda.synchronize()
+            c, st, det = sp.spamm_detailed(a, b, sp.SpammConfig(tau=tau))
+            del c
+            if step >= warmup:
+                f += leaf_flops(leaf, st.leaf_matmuls)
+                ms += det.ms_total
+                gemm += det.ms_gemm
+                per_tau[tau] = (st.leaf_matmuls, det.ms_total)
+    del a, b
+    torch.cuda.empty_cache()
+    f64_tensor = dtype == "f64" and leaf >= 32
+    peak, _ = fp64_peak() if f64_tensor else fp32_peak()
+    k3 = f / (gemm * 1e-3) / 1e12 if gemm > 0 else 0.0
+    return {"workload": workload_string(cfg_name, n, leaf, taus), "dtype": dtype,
+            "value": f / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "ms_per_multiply": ms / (steps * len(taus)),
+            "per_tau": [{"tau": t, "retained": r, "ms": m} for t, (r, m) in per_tau.items()],
+            "roofline": {"kernel": "K3", "achieved": k3, "peak": peak,
+                         "bound": "tensor" if f64_tensor else "fma", "frac": k3 / peak},
+            "timing": "CUDA events per multiply, L2 flushed, inputs resident; "
+                      f"{steps} steps after {warmup} warm-up"}
 
 
 def run_b200(args, cfg_name):
@@ -345,8 +420,7 @@ def run_b200(args, cfg_name):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
         "data": ("synthetic, generated on the GPU (torch Philox stream, the recipe's formula)"
                  if dev_cfg else "synthetic (seeded numpy PCG64, SURVEY §8(d))"),
-        "config": {"workload": f"{cfg_name}: n={n} leaf={leaf} {WORKLOAD_DESC.get(cfg_name, '')}, "
-                               f"tau sweep {list(taus)}, one spamm per tau per step",
+        "config": {"workload": workload_string(cfg_name, n, leaf, taus),
                    "l2": "flushed (256 MiB write) before every multiply",
                    "parallelism": (f"tau sweep partitioned over {world} ranks: each tau whole or "
                                    f"split into C block-row shards (no data-path collective)"
@@ -382,6 +456,21 @@ def run_b200(args, cfg_name):
             "ms": 2.0 * n ** 3 / (rate * 1e12) * 1e3, "tflops": rate,
             "note": "estimated from the measured cuBLAS DGEMM 8192^3 rate"}
 
+    if rank == 0 and world == 1 and not args.profile and not args.no_extra:
+        same = fp64_peak_same_run()
+        if same is not None:
+            roofline["peak_same_run"] = same
+            if f64_tensor:
+                roofline["frac_same_run"] = achieved / same["dmma_tflops"]
+        if cfg_name == "c2":
+            # the rest of the metric's n range, device-timed like `value`
+            # (parity for each: tests/test_gpu_parity.py, tests/test_gpu_fullsize.py)
+            line["config"]["per_config"] = [
+                measure_config(sp, "c3_l2", "f64", flush),
+                measure_config(sp, "c5", "f64", flush),
+                measure_config(sp, "c5", "f32", flush),
+            ]
+
     if not args.no_e2e and not args.profile:
         if dev_cfg:
             line["e2e"] = {"unavailable": "inputs generated on the GPU: host staging of a "
@@ -392,6 +481,11 @@ def run_b200(args, cfg_name):
         else:
             with NumaLocal(local):
                 line["e2e"] = e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host)
+                if not use_dist:
+                    # beside it: every product read back dense, as a reference
+                    # caller does with to_dense(C) (quadtree.py:264-266)
+                    line["e2e"]["to_dense"] = e2e_leg(args, sp, a_host, leaf, taus, shard,
+                                                      use_dist, b_host, readback="dense")
 
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile and not dev_cfg:
         cv, sec, cores = cpu_reference(a_host, leaf, taus, 1, 1, b_host)
@@ -437,12 +531,14 @@ class NumaLocal:
                 pass
 
 
-def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
+def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None, readback="blocks"):
     """The same metric through the public API with host buffers.
 
     Every step: pinned host A (and B) -> from_dense (H2D + K1 pyramid), one
-    spamm per tau, and each product back to pinned host memory as its nonzero
-    leaf blocks and norm pyramid.  With row shards each rank multiplies its C
+    spamm per tau, and each product back to pinned host memory -- as its
+    nonzero leaf blocks and norm pyramid (readback="blocks"), or as the dense
+    n x n matrix through to_dense (readback="dense", what a caller of the
+    reference's API reads).  With row shards each rank multiplies its C
     block rows and reads back only those (bands partition C); wall time is
     the max over ranks."""
     import torch
@@ -476,7 +572,10 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
     # one pinned buffer per tau: a product's copy overlaps the next multiply
     # (and the next step's host->device copy of A: PCIe is full duplex); a
     # buffer is reused only after its previous transfer has been waited for
-    pin_blk = [torch.empty((G, leaf, leaf), dtype=tdt, pin_memory=True).numpy() for _ in taus]
+    if readback == "dense":
+        pin_blk = [torch.empty((n, n), dtype=tdt, pin_memory=True).numpy() for _ in taus]
+    else:
+        pin_blk = [torch.empty((G, leaf, leaf), dtype=tdt, pin_memory=True).numpy() for _ in taus]
     pending = [None] * len(taus)
     t0 = None
     e_f = 0.0
@@ -504,11 +603,15 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
                 c, st = sp.spamm(at, bt, sp.SpammConfig(tau=tau))
             else:
                 c, st, _ = sp.spamm_detailed(at, bt, sp.SpammConfig(tau=tau), rows=shard)
-            if pending[q] is not None:
-                pending[q].wait()
-            pending[q] = c.nonzero_blocks(out=pin_blk[q], wait=False)
-            d2h += (pending[q].blocks.nbytes + pending[q].ids.nbytes + c._pyramid()[2].nbytes
-                    + c._pyramid()[3].nbytes)
+            if readback == "dense":
+                sp.to_dense(c, out=pin_blk[q])
+                d2h += pin_blk[q].nbytes
+            else:
+                if pending[q] is not None:
+                    pending[q].wait()
+                pending[q] = c.nonzero_blocks(out=pin_blk[q], wait=False)
+                d2h += (pending[q].blocks.nbytes + pending[q].ids.nbytes + c._pyramid()[2].nbytes
+                        + c._pyramid()[3].nbytes)
             f += leaf_flops(leaf, st.leaf_matmuls)
             del c
         del at, bt
@@ -518,7 +621,8 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
             print(f"[e2e] step {it} t={(time.perf_counter() - (t0 or 0)) * 1e3:.3f} ms",
                   file=sys.stderr, flush=True)
     for p in pending:
-        p.wait()
+        if p is not None:
+            p.wait()
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     d2h = d2h // max(args.steps, 1)
@@ -532,9 +636,11 @@ def e2e_leg(args, sp, a_host, leaf, taus, shard, use_dist, b_host=None):
             "h2d_bytes_per_step": n * n * esz * (1 if same else 2) * (dist_world() if use_dist else 1),
             "d2h_bytes_per_step": d2h,
             "ms_per_step": el / args.steps * 1e3,
-            "result": "each product read back as its nonzero leaf blocks + norm pyramid "
-                      "(QuadTreeMatrix.nonzero_blocks, copy-out stream overlapping the next "
-                      "call; all copies waited for inside the timed region)",
+            "result": ("each product read back dense through to_dense(C, out=pinned) "
+                       "(materialised on the device, one n x n copy)" if readback == "dense" else
+                       "each product read back as its nonzero leaf blocks + norm pyramid "
+                       "(QuadTreeMatrix.nonzero_blocks, copy-out stream overlapping the next "
+                       "call; all copies waited for inside the timed region)"),
             "pipelining": "from_dense(wait=False): step s+1's host->device copy of A runs on the "
                           "copy-in stream during step s's multiplies (PCIe full duplex with the "
                           "read-backs); no copy crosses the timed region's boundaries",
