@@ -186,7 +186,7 @@ extern "C" int spamm_boxes_morton_order(const int64_t *boxes, int64_t count, int
   const size_t bytes_kv = (size_t)count * 8;
   const size_t bytes_hist = (size_t)ntiles * 256 * sizeof(unsigned);
   char *mem = nullptr;
-  SPAMM_CUDA_TRY(cudaMallocAsync((void **)&mem, bytes_boxes + 4 * bytes_kv + bytes_hist, st));
+  SPAMM_CUDA_TRY(dev_alloc((void **)&mem, bytes_boxes + 4 * bytes_kv + bytes_hist, st));
   int64_t *d_boxes = (int64_t *)mem;
   uint64_t *keys[2] = {(uint64_t *)(mem + bytes_boxes), (uint64_t *)(mem + bytes_boxes + bytes_kv)};
   int64_t *vals[2] = {(int64_t *)(mem + bytes_boxes + 2 * bytes_kv),

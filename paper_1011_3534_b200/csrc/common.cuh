@@ -127,6 +127,10 @@ int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed = 
 // copy engine and so queues behind device->host copies in flight (an async
 // product read-back would otherwise stall the next multiply).
 int zero_async(void *p, size_t bytes, cudaStream_t st, int ctas);
+// cudaMallocAsync, plus (debug: SPAMM_POISON=<byte>) the new memory filled with
+// that byte, so a read of memory nothing initialised shows up as NaN / set
+// occupancy / huge counts instead of the zeros a fresh allocation often holds.
+cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t st);
 
 // Small device->host reads (statistics, root norms, pyramids) without the
 // copy engines: a kernel stores the bytes into pinned host memory, then the

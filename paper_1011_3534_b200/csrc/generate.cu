@@ -84,7 +84,7 @@ static int generate(int mode, const double *t0, const double *t1, int64_t n, int
   double *tab = nullptr;
   int rc = SPAMM_OK;
   do {
-    cudaError_t e = cudaMallocAsync((void **)&tab, tbytes, st);
+    cudaError_t e = dev_alloc((void **)&tab, tbytes, st);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(tab, t0, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess && mode == 1 && n > 1)

@@ -452,8 +452,9 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
     for (int x = 0; x < C::NACC; ++x) acc[x] = 0.0;
     uint32_t pending = 0;
     bool top_dirty = false;
+    const int tm_slots = args.tm_slots < C::TM_SLOTS ? args.tm_slots : C::TM_SLOTS;
     auto spill = [&](int slot) {
-      if (slot < C::TM_SLOTS) {
+      if (slot < tm_slots) {
         uint32_t r[C::NREG];
 #pragma unroll
         for (int x = 0; x < C::NACC; ++x) {
@@ -461,13 +462,14 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
           r[2 * x + 1] = (uint32_t)__double2hiint(top[x]);
         }
         tmem_store<C::NREG>(t_my + slot * C::SLOT_COLS, r);
+        if (args.tm_sync) asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       } else {
 #pragma unroll
         for (int x = 0; x < C::NACC; ++x) stk[slot][x] = top[x];
       }
     };
     auto reload = [&](int slot) {
-      if (slot < C::TM_SLOTS) {
+      if (slot < tm_slots) {
         uint32_t r[C::NREG];
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         tmem_load<C::NREG>(t_my + slot * C::SLOT_COLS, r);
@@ -631,6 +633,10 @@ static bool make_b_map5(CUtensorMap *map, const void *base, int64_t N) {
 template <int TILE, int CW = 16, int WMv = 4, int ST = 0>
 static int launch_dmma_ws(LeafArgs args, int num_sms, cudaStream_t st) {
   using C = WsCfg<TILE, CW, WMv, ST>;
+  static const int tm_env = getenv("SPAMM_K3_TM_SLOTS") ? atoi(getenv("SPAMM_K3_TM_SLOTS")) : C::TM_SLOTS;
+  static const int tm_sync = getenv("SPAMM_K3_TM_SYNC") != nullptr;
+  args.tm_slots = tm_env;
+  args.tm_sync = tm_sync;
   CUtensorMap ma, mb;
   SPAMM_TRY(make_operand_map(&ma, args.a, args.N, 2, TILE));             // A: 32 k x TILE rows
   args.b_map5 = TILE == 64 && make_b_map5(&mb, args.b, args.N);

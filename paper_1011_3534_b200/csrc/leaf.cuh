@@ -21,6 +21,8 @@ struct LeafArgs {
   unsigned *grp_done;                 // optional: per-group count of finished warp tiles
   const uint32_t *order;              // optional: work order over the groups (longest first)
   int pdl;                            // launch as a programmatic dependent of the previous kernel
+  int tm_slots;                       // merge-stack slots kept in TMEM (the rest in local memory)
+  int tm_sync;                        // wait for each TMEM spill to complete (debug)
 };
 
 // Returns through *signals whether the launched kernel reports finished groups

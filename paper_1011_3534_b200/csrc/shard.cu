@@ -217,9 +217,9 @@ static int alloc_norms_only(DeviceContext *ctx, const spamm_tree *like, spamm_tr
   t->dtype = like->dtype;
   t->device = like->device;
   const size_t P = (size_t)pyramid_size(t->depth);
-  cudaError_t e = cudaMallocAsync((void **)&t->nsq, sizeof(double) * P, ctx->stream);
-  if (e == cudaSuccess) e = cudaMallocAsync((void **)&t->occ, P, ctx->stream);
-  if (e == cudaSuccess) e = cudaMallocAsync((void **)&t->nrm, sizeof(double) * P, ctx->stream);
+  cudaError_t e = dev_alloc((void **)&t->nsq, sizeof(double) * P, ctx->stream);
+  if (e == cudaSuccess) e = dev_alloc((void **)&t->occ, P, ctx->stream);
+  if (e == cudaSuccess) e = dev_alloc((void **)&t->nrm, sizeof(double) * P, ctx->stream);
   if (e != cudaSuccess) {
     free_tree_async(t, ctx->stream);
     set_error("allocation: %s", cudaGetErrorString(e));

@@ -137,13 +137,20 @@ int read_small_sync(DeviceContext *ctx, cudaStream_t st, const SmallRead *r, int
   return SPAMM_OK;
 }
 
+cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t st) {
+  static const int poison = getenv("SPAMM_POISON") ? (int)strtol(getenv("SPAMM_POISON"), nullptr, 0) : -1;
+  cudaError_t e = cudaMallocAsync(p, bytes, st);
+  if (e == cudaSuccess && poison >= 0 && bytes) e = cudaMemsetAsync(*p, poison & 0xff, bytes, st);
+  return e;
+}
+
 int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed) {
   if (s.bytes >= bytes) return SPAMM_OK;
   if (s.ptr) SPAMM_CUDA_TRY(cudaFreeAsync(s.ptr, stream));
   s.ptr = nullptr;
   s.bytes = 0;
   size_t want = bytes + bytes / 4 + 256;
-  SPAMM_CUDA_TRY(cudaMallocAsync(&s.ptr, want, stream));
+  SPAMM_CUDA_TRY(dev_alloc((void **)&s.ptr, want, stream));
   s.bytes = want;
   if (zeroed) SPAMM_TRY(zero_async(s.ptr, want, stream, 1024));
   return SPAMM_OK;
@@ -989,11 +996,11 @@ int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm
   t->dtype = dtype;
   t->device = ctx->device;
   const int64_t esz = t->elem_size();
-  SPAMM_CUDA_TRY(cudaMallocAsync(&t->padded, (size_t)(t->N * t->N * esz), st));
-  SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->nsq, sizeof(double) * pyramid_size(t->depth),
+  SPAMM_CUDA_TRY(dev_alloc((void **)&t->padded, (size_t)(t->N * t->N * esz), st));
+  SPAMM_CUDA_TRY(dev_alloc((void **)&t->nsq, sizeof(double) * pyramid_size(t->depth),
                                  st));
-  SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->occ, pyramid_size(t->depth), st));
-  SPAMM_CUDA_TRY(cudaMallocAsync((void **)&t->nrm, sizeof(double) * pyramid_size(t->depth),
+  SPAMM_CUDA_TRY(dev_alloc((void **)&t->occ, pyramid_size(t->depth), st));
+  SPAMM_CUDA_TRY(dev_alloc((void **)&t->nrm, sizeof(double) * pyramid_size(t->depth),
                                  st));
   *out = t.release();
   return SPAMM_OK;
@@ -1319,9 +1326,9 @@ int spamm_tree_recompute_norms(const spamm_tree *t, double *nsq_host) {
   view.nrm = nullptr;
   const int64_t P = pyramid_size(t->depth);
   int rc = SPAMM_OK;
-  cudaError_t e = cudaMallocAsync((void **)&view.nsq, sizeof(double) * P, ctx->stream);
-  if (e == cudaSuccess) e = cudaMallocAsync((void **)&view.occ, P, ctx->stream);
-  if (e == cudaSuccess) e = cudaMallocAsync((void **)&view.nrm, sizeof(double) * P, ctx->stream);
+  cudaError_t e = dev_alloc((void **)&view.nsq, sizeof(double) * P, ctx->stream);
+  if (e == cudaSuccess) e = dev_alloc((void **)&view.occ, P, ctx->stream);
+  if (e == cudaSuccess) e = dev_alloc((void **)&view.nrm, sizeof(double) * P, ctx->stream);
   if (e == cudaSuccess) {
     rc = build_pyramid_async(ctx, &view, ctx->stream, nullptr, nullptr, nullptr, 0, nullptr, 0,
                              nullptr, nullptr);

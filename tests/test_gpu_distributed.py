@@ -26,7 +26,40 @@ def _free_port():
     return port
 
 
-def _check_multiply(spd, sp, comm, a_full, b_full, leaf, tau, out, tag):
+def _reference(tmp_path):
+    """The single-GPU results the ranks are compared with, computed once here
+    (not in every rank process) and handed to the workers through a file."""
+    import pickle
+
+    import paper_1011_3534_b200 as sp
+    from paper_1011_3534_b200 import purification as P
+    from paper_1011_3534_b200 import workloads
+
+    ref = {}
+    for tag, name, tau_i in (("c1", "c1", 0), ("c2", "c2", 2)):
+        a, b, leaf, taus = workloads.make_config(name)
+        a1 = sp.from_dense(a, leaf_size=leaf)
+        b1 = a1 if name == "c2" else sp.from_dense(b, leaf_size=leaf)
+        cfg = sp.SpammConfig(tau=taus[tau_i], collect_boxes=True)
+        c1, st1 = sp.spamm(a1, b1, cfg)
+        ref[tag] = dict(c=c1._padded.copy(), pyr=c1._pyramid()[2].copy(), occ=c1._pyramid()[3].copy(),
+                        a_pyr=a1._pyramid()[2].copy(), norm=c1.norm(),
+                        stats={k: getattr(st1, k) for k in
+                               ("leaf_matmuls", "pruned_calls", "pruned_volume", "empty_skip_volume",
+                                "max_depth_reached", "omitted_budget")},
+                        boxes=st1.boxes)
+    h = workloads.cubic_lattice_hamiltonian(16)
+    r = P.purify(sp.from_dense(h, leaf_size=64), h.shape[0] // 2, P.SpammMode(1e-7), max_iter=12,
+                 reference_energy=0.0)
+    ref["purify"] = dict(density=r.density._padded.copy(), traces=r.trace_history,
+                         counts=r.step_leaf_matmuls, energy=r.energy)
+    path = tmp_path / "ref.pkl"
+    with open(path, "wb") as fh:
+        pickle.dump(ref, fh)
+    return str(path)
+
+
+def _check_multiply(spd, sp, comm, a_full, b_full, leaf, tau, ref, out, tag):
     import torch
 
     n = a_full.shape[0]
@@ -36,29 +69,25 @@ def _check_multiply(spd, sp, comm, a_full, b_full, leaf, tau, out, tag):
     B = A if b_full is a_full else spd.ShardedTree.scatter(bt, n, leaf, comm)
     cfg = sp.SpammConfig(tau=tau, collect_boxes=True)
     C, st, det = spd.spamm_sharded(A, B, cfg)
-    # the single-GPU product on the same inputs (every rank computes it)
-    a1 = sp.from_dense(a_full, leaf_size=leaf)
-    b1 = a1 if b_full is a_full else sp.from_dense(b_full, leaf_size=leaf)
-    c1, st1 = sp.spamm(a1, b1, cfg)
     got = C.gather_padded().cpu().numpy()
+    u = np.uint64 if got.dtype == np.float64 else np.uint32
     ok = dict(
-        c=np.array_equal(got.view(np.uint64 if got.dtype == np.float64 else np.uint32),
-                         c1._padded.view(np.uint64 if got.dtype == np.float64 else np.uint32)),
-        pyramid=np.array_equal(C.tree._pyramid()[2].view(np.uint64), c1._pyramid()[2].view(np.uint64))
-        and np.array_equal(C.tree._pyramid()[3], c1._pyramid()[3]),
-        a_pyramid=np.array_equal(A.tree._pyramid()[2].view(np.uint64), a1._pyramid()[2].view(np.uint64)),
-        stats=all(getattr(st, k) == getattr(st1, k) for k in
+        c=np.array_equal(got.view(u), ref["c"].view(u)),
+        pyramid=np.array_equal(C.tree._pyramid()[2].view(np.uint64), ref["pyr"].view(np.uint64))
+        and np.array_equal(C.tree._pyramid()[3], ref["occ"]),
+        a_pyramid=np.array_equal(A.tree._pyramid()[2].view(np.uint64), ref["a_pyr"].view(np.uint64)),
+        stats=all(getattr(st, k) == ref["stats"][k] for k in
                   ("leaf_matmuls", "pruned_calls", "pruned_volume", "empty_skip_volume",
                    "max_depth_reached")),
-        budget=st.omitted_budget == st1.omitted_budget,
-        boxes=st.boxes == st1.boxes,
-        norm=C.norm() == c1.norm(),
+        budget=st.omitted_budget == ref["stats"]["omitted_budget"],
+        boxes=st.boxes == ref["boxes"],
+        norm=C.norm() == ref["norm"],
         halo=det.halo_bytes if det is not None else 0,
     )
     out[tag] = ok
 
 
-def _check_purify(spd, sp, comm, L, tau, sweeps, out):
+def _check_purify(spd, sp, comm, L, tau, sweeps, ref, out):
     import torch
 
     from paper_1011_3534_b200 import purification as P
@@ -68,18 +97,19 @@ def _check_purify(spd, sp, comm, L, tau, sweeps, out):
     n = h.shape[0]
     F = spd.ShardedTree.scatter(torch.from_numpy(h).cuda() if comm.rank == 0 else None, n, 64, comm)
     res = spd.purify_sharded(F, n // 2, P.SpammMode(tau), max_iter=sweeps, reference_energy=0.0)
-    ref = P.purify(sp.from_dense(h, leaf_size=64), n // 2, P.SpammMode(tau), max_iter=sweeps,
-                   reference_energy=0.0)
     got = res.density.gather_padded().cpu().numpy()
     out["purify"] = dict(
-        density=np.array_equal(got.view(np.uint64), ref.density._padded.view(np.uint64)),
-        traces=res.trace_history == ref.trace_history,
-        counts=res.step_leaf_matmuls == ref.step_leaf_matmuls,
-        energy=res.energy == ref.energy,
+        density=np.array_equal(got.view(np.uint64), ref["density"].view(np.uint64)),
+        traces=res.trace_history == ref["traces"],
+        counts=res.step_leaf_matmuls == ref["counts"],
+        energy=res.energy == ref["energy"],
     )
+    # diagnostics (not asserted): first sweep whose trace differs
+    diff = [q for q, (u, v) in enumerate(zip(res.trace_history, ref["traces"])) if u != v]
+    out["purify_diag"] = dict(first_trace_diff=diff[:1])
 
 
-def _worker(rank, world, port, out_dir, backend):
+def _worker(rank, world, port, out_dir, backend, ref_path):
     import pickle
 
     import torch
@@ -96,12 +126,14 @@ def _worker(rank, world, port, out_dir, backend):
 
         sp.set_device(0)
         comm = spd.Comm()
+        with open(ref_path, "rb") as fh:
+            ref = pickle.load(fh)
         out = {}
         a, b, leaf, taus = workloads.make_config("c1")             # A != B, leaf 32
-        _check_multiply(spd, sp, comm, a, b, leaf, taus[0], out, "c1")
+        _check_multiply(spd, sp, comm, a, b, leaf, taus[0], ref["c1"], out, "c1")
         a, _, leaf, taus = workloads.make_config("c2")             # B = A, leaf 64
-        _check_multiply(spd, sp, comm, a, a, leaf, taus[2], out, "c2")
-        _check_purify(spd, sp, comm, 16, 1e-7, 12, out)            # 16^3 lattice, n = 4096
+        _check_multiply(spd, sp, comm, a, a, leaf, taus[2], ref["c2"], out, "c2")
+        _check_purify(spd, sp, comm, 16, 1e-7, 12, ref["purify"], out)  # 16^3 lattice, n = 4096
         with open(os.path.join(out_dir, f"r{rank}.pkl"), "wb") as fh:
             pickle.dump(out, fh)
     finally:
@@ -113,8 +145,9 @@ def _run(world, backend, tmp_path):
 
     import torch.multiprocessing as mp
 
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), backend), nprocs=world,
-                       start_method="spawn")
+    ref_path = _reference(tmp_path)
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), backend, ref_path),
+                       nprocs=world, start_method="spawn")
     outs = []
     for r in range(world):
         with open(tmp_path / f"r{r}.pkl", "rb") as fh:
@@ -126,7 +159,7 @@ def _run(world, backend, tmp_path):
             assert all(o.values()), (r, tag, o)
             if world > 1:
                 assert halo > 0, (r, tag, "no operand blocks were fetched")
-        assert all(out["purify"].values()), (r, out["purify"])
+        assert all(out["purify"].values()), (r, out["purify"], out.get("purify_diag"))
 
 
 def test_distributed_world1_nccl(tmp_path):
