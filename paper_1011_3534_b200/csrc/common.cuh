@@ -110,6 +110,7 @@ struct DeviceContext {
   int counter_parity = 0; // which traversal counter set the next call uses
   bool last_overlapped = false;  // the last product's C tree overlapped K3
   bool last_k3_pdl = false;      // the last product's K3 followed the traversal programmatically
+  bool last_bitmask = false;     // the last traversal published bitmask groups (no ks lists)
   Scratch grp_done;       // per-group finished-tile counters (zero at rest)
   Scratch lpt_order;      // groups by decreasing size (K3's work order)
   Scratch pw_part;        // budget: per-tier partial sums of the split recursion

@@ -306,6 +306,30 @@ __device__ __forceinline__ void tmem_load<64>(uint32_t taddr, uint32_t (&r)[64])
 #undef R4
 #undef W4
 
+// Bitmask groups: the inner indices k of C block (i, j)'s retained triples
+// as a bit set, read from the dense traversal's retained leaf-triple bitmask
+// (bit x = Morton code spread3(i) << 2 | spread3(j) << 1 | spread3(k)).  Four
+// k per 32-bit word (k's two low bits sit at x bits 0 and 3); nb <= 64.
+__device__ __noinline__ uint64_t retained_kmask(const uint32_t *__restrict__ am, uint32_t i,
+                                                   uint32_t j, int nb) {
+  const uint32_t base = (spread3(i) << 2) | (spread3(j) << 1);
+  uint64_t m = 0;
+  if (nb >= 4) {
+#pragma unroll 4
+    for (int q = 0; q < 16; ++q) {
+      const uint32_t x0 = base | spread3((uint32_t)(4 * q));
+      const uint32_t w = 4 * q < nb ? __ldcg(am + (x0 >> 5)) >> (x0 & 31) : 0u;
+      m |= ((uint64_t)(w & 3u) | ((uint64_t)((w >> 8) & 3u) << 2)) << (4 * q);
+    }
+  } else {
+    for (int k = 0; k < nb; ++k) {
+      const uint32_t x = base | spread3((uint32_t)k);
+      m |= (uint64_t)((__ldcg(am + (x >> 5)) >> (x & 31)) & 1u) << k;
+    }
+  }
+  return m;
+}
+
 template <int TILE, int CW = 16, int WMv = 4, int ST = 0>
 __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
     leaf_dmma_ws_kernel(LeafArgs args, const __grid_constant__ CUtensorMap tmA,
@@ -350,8 +374,19 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
       asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmB) : "memory");
       // launched as a programmatic dependent of the traversal: its outputs
       // (group lists, counts) are complete and visible after this (a no-op
-      // for a plain launch)
-      asm volatile("griddepcontrol.wait;\n" ::: "memory");
+      // for a plain launch).  Bitmask groups: the traversal publishes the
+      // group list before its record / budget CTAs finish; start on that.
+      if (args.am) {
+        const unsigned *rdy = &args.tc->groups_ready;
+        for (;;) {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(rdy) : "memory");
+          if (v) break;
+          __nanosleep(32);
+        }
+      } else {
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+      }
       // the traversal is complete: a programmatic dependent (C's norm kernel,
       // which waits on args.grp_done) may start now and overlap this kernel.
       // Not earlier: it reads the traversal's group list and count.
@@ -361,7 +396,11 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
       atomicMax(&args.tc->k3_t0n, ~gtimer());
       unsigned long long m = *args.n_codes;
       if (m > args.capacity) m = args.capacity;
-      const int ng = args.tc->overflow ? 0 : (int)args.tc->num_groups;  // overflow: result discarded, re-run
+      // overflow: result discarded, re-run (bitmask groups never overflow:
+      // the group list holds every C block; a pruned-record overflow set
+      // later by the traversal does not concern the products)
+      const int ng = args.am ? (int)args.tc->num_groups
+                             : args.tc->overflow ? 0 : (int)args.tc->num_groups;
       const int subs = subs_side * subs_side;
       int stage = 0;
       unsigned phase = 0;
@@ -383,15 +422,28 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
         const int gi = item / subs, sub = item - gi * subs;
         const int grp = args.order ? (int)args.order[gi] : gi;
         const int si = sub / subs_side, sj = sub - si * subs_side;
-        const int64_t start = args.group_starts[grp];
-        const int64_t end = grp + 1 < ng ? args.group_starts[grp + 1] : (int64_t)m;
         const uint32_t gid = args.group_ids[grp];
         const int64_t ci = gid / (uint64_t)args.nb, cj = gid - ci * args.nb;
         const int arow0 = (int)(ci * b + si * TILE), bcol16 = (int)((cj * b + sj * TILE) >> 4);
         const int64_t c_off = (int64_t)arow0 * N + cj * b + sj * TILE;
-        uint32_t k = args.ks[start];
-        for (int64_t s = start; s < end; ++s) {
-          const uint32_t knext = s + 1 < end ? args.ks[s + 1] : 0u;
+        // the group's inner indices, ascending: ks[start, end) or the set
+        // bits of kmask (bitmask groups)
+        int64_t s = 0, end = 0;
+        uint64_t kmask = 0;
+        uint32_t k;
+        if (args.am) {
+          kmask = retained_kmask(args.am, (uint32_t)ci, (uint32_t)cj, (int)args.nb);
+          k = (uint32_t)(__ffsll((long long)kmask) - 1);
+          kmask &= kmask - 1;
+        } else {
+          s = args.group_starts[grp];
+          end = grp + 1 < ng ? args.group_starts[grp + 1] : (int64_t)m;
+          k = args.ks[s];
+        }
+        for (;;) {
+          const bool has_next = args.am ? kmask != 0 : s + 1 < end;
+          const uint32_t knext = !has_next ? 0u
+                                 : args.am ? (uint32_t)(__ffsll((long long)kmask) - 1) : args.ks[s + 1];
           for (int kc = 0; kc < kchunks; ++kc) {
             acquire();
             double *stg = dsm + stage * C::STAGE_ELEMS;
@@ -399,7 +451,7 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
             int flags = 0, h = 31;
             if (kc == kchunks - 1) {
               flags = STG_MERGE;
-              if (s + 1 < end) h = merge_level(k, knext);
+              if (has_next) h = merge_level(k, knext);
               else flags |= STG_END;
             }
             info[stage].flags = flags;
@@ -414,7 +466,10 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
               tma_load_3d(stg + C::A_ELEMS, &tmB, 0, bcol16, kcol, &full_bar[stage]);
             advance();
           }
+          if (!has_next) break;
           k = knext;
+          if (args.am) kmask &= kmask - 1;
+          else ++s;
         }
       }
       stages_total = (unsigned)gstep;

@@ -21,6 +21,11 @@ struct LeafArgs {
   unsigned *grp_done;                 // optional: per-group count of finished warp tiles
   const uint32_t *order;              // optional: work order over the groups (longest first)
   int pdl;                            // launch as a programmatic dependent of the previous kernel
+  // bitmask groups (dense traversal): each group's k list is the set bits of
+  // the retained leaf-triple bitmask (Morton order) for its C block, and the
+  // group list is ready once tc->groups_ready is set -- no ks / group_starts
+  // and no wait for the traversal grid's completion
+  const uint32_t *am;
   int tm_slots;                       // merge-stack slots kept in TMEM (the rest in local memory)
   int tm_sync;                        // wait for each TMEM spill to complete (debug)
 };

@@ -33,7 +33,8 @@ void free_tree_async(spamm_tree *t, cudaStream_t st);
 int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap,
                         unsigned *grp_done, unsigned grp_target, const int *overflow,
-                        unsigned long long *t_end);
+                        unsigned long long *t_end,
+                        const unsigned *ready = nullptr, const unsigned *trav_done = nullptr);
 int finish_tree(DeviceContext *ctx, spamm_tree *t);
 void k1_timeline_enable(cudaStream_t st);
 void k1_timeline_dump(unsigned long long k3_end, unsigned long long k3_start);
@@ -202,6 +203,15 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
         if ((rc = ensure_scratch(ctx->lpt_order, sizeof(uint32_t) * G, st))) break;
         ta.lpt_order = (uint32_t *)ctx->lpt_order.ptr;
       }
+      // Bitmask groups (default on the dense path with the FP64 tensor-core
+      // leaf kernel): the traversal publishes only the non-empty C blocks;
+      // K3 reads each block's k list from the retained bitmask and starts on
+      // tc->groups_ready while the traversal's record and budget CTAs finish
+      // (they are off K3's critical path).  SPAMM_NO_BITMASK_GROUPS: the k
+      // lists (ks / group_starts) and a start on the traversal's completion.
+      static const bool no_bm = getenv("SPAMM_NO_BITMASK_GROUPS") != nullptr;
+      ta.bitmask_groups = !no_bm && !lpt && depth <= 6 &&
+                          (trav_only || (a->dtype == SPAMM_DTYPE_F64 && a->leaf >= 32));
     }
     static const bool tv_timeline = getenv("SPAMM_TRAVERSE_TIMELINE") != nullptr;
     static unsigned long long *tv_tl = nullptr;
@@ -222,6 +232,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       break;
     ctx->counter_parity ^= 1;
     if (dense) ctx->dense_parity ^= 1;
+    ctx->last_bitmask = ta.bitmask_groups != 0;
     ++launches;
     if (trav_only) {
       SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[4], st));
@@ -290,6 +301,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     la.order = ta.lpt_order;
     la.tc = dtc;
     la.pdl = k3_pdl;
+    la.am = ta.bitmask_groups ? ta.dn_retained : nullptr;
     static const bool want_timeline = getenv("SPAMM_GEMM_TIMELINE") != nullptr;
     if (want_timeline) {
       if ((rc = ensure_scratch(ctx->reduce_tmp, sizeof(unsigned long long) * 3 * 4096, st))) break;
@@ -318,9 +330,13 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     {
       const int tile = a->leaf < 64 ? a->leaf : 64;
       const unsigned subs = (unsigned)((a->leaf / tile) * (a->leaf / tile));
+      const bool bm = ta.bitmask_groups != 0;
       if ((rc = build_pyramid_async(ctx, c, st, &launches, ta.group_ids, &dtc->num_groups,
                                     (int64_t)gcap, overlapped ? la.grp_done : nullptr,
-                                    leaf_signals_per_tile(a->leaf) * subs, &dtc->overflow, &dtc->k1_t1)))
+                                    leaf_signals_per_tile(a->leaf) * subs,
+                                    bm ? nullptr : &dtc->overflow, &dtc->k1_t1,
+                                    bm ? &dtc->groups_ready : nullptr,
+                                    bm ? &dtc->trav_done : nullptr)))
         break;
     }
     ctx->last_overlapped = overlapped;
@@ -506,7 +522,26 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
           p->pruned.insert(p->pruned.end(), {(int32_t)t, (int32_t)i, (int32_t)j, (int32_t)k});
         }
     }
-    if ((flags & SPAMM_KEEP_TRIPLES) && m && e == cudaSuccess) {
+    if ((flags & SPAMM_KEEP_TRIPLES) && m && e == cudaSuccess && ctx->last_bitmask) {
+      // bitmask groups: each group's k list is its C block's retained bits
+      const int64_t ng = s.n_groups;
+      std::vector<uint32_t> ids(ng), am(dense_retained_words(depth));
+      e = cudaMemcpy(ids.data(), ctx->group_starts.ptr, ng * sizeof(uint32_t),
+                     cudaMemcpyDeviceToHost);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(am.data(), ctx->dn_retained.ptr, am.size() * sizeof(uint32_t),
+                       cudaMemcpyDeviceToHost);
+      p->triples.reserve(3 * m);
+      for (int64_t q = 0; q < ng && e == cudaSuccess; ++q) {
+        const uint32_t i = (uint32_t)(ids[q] / nb), j = (uint32_t)(ids[q] % nb);
+        const uint32_t base = (spread3(i) << 2) | (spread3(j) << 1);
+        for (uint32_t k = 0; k < (uint32_t)nb; ++k) {
+          const uint32_t x = base | spread3(k);
+          if ((am[x >> 5] >> (x & 31)) & 1u)
+            p->triples.insert(p->triples.end(), {(int32_t)i, (int32_t)j, (int32_t)k});
+        }
+      }
+    } else if ((flags & SPAMM_KEEP_TRIPLES) && m && e == cudaSuccess) {
       const int64_t ng = s.n_groups;
       const size_t gcap = std::min<size_t>(ctx->cull_capacity, G);
       std::vector<uint32_t> ids(ng), starts(ng), ks(m);

@@ -45,7 +45,22 @@ struct PyrTail {
   const int *overflow;
   unsigned long long *t_end;  // %globaltimer when the C tree is complete
   int pdl_wait;               // launched programmatically without grp_done: wait for the grid
+  // bitmask groups (the leaf-product kernel started on the traversal's group
+  // list, not its completion): wait for *ready before reading the list, and
+  // the last CTA waits for *trav_done (the traversal's statistics final)
+  // before the kernel may complete
+  const unsigned *ready;
+  const unsigned *trav_done;
 };
+
+__device__ __forceinline__ void spin_acquire_nonzero(const unsigned *flag) {
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v) break;
+    __nanosleep(64);
+  }
+}
 
 // Whole pyramid above the leaves in one CTA: parent = ((c11 + c12) + c21) +
 // c22 (quadtree.py:90-92), occupancy OR, nrm = rn(sqrt(nsq)) for every

@@ -32,7 +32,8 @@ void free_tree_async(spamm_tree *t, cudaStream_t st);
 int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap,
                         unsigned *grp_done, unsigned grp_target, const int *overflow,
-                        unsigned long long *t_end);
+                        unsigned long long *t_end,
+                        const unsigned *ready = nullptr, const unsigned *trav_done = nullptr);
 int finish_tree(DeviceContext *ctx, spamm_tree *t);
 
 __global__ void iota_u32_kernel(uint32_t *__restrict__ out, uint32_t base, int64_t n,

@@ -779,23 +779,6 @@ static_assert(DN_PARTS_H == 16 && DN_MAXT_H == DN_MAX_DEPTH + 1, "TraverseCounte
 constexpr int DN_PARTS = DN_PARTS_H;
 constexpr int DN_PW = 64;   // pruned-bitmask words per scan tile
 
-__host__ __device__ __forceinline__ uint32_t compact3(uint32_t x) {
-  x &= 0x09249249u;
-  x = (x ^ (x >> 2)) & 0x030c30c3u;
-  x = (x ^ (x >> 4)) & 0x0300f00fu;
-  x = (x ^ (x >> 8)) & 0xff0000ffu;
-  x = (x ^ (x >> 16)) & 0x000003ffu;
-  return x;
-}
-__host__ __device__ __forceinline__ uint32_t spread3(uint32_t x) {
-  x &= 0x3ffu;
-  x = (x | (x << 16)) & 0xff0000ffu;
-  x = (x | (x << 8)) & 0x0300f00fu;
-  x = (x | (x << 4)) & 0x030c30c3u;
-  x = (x | (x << 2)) & 0x09249249u;
-  return x;
-}
-
 __host__ __device__ constexpr uint64_t dn_words(int t) {  // bitmask words of tier t
   return ((uint64_t(1) << (3 * t)) + 31) >> 5;
 }
@@ -1035,7 +1018,21 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   // roles after the barrier: budget CTAs (one per tier), grouping CTAs, scan CTAs
   // one budget CTA per tier plus a few for the subtrees of large tiers
   const unsigned n_b = (D + 1) + 8 < nblocks / 4 ? (D + 1) + 8 : nblocks / 4;
-  const unsigned n_q = (unsigned)(LY::Q_TILES < (nblocks - n_b) / 4 ? LY::Q_TILES : (nblocks - n_b) / 4 > 0 ? (nblocks - n_b) / 4 : 1);
+  const unsigned n_q = a.bitmask_groups ? 1u
+      : (unsigned)(LY::Q_TILES < (nblocks - n_b) / 4 ? LY::Q_TILES : (nblocks - n_b) / 4 > 0 ? (nblocks - n_b) / 4 : 1);
+  // every CTA reports its exit; the last one sets tc->trav_done (release), so
+  // that a kernel which starts on tc->groups_ready can still tell when the
+  // whole traversal -- pruned records, budget, statistics -- is final
+  auto signal_exit = [&]() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&tc->exited, 1u) == nblocks - 1) {
+        __threadfence();
+        asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&tc->trav_done), "r"(1u) : "memory");
+      }
+    }
+  };
   const unsigned n_p = nblocks - n_b - n_q;
 
   if (blockIdx.x < n_p) {
@@ -1105,6 +1102,7 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
       }
     }
     if (a.timeline && threadIdx.x == 0) a.timeline[4 * blockIdx.x + 3] = globaltimer();
+    signal_exit();
     return;
   }
 
@@ -1182,6 +1180,40 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
       atomicMax(&tc->phase_ns[13], globaltimer());
       if (a.timeline) a.timeline[4 * blockIdx.x + 3] = globaltimer();
     }
+    signal_exit();
+    return;
+  }
+
+  if (a.bitmask_groups) {
+    // ---------------- phase 2Q (bitmask groups): one CTA compacts the
+    // non-empty C blocks, ascending i * nb + j; the leaf-product kernel reads
+    // each block's k list from the retained bitmask and starts as soon as
+    // this is published (the record / budget CTAs are still running)
+    unsigned long long base = 0;
+    for (uint64_t w0 = 0; w0 < LY::NE_WORDS; w0 += DN_THREADS) {
+      const uint64_t w = w0 + threadIdx.x;
+      uint32_t bits = w < LY::NE_WORDS ? __ldcg(ne + w) : 0u;
+      unsigned long long tot;
+      const unsigned long long ex =
+          block_exclusive<DN_THREADS>(pack2(0u, (unsigned)__popc(bits)), sh.warp, &tot);
+      unsigned pos = (unsigned)(base + unpack_b(ex));
+      while (bits) {
+        const int q = __ffs(bits) - 1;
+        bits &= bits - 1;
+        a.group_ids[pos++] = (uint32_t)(w * 32 + q);
+      }
+      base += unpack_b(tot);
+      __syncthreads();  // (sh.warp is reused by the next chunk's scan)
+    }
+    if (threadIdx.x == 0) {
+      tc->num_groups = (unsigned)base;
+      __threadfence();
+      asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&tc->groups_ready), "r"(1u) : "memory");
+      atomicMax(&tc->phase_ns[13], globaltimer());
+      tc->phase_ns[11] = globaltimer();
+      if (a.timeline) a.timeline[4 * blockIdx.x + 3] = globaltimer();
+    }
+    signal_exit();
     return;
   }
 
@@ -1312,6 +1344,7 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
     tc->phase_ns[11] = globaltimer();
     if (a.timeline) a.timeline[4 * blockIdx.x + 3] = globaltimer();
   }
+  signal_exit();
 }
 
 template <int D>

@@ -5,6 +5,26 @@
 namespace spamm {
 
 constexpr int MAX_TIERS = 32;
+
+// 3-bit interleave helpers of the dense traversal's Morton codes (10-bit
+// coordinates): x = spread3(i) << 2 | spread3(j) << 1 | spread3(k).
+__host__ __device__ __forceinline__ uint32_t compact3(uint32_t x) {
+  x &= 0x09249249u;
+  x = (x ^ (x >> 2)) & 0x030c30c3u;
+  x = (x ^ (x >> 4)) & 0x0300f00fu;
+  x = (x ^ (x >> 8)) & 0xff0000ffu;
+  x = (x ^ (x >> 16)) & 0x000003ffu;
+  return x;
+}
+__host__ __device__ __forceinline__ uint32_t spread3(uint32_t x) {
+  x &= 0x3ffu;
+  x = (x | (x << 16)) & 0xff0000ffu;
+  x = (x | (x << 8)) & 0x0300f00fu;
+  x = (x | (x << 4)) & 0x030c30c3u;
+  x = (x | (x << 2)) & 0x09249249u;
+  return x;
+}
+
 constexpr int DN_PARTS_H = 16, DN_MAXT_H = 8;  // dn_part dimensions
 
 // Device-resident counters of one multiply.  Two sets alternate between
@@ -38,6 +58,12 @@ struct TraverseCounters {
   unsigned lpt_hist[132];                    // dense traversal: groups per size (k count)
   unsigned pw_done[MAX_TIERS];               // budget items finished per tier
   unsigned tiers_done, pad1;                 // tiers whose budget is final
+  // dense traversal, bitmask groups: set (release) once the group list and
+  // num_groups are final -- the leaf products start on this, not on the
+  // traversal grid's completion (its pruned-record and budget CTAs run on)
+  alignas(128) unsigned groups_ready;
+  unsigned exited;                           // traversal CTAs that have finished
+  unsigned trav_done;                        // set (release) by the last one
 };
 
 struct TraverseArgs {
@@ -76,6 +102,11 @@ struct TraverseArgs {
   // while classifying -- only the C blocks that receive products get norms
   double *c_nsq_leaf, *c_nrm_leaf;
   uint8_t *c_occ_leaf;
+  // dense traversal: the groups are only the non-empty C blocks (group_ids,
+  // num_groups); each block's k list is read from the retained bitmask by
+  // the leaf-product kernel itself (no ks / group_starts), and readiness is
+  // signalled through tc->groups_ready
+  int bitmask_groups;
 };
 
 // Launch the cooperative traversal kernel (one launch per multiply).

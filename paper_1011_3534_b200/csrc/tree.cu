@@ -274,6 +274,10 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
   // may be resident before that kernel finishes; without per-group counters
   // it waits for the whole grid (and its stores) here
   if (tail.pdl_wait) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (tail.ready) {
+    if (threadIdx.x == 0) spin_acquire_nonzero(tail.ready);
+    __syncthreads();
+  }
   const int64_t n_leaves = list ? (int64_t)*list_count : nb * nb;
   const int64_t leaf0 = (int64_t)blockIdx.x * K1_LT;
   if (leaf0 < n_leaves) {
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
       }
     }
     const int shift_cpr = __ffs(chunks_per_row) - 1;
-    if (tail.grp_done && !*(volatile const int *)tail.overflow) {
+    if (tail.grp_done && (!tail.overflow || !*(volatile const int *)tail.overflow)) {
       // wait until the leaf-product kernel has stored each of this thread's leaves
 #pragma unroll
       for (int q = 0; q < MAX_SLOTS; ++q) {
@@ -489,6 +493,7 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
     }
     __syncthreads();
     if (s_last) {
+      if (tail.trav_done && threadIdx.x == 0) spin_acquire_nonzero(tail.trav_done);
       __threadfence();
       pyramid_cta(tail, k1_smem, (size_t)K1_STAGES * K1_LT * K1_LEAF_STRIDE);
       if (threadIdx.x == 0) {
@@ -545,12 +550,16 @@ __global__ void __launch_bounds__(32 * SEG_WARPS) leaf_norm_seg_kernel(
   extern __shared__ __align__(16) unsigned char seg_smem[];
   __shared__ SegInfo tbl[SEG_WARPS][64];
   if (tail.pdl_wait) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (tail.ready) {
+    if (threadIdx.x == 0) spin_acquire_nonzero(tail.ready);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned char *wsm = seg_smem + (size_t)warp * seg_warp_bytes<T, LEAF>();
   const int64_t n_leaves = list ? (int64_t)*list_count : nb * nb;
   const int64_t gw = (int64_t)blockIdx.x * SEG_WARPS + warp;
   const int64_t nw = (int64_t)gridDim.x * SEG_WARPS;
-  const bool check_flags = tail.grp_done && !*(volatile const int *)tail.overflow;
+  const bool check_flags = tail.grp_done && (!tail.overflow || !*(volatile const int *)tail.overflow);
   for (int64_t lx = gw; lx < n_leaves; lx += nw) {
     const int64_t leaf = list ? (int64_t)list[lx] : lx;
     const int64_t bi = leaf / nb, bj = leaf - bi * nb;
@@ -600,6 +609,7 @@ __global__ void __launch_bounds__(32 * SEG_WARPS) leaf_norm_seg_kernel(
     }
     __syncthreads();
     if (s_last) {
+      if (tail.trav_done && threadIdx.x == 0) spin_acquire_nonzero(tail.trav_done);
       __threadfence();
       pyramid_cta(tail, seg_smem, smem_bytes);
       if (threadIdx.x == 0) {
@@ -762,6 +772,7 @@ struct K1Overlap {
   const int *overflow;
   unsigned long long *t_end;
   bool pdl;  // programmatic dependent launch behind the leaf-product kernel
+  const unsigned *ready, *trav_done;  // bitmask groups (see PyrTail)
 };
 
 template <typename T, int S, int LT>
@@ -787,6 +798,8 @@ static int launch_staged(spamm_tree *t, cudaStream_t st, const uint32_t *list,
     tail.overflow = ov->overflow;
     tail.t_end = ov->t_end;
     tail.pdl_wait = ov->pdl && !ov->grp_done;
+    tail.ready = ov->ready;
+    tail.trav_done = ov->trav_done;
   }
   double *nsq_leaf = t->nsq + level_offset(t->depth);
   uint8_t *occ_leaf = t->occ + level_offset(t->depth);
@@ -884,12 +897,19 @@ void k1_timeline_dump(unsigned long long k3_end, unsigned long long k3_start) {
   fprintf(stderr, "\n");
 }
 
+int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
+                        const uint32_t *list, const unsigned *list_count, int64_t list_cap,
+                        unsigned *grp_done, unsigned grp_target, const int *overflow,
+                        unsigned long long *t_end, const unsigned *ready = nullptr,
+                        const unsigned *trav_done = nullptr);
+
 // Rebuild the whole pyramid of `t` from its padded storage (canonicalising
 // all-zero leaves in place).  Stream-ordered; no host sync; two launches.
 int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap,
                         unsigned *grp_done, unsigned grp_target, const int *overflow,
-                        unsigned long long *t_end) {
+                        unsigned long long *t_end, const unsigned *ready,
+                        const unsigned *trav_done) {
   // builds on copy_in run concurrently with the main stream's: own tickets
   Scratch &k1t = st == ctx->copy_in ? ctx->k1_ticket_in : ctx->k1_ticket;
   SPAMM_TRY(ensure_scratch(k1t, sizeof(unsigned), st, /*zeroed=*/true));
@@ -897,7 +917,8 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
   bool fused = false;
   // list mode follows the leaf-product kernel: launch it programmatically so
   // its CTAs are resident (and waiting) as that kernel's CTAs retire
-  K1Overlap ovs{grp_done, grp_target, overflow, t_end, list != nullptr && t_end != nullptr};
+  K1Overlap ovs{grp_done, grp_target, overflow, t_end, list != nullptr && t_end != nullptr, ready,
+                trav_done};
   const K1Overlap *ov = (grp_done || t_end) ? &ovs : nullptr;
   // list mode (C's tree): the segmented-chain kernel, a warp per leaf
   static const bool no_seg = getenv("SPAMM_NO_SEG_CHAIN") != nullptr;
@@ -919,6 +940,8 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
       tail.overflow = ov->overflow;
       tail.t_end = ov->t_end;
       tail.pdl_wait = ov->pdl && !ov->grp_done;
+      tail.ready = ov->ready;
+      tail.trav_done = ov->trav_done;
     }
     // shared memory: a staged leaf per warp (one CTA per SM)
     const unsigned smem = (unsigned)(SEG_WARPS * (t->leaf == 64

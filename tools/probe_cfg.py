@@ -10,8 +10,12 @@ trav = sys.argv[2] if len(sys.argv) > 2 else "auto"
 a_h, b_h, leaf, taus = workloads.make_config(name)
 a = sp.from_dense(a_h, leaf_size=leaf)
 b = a if b_h is a_h else sp.from_dense(b_h, leaf_size=leaf)
+import torch
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for rep in range(2):
     for tau in taus:
+        flush.fill_(rep)  # L2 flushed before every multiply, as bench.py does
+        torch.cuda.synchronize()
         c, st, det = sp.spamm_detailed(a, b, sp.SpammConfig(tau=tau), traversal=trav)
         if rep == 1:
             print(name, trav, tau, "cull %.3f gemm %.3f ctree %.3f total %.3f" % (
