@@ -41,7 +41,7 @@ struct Status {
 // Level k (2^k x 2^k, row-major) of the norm / occupancy pyramid starts at
 // (4^k - 1) / 3 in one concatenated array (the reference keeps a Python list
 // of per-level arrays, quadtree.py:131-138).
-__host__ __device__ inline int64_t level_offset(int k) {
+__host__ __device__ constexpr int64_t level_offset(int k) {
   return ((int64_t(1) << (2 * k)) - 1) / 3;
 }
 inline int64_t pyramid_size(int depth) { return level_offset(depth + 1); }

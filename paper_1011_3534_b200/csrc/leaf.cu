@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
   unsigned items = 0, stages_total = 0;
   if (warp == 0) {
     // ============================================================ producer
+    if (args.am && lane != 0) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmA) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmB) : "memory");
@@ -483,6 +484,10 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
     __syncwarp();
   } else {
     // ============================================================ consumers
+    // bitmask groups: C's norm kernel waits for the group list itself, so it
+    // may launch (and take its slot beside this CTA) right away; the launch
+    // of dependents counts once every thread of every CTA has signalled
+    if (args.am) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int cw = warp - 1;
     const int wm = cw / C::WN, wn = cw % C::WN, g = lane >> 2, t = lane & 3;
     double *__restrict__ Cm = (double *)args.c;

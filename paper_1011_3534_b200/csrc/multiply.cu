@@ -447,6 +447,8 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   s.kernel_launches = launches;
   for (int q = 1; q < 14; ++q)
     s.traverse_phase_us[q] = cc.phase_ns[q] ? (float)((double)(cc.phase_ns[q] - cc.phase_ns[0]) * 1e-3) : 0.f;
+  for (int q = 2; q < 8; ++q)  // (dense traversal: durations from kernel entry, CTA 0)
+    if (cc.phase_ns[q] && cc.phase_ns[q] < 1000000000ull) s.traverse_phase_us[q] = (float)(cc.phase_ns[q] * 1e-3);
   // slot 0: kernel entry -> phase 0 (negative offset of the prologue)
   s.traverse_phase_us[0] = cc.phase_ns[15] ? (float)((double)(cc.phase_ns[0] - cc.phase_ns[15]) * 1e-3) : 0.f;
   cudaEventElapsedTime(&s.ms_total, ctx->ev[0], ctx->ev[4]);

@@ -152,6 +152,12 @@ constexpr int PYR_TAIL_MAX_DEPTH = 6;
 
 constexpr int SEG_PAD = 16;  // bytes after each staged segment
 
+// 2^k for k in [-1074, 1023] (subnormal powers included), exactly
+__device__ __forceinline__ double pow2_exact(int k) {
+  return k >= -1022 ? __longlong_as_double((long long)(1023 + k) << 52)
+                    : __longlong_as_double(1ll << (k + 1074));
+}
+
 template <typename T, int LEAF>
 __host__ __device__ constexpr int seg_stride() {  // bytes per staged segment
   return LEAF * LEAF / 64 * (int)sizeof(T) + SEG_PAD;

@@ -859,34 +859,76 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
        x += (uint64_t)nblocks * DN_THREADS)
     a.dn_masks_clear[x] = 0u;
   for (int x = threadIdx.x; x < (D + 1) * 4; x += DN_THREADS) (&s_cnt[0][0])[x] = 0u;
+  // the operands' pyramid tops (levels 0..U: the warp-uniform tiers), staged
+  // once per CTA -- those tiers' verdicts then cost shared-memory reads
+  constexpr int U = D >= 2 ? D - 2 : -1;
+  constexpr int TOPN = U >= 0 ? (int)level_offset(U + 1) : 1;
+  static_assert(TOPN <= PREFIX_ENTRIES, "pyramid top exceeds the staging area");
+  double *s_top_na = sh.u.top.nrm_a, *s_top_nb = sh.u.top.nrm_b;  // (sh.u is free until the barrier)
+  uint8_t *s_top_oa = sh.u.top.occ_a, *s_top_ob = sh.u.top.occ_b;
+  if (U >= 0)
+    for (int e = threadIdx.x; e < TOPN; e += DN_THREADS) {
+      s_top_na[e] = __ldg(nrm_a + e);
+      s_top_nb[e] = __ldg(nrm_b + e);
+      s_top_oa[e] = __ldg(occ_a + e);
+      s_top_ob[e] = __ldg(occ_b + e);
+    }
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) tc->phase_ns[2] = globaltimer() - t_entry;  // (durations)
 
   // ---------------- phase 1: classify every leaf triple and its ancestors
   // Tiers t <= U have one ancestor per 64 consecutive x, so a warp's 32
   // lanes share it: those verdicts are warp-uniform and a warp whose tier-U
   // ancestor is not active leaves after them.
-  constexpr int U = D >= 2 ? D - 2 : -1;
   unsigned wc[D + 1][4];
 #pragma unroll
   for (int t = 0; t <= D; ++t) wc[t][0] = wc[t][1] = wc[t][2] = wc[t][3] = 0u;
-  for (uint64_t x = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x; x < N_X32;
-       x += (uint64_t)nblocks * DN_THREADS) {
+  // Per-lane tiers T0..D read the operands' lower pyramid levels from L2;
+  // those loads do not depend on the verdicts, so the next x's are issued
+  // before this x is classified (one memory round trip per thread, not one
+  // per x: a thread has 3-4 x at c2).
+  constexpr int T0 = U + 1;
+  constexpr int NPL = D + 1 - T0;
+  struct LaneOps {
+    double na[NPL], nb[NPL];
+    bool oc[NPL];
+  };
+  auto load_lane = [&](uint64_t x, LaneOps &o) {
+    const uint32_t xe = x < N_X ? (uint32_t)x : 0u;
+    const uint32_t ix = compact3(xe >> 2), jx = compact3(xe >> 1), kx = compact3(xe);
+#pragma unroll
+    for (int t = T0; t <= D; ++t) {
+      const uint32_t I = ix >> (D - t), J = jx >> (D - t), K = kx >> (D - t);
+      const int64_t ik = level_offset(t) + (int64_t(I) << t) + K;
+      const int64_t kj = level_offset(t) + (int64_t(K) << t) + J;
+      o.oc[t - T0] = __ldg(occ_a + ik) & __ldg(occ_b + kj);
+      o.na[t - T0] = __ldg(nrm_a + ik);
+      o.nb[t - T0] = __ldg(nrm_b + kj);
+    }
+  };
+  const uint64_t x_stride = (uint64_t)nblocks * DN_THREADS;
+  LaneOps cur;
+  uint64_t x = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x;
+  if (x < N_X32) load_lane(x, cur);
+  for (; x < N_X32; x += x_stride) {
+    LaneOps nxt;
+    if (x + x_stride < N_X32) load_lane(x + x_stride, nxt);
     const bool valid = x < N_X;
     const uint32_t xe = valid ? (uint32_t)x : 0u;  // lanes past the end read triple 0
     const uint32_t ix = compact3(xe >> 2), jx = compact3(xe >> 1), kx = compact3(xe);
     const uint64_t xw = x - lane;  // the warp's first x
     bool cand = valid;
 #pragma unroll
-    for (int t = 0; t <= U; ++t) {  // warp-uniform tiers
+    for (int t = 0; t <= U; ++t) {  // warp-uniform tiers (operands staged in shared memory)
       const int sh_t = D - t;
       const uint32_t I = ix >> sh_t, J = jx >> sh_t, K = kx >> sh_t;
-      const int64_t ik = level_offset(t) + (int64_t(I) << t) + K;
-      const int64_t kj = level_offset(t) + (int64_t(K) << t) + J;
+      const int ik = (int)level_offset(t) + (int)(I << t) + (int)K;
+      const int kj = (int)level_offset(t) + (int)(K << t) + (int)J;
       const int64_t r0 = int64_t(I) << sh_t, r1 = int64_t(I + 1) << sh_t;
       const bool intersects = r1 > a.row_lo && r0 < a.row_hi;
       const bool owned = r0 >= a.row_lo && r0 < a.row_hi;
-      const bool oc = occ_a[ik] & occ_b[kj];
-      const double np_ = __dmul_rn(nrm_a[ik], nrm_b[kj]);
+      const bool oc = s_top_oa[ik] & s_top_ob[kj];
+      const double np_ = __dmul_rn(s_top_na[ik], s_top_nb[kj]);
       const bool alive = cand && intersects && oc;
       const bool pruned = alive && np_ < a.tau_tier[t];
       const bool active = alive && !pruned;
@@ -907,71 +949,60 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
     }
     if (U >= 0 && !__any_sync(0xffffffffu, cand)) {  // nothing below survives
       if (lane == 0) am[x >> 5] = 0u;  // (pm's leaf words are zero at rest)
-      continue;
-    }
-    // per-lane tiers: operands of both loaded at once
-    constexpr int T0 = U + 1;
-    double na[D + 1 - T0], nbv[D + 1 - T0];
-    bool oc[D + 1 - T0];
+    } else {
+      bool pruned_leaf = false, active_leaf = false;
+      double np_leaf = 0.0;
 #pragma unroll
-    for (int t = T0; t <= D; ++t) {
-      const uint32_t I = ix >> (D - t), J = jx >> (D - t), K = kx >> (D - t);
-      const int64_t ik = level_offset(t) + (int64_t(I) << t) + K;
-      const int64_t kj = level_offset(t) + (int64_t(K) << t) + J;
-      oc[t - T0] = occ_a[ik] & occ_b[kj];
-      na[t - T0] = nrm_a[ik];
-      nbv[t - T0] = nrm_b[kj];
-    }
-    bool pruned_leaf = false, active_leaf = false;
-    double np_leaf = 0.0;
-#pragma unroll
-    for (int t = T0; t <= D; ++t) {
-      const int sh_t = D - t;
-      const uint32_t I = ix >> sh_t;
-      const bool rep = valid && (x & ((uint64_t(1) << (3 * sh_t)) - 1)) == 0;
-      const int64_t r0 = int64_t(I) << sh_t, r1 = int64_t(I + 1) << sh_t;
-      const bool intersects = r1 > a.row_lo && r0 < a.row_hi;
-      const bool owned = r0 >= a.row_lo && r0 < a.row_hi;
-      const double np_ = __dmul_rn(na[t - T0], nbv[t - T0]);
-      const bool alive = cand && intersects && oc[t - T0];
-      const bool pruned = alive && np_ < a.tau_tier[t];
-      const bool active = alive && !pruned;
-      const bool p_own = pruned && owned;
-      const bool skip = cand && intersects && !oc[t - T0] && owned;
-      wc[t][0] += __popc(__ballot_sync(0xffffffffu, rep && alive));
-      wc[t][1] += __popc(__ballot_sync(0xffffffffu, rep && active));
-      wc[t][2] += __popc(__ballot_sync(0xffffffffu, rep && p_own));
-      wc[t][3] += __popc(__ballot_sync(0xffffffffu, rep && skip));
-      if (t < D) {
-        if (rep && p_own) {
-          const uint64_t m = x >> (3 * sh_t);
-          const uint64_t w = dn_base(t) + (m >> 5);
-          atomicOr(&pm[w], 1u << (m & 31));
-          atomicAdd(&ptc[w / DN_PW], 1u);
+      for (int t = T0; t <= D; ++t) {
+        const int sh_t = D - t;
+        const uint32_t I = ix >> sh_t;
+        const bool rep = valid && (x & ((uint64_t(1) << (3 * sh_t)) - 1)) == 0;
+        const int64_t r0 = int64_t(I) << sh_t, r1 = int64_t(I + 1) << sh_t;
+        const bool intersects = r1 > a.row_lo && r0 < a.row_hi;
+        const bool owned = r0 >= a.row_lo && r0 < a.row_hi;
+        const double np_ = __dmul_rn(cur.na[t - T0], cur.nb[t - T0]);
+        const bool alive = cand && intersects && cur.oc[t - T0];
+        const bool pruned = alive && np_ < a.tau_tier[t];
+        const bool active = alive && !pruned;
+        const bool p_own = pruned && owned;
+        const bool skip = cand && intersects && !cur.oc[t - T0] && owned;
+        wc[t][0] += __popc(__ballot_sync(0xffffffffu, rep && alive));
+        wc[t][1] += __popc(__ballot_sync(0xffffffffu, rep && active));
+        wc[t][2] += __popc(__ballot_sync(0xffffffffu, rep && p_own));
+        wc[t][3] += __popc(__ballot_sync(0xffffffffu, rep && skip));
+        if (t < D) {
+          if (rep && p_own) {
+            const uint64_t m = x >> (3 * sh_t);
+            const uint64_t w = dn_base(t) + (m >> 5);
+            atomicOr(&pm[w], 1u << (m & 31));
+            atomicAdd(&ptc[w / DN_PW], 1u);
+          }
+        } else {
+          pruned_leaf = p_own;
+          active_leaf = active;
+          np_leaf = np_;
         }
-      } else {
-        pruned_leaf = p_own;
-        active_leaf = active;
-        np_leaf = np_;
+        cand = active;
       }
-      cand = active;
-    }
-    const unsigned bp = __ballot_sync(0xffffffffu, pruned_leaf);
-    const unsigned bv = __ballot_sync(0xffffffffu, active_leaf);
-    if (pruned_leaf) npd[x] = np_leaf;
-    // C block of this lane's triple; a warp's blocks all lie in one grouping tile
-    const uint64_t g = (uint64_t)ix * NB + jx;
-    const unsigned same = __match_any_sync(0xffffffffu, g);
-    if (bv && lane == __ffs(same) - 1 && (bv & same)) atomicOr(&ne[g >> 5], 1u << (g & 31));
-    if (lane == 0) {
-      const uint64_t w = dn_base(D) + (x >> 5);
-      if (bp) {
-        pm[w] = bp;
-        atomicAdd(&ptc[w / DN_PW], (unsigned)__popc(bp));
+      const unsigned bp = __ballot_sync(0xffffffffu, pruned_leaf);
+      const unsigned bv = __ballot_sync(0xffffffffu, active_leaf);
+      if (pruned_leaf) npd[x] = np_leaf;
+      // C block of this lane's triple; a warp's blocks all lie in one grouping tile
+      const uint64_t g = (uint64_t)ix * NB + jx;
+      const unsigned same = __match_any_sync(0xffffffffu, g);
+      if (bv && lane == __ffs(same) - 1 && (bv & same)) atomicOr(&ne[g >> 5], 1u << (g & 31));
+      if (lane == 0) {
+        const uint64_t w = dn_base(D) + (x >> 5);
+        if (bp) {
+          pm[w] = bp;
+          atomicAdd(&ptc[w / DN_PW], (unsigned)__popc(bp));
+        }
+        am[x >> 5] = bv;
+        if (bv && !a.bitmask_groups) atomicAdd(&qtc[g / DN_THREADS], (unsigned)__popc(bv));
       }
-      am[x >> 5] = bv;
-      if (bv) atomicAdd(&qtc[g / DN_THREADS], (unsigned)__popc(bv));
     }
+    cur = nxt;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && x < 4 * x_stride) tc->phase_ns[3 + x / x_stride] = globaltimer() - t_entry;
   }
   if (lane == 0) {
 #pragma unroll
@@ -1386,7 +1417,9 @@ static int launch_dense_d(const TraverseArgs &args, int num_sms, cudaStream_t st
       return SPAMM_ERR_INTERNAL;
     }
   }
-  const int grid = num_sms * (per_sm < 2 ? per_sm : 2);
+  // CTAs per SM (SPAMM_TRAVERSE_CTAS_PER_SM, default 2, capped by occupancy)
+  static const int want = getenv("SPAMM_TRAVERSE_CTAS_PER_SM") ? atoi(getenv("SPAMM_TRAVERSE_CTAS_PER_SM")) : 2;
+  const int grid = num_sms * (per_sm < want ? per_sm : want);
   void *kargs[] = {(void *)&args};
   // profiling aid: a plain launch (the grid still fits in one wave) so that
   // tools which skip cooperative launches can capture the kernel

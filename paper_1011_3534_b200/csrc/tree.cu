@@ -560,9 +560,12 @@ __global__ void __launch_bounds__(32 * SEG_WARPS) leaf_norm_seg_kernel(
   const int64_t gw = (int64_t)blockIdx.x * SEG_WARPS + warp;
   const int64_t nw = (int64_t)gridDim.x * SEG_WARPS;
   const bool check_flags = tail.grp_done && (!tail.overflow || !*(volatile const int *)tail.overflow);
+  unsigned long long *const k1_tl = g_k1_tl;  // optional per-leaf timeline (SPAMM_K1_TIMELINE)
   for (int64_t lx = gw; lx < n_leaves; lx += nw) {
     const int64_t leaf = list ? (int64_t)list[lx] : lx;
     const int64_t bi = leaf / nb, bj = leaf - bi * nb;
+    const bool tl_on = k1_tl && lane == 0 && lx < 8192;
+    if (tl_on) k1_tl[4 * lx + 3] = k1_gt();
     if (check_flags) {  // the leaf-product kernel has stored every tile of this block
       const unsigned *flag = tail.grp_done + lx;
       for (;;) {
@@ -580,11 +583,14 @@ __global__ void __launch_bounds__(32 * SEG_WARPS) leaf_norm_seg_kernel(
       const int sg = e / L, off = e % L;
       cp_async16(wsm + sg * SS + off * (int)sizeof(T), base + (int64_t)(e / LEAF) * N + (e % LEAF));
     }
+    if (tl_on) k1_tl[4 * lx] = k1_gt();
     cp_async_commit();
     cp_async_wait<0>();
     __syncwarp();
+    if (tl_on) k1_tl[4 * lx + 1] = k1_gt();
     U bits = 0;
     const double acc = seg_leaf_norm<T, LEAF>(wsm, tbl[warp], lane, bits);
+    if (tl_on) k1_tl[4 * lx + 2] = k1_gt();
     // occupancy / -0.0 (as the staged kernel): OR of every lane's raw bits
     unsigned long long all = (unsigned long long)bits;
 #pragma unroll
@@ -612,6 +618,361 @@ __global__ void __launch_bounds__(32 * SEG_WARPS) leaf_norm_seg_kernel(
       if (tail.trav_done && threadIdx.x == 0) spin_acquire_nonzero(tail.trav_done);
       __threadfence();
       pyramid_cta(tail, seg_smem, smem_bytes);
+      if (threadIdx.x == 0) {
+        *tail.ticket = 0u;
+        if (tail.t_end) *tail.t_end = k1_gt();
+      }
+    }
+  }
+}
+
+// ------------------------------------------------ K1, streaming exact norms
+// (opt-in: SPAMM_STREAM_NORMS.)  A CTA of 256 threads per C block, built to
+// form each norm with one FP64 multiply per element and integer work --
+// measured slower than the segmented-chain kernel above on c2 (C tree 52-78
+// vs 27-33 us: ~15 us per leaf, and it cannot share an SM with K3, whose 17
+// warps of 96 registers leave too few registers in one SM sub-partition).
+// The norm is the reference's sequential chain acc = rn(acc + s_i), s_i =
+// rn(x_i^2), row-major (quadtree.py:80-87), reproduced exactly:
+//   * every thread owns EPT consecutive elements; a CTA scan of their float
+//     sums estimates the chain value P_i before each element (FP32 from the
+//     squares' bits, relative error < 2^-17);
+//   * element i is "clean" when P_i (1 - 2^-10) and (P_i + s_i)(1 + 2^-10)
+//     share a binade [2^E, 2^(E+1)) (E >= -99): then the exact chain stays
+//     in that binade across it, where every value is a multiple of u =
+//     2^(E-52), so rn(A + s_i) = A + rnd_u(s_i) u -- an integer add, with
+//     rnd_u(s_i) formed from s_i's bits (a half-way s_i is a tie: not clean);
+//   * consecutive clean elements of one binade form a run (one integer D);
+//     every other element is a single rounded add; zeros are skipped (rn(A +
+//     0) = A); a thread with more than SN_R records uses the plain chain;
+//   * every warp merges its lanes' runs of one binade (warp-segmented sums);
+//     one warp applies the segments in order, each run as one exact add
+//     after checking that the exact chain value is in the binade and the sum
+//     stays below 2^(E+1) (otherwise the plain chain over its elements).
+constexpr int SN_THREADS = 256;
+constexpr int SN_R = 3;  // records per thread (more: the thread's elements by the plain chain)
+constexpr int SN_RUN = 0, SN_SINGLE = 1, SN_PLAIN = 2;
+struct SnRec {
+  unsigned long long D;  // run: sum of rnd_u(s_i); single: the bits of s_i
+  short E;
+  short kind;
+  short first, last;     // element range (row-major index in the leaf)
+};
+static_assert(sizeof(SnRec) == 16, "record layout");
+template <int LEAF>
+constexpr unsigned sn_smem_bytes() {  // the staged leaf, then the records
+  return (unsigned)(LEAF * LEAF * sizeof(double) + 2 * SN_THREADS * SN_R * sizeof(SnRec));
+}
+
+// float estimate of a square s >= 0 from its bits (no FP64 instruction):
+// exponent rebiased, mantissa truncated; below 2^-126 -> 0, beyond -> inf
+__device__ __forceinline__ float sq_est(double sq) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(sq);
+  const int fe = (int)((b >> 52) & 0x7ff) - 1023 + 127;
+  if (fe <= 0) return 0.f;
+  if (fe >= 255) return __uint_as_float(0x7f800000u);
+  return __uint_as_float(((unsigned)fe << 23) | (unsigned)((b >> 29) & 0x7fffffu));
+}
+
+template <int LEAF>
+__global__ void __launch_bounds__(SN_THREADS, 2) leaf_norm_stream_kernel(
+    double *__restrict__ padded, int64_t N, int64_t nb, double *__restrict__ nsq_leaf,
+    uint8_t *__restrict__ occ_leaf, const uint32_t *__restrict__ list, const unsigned *list_count,
+    PyrTail tail, unsigned smem_bytes) {
+  constexpr int NE = LEAF * LEAF, EPT = NE / SN_THREADS;
+  static_assert(EPT % 2 == 0 && LEAF % EPT == 0, "a thread's elements lie in one row");
+  static_assert(NE < 32768, "element indices are 16-bit");
+  extern __shared__ __align__(16) unsigned char sn_smem[];
+  double *stage = reinterpret_cast<double *>(sn_smem);
+  SnRec *rec = reinterpret_cast<SnRec *>(sn_smem + NE * sizeof(double));  // per warp: its records
+  SnRec *seg = rec + SN_THREADS * SN_R;                                      // ... and merged segments
+  constexpr int NW = SN_THREADS / 32;
+  __shared__ float s_wsum[NW];
+  __shared__ int s_wcnt[NW];
+  __shared__ unsigned long long s_bits[NW];
+  __shared__ double s_acc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tail.pdl_wait) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (tail.ready) {
+    if (tid == 0) spin_acquire_nonzero(tail.ready);
+    __syncthreads();
+  }
+  const int64_t n_leaves = list ? (int64_t)*list_count : nb * nb;
+  const bool check_flags = tail.grp_done && (!tail.overflow || !*(volatile const int *)tail.overflow);
+  unsigned long long *const k1_tl = g_k1_tl;  // optional per-leaf timeline (SPAMM_K1_TIMELINE)
+  for (int64_t lx = blockIdx.x; lx < n_leaves; lx += gridDim.x) {
+    const int64_t leaf = list ? (int64_t)list[lx] : lx;
+    const int64_t bi = leaf / nb, bj = leaf - bi * nb;
+    const bool tl_on = k1_tl && tid == 0 && lx < 8192;
+    if (tl_on) k1_tl[4 * lx + 3] = k1_gt();
+    if (check_flags) {  // the leaf-product kernel has stored every tile of this block
+      if (tid == 0) {
+        const unsigned *flag = tail.grp_done + lx;
+        for (;;) {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+          if (v >= tail.grp_target) break;
+          __nanosleep(64);
+        }
+      }
+      __syncthreads();
+    }
+    if (tl_on) k1_tl[4 * lx] = k1_gt();
+    double *base = padded + (bi * LEAF) * N + bj * LEAF;
+    const int e0 = tid * EPT;
+    const double *src = base + (int64_t)(e0 / LEAF) * N + (e0 % LEAF);
+    // pass A: raw-bit OR (occupancy, -0.0) and the chunk's estimated sum.
+    // Estimates are FP32 (the FP64 pipe is K3's): each square's float value
+    // from its bits (truncated mantissa), prefix error < 2^-17 relative.
+    unsigned long long bits = 0;
+    float csum = 0.f;
+    // this thread's elements, staged for pass B: pair q/2 of thread t at
+    // double2 slot (q/2) * SN_THREADS + t (bank-conflict free)
+    double2 *stage2 = reinterpret_cast<double2 *>(stage);
+#pragma unroll
+    for (int q = 0; q < EPT; q += 2) {
+      const double2 v = __ldcg(reinterpret_cast<const double2 *>(src + q));
+      stage2[(q / 2) * SN_THREADS + tid] = v;
+      bits |= (unsigned long long)__double_as_longlong(v.x) | (unsigned long long)__double_as_longlong(v.y);
+      csum += sq_est(__dmul_rn(v.x, v.x));
+      csum += sq_est(__dmul_rn(v.y, v.y));
+    }
+    // CTA exclusive scan of the chunk sums (estimates of the chain)
+    float incl = csum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const float y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    unsigned long long wb = bits;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wb |= __shfl_xor_sync(0xffffffffu, wb, o);
+    if (lane == 31) s_wsum[warp] = incl;
+    if (lane == 0) s_bits[warp] = wb;
+    __syncthreads();
+    float P = incl - csum;
+    for (int w = 0; w < warp; ++w) P += s_wsum[w];
+    // pass B: classify the elements into runs / single adds
+    SnRec lr[SN_R];
+    int nr = 0;
+    int runE = 0, runFirst = -1, runLast = -1;
+    unsigned long long runD = 0;
+    auto flush = [&]() {
+      if (runFirst < 0) return;
+      if (nr < SN_R) lr[nr] = SnRec{runD, (short)runE, (short)SN_RUN, (short)runFirst, (short)runLast};
+      ++nr;
+      runFirst = -1;
+    };
+    // (not unrolled: the classification body is long and one warp per SM
+    // sub-partition cannot afford instruction-cache misses)
+#pragma unroll 1
+    for (int q = 0; q < EPT; q += 2) {
+      const double2 v = stage2[(q / 2) * SN_THREADS + tid];
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const double x = h ? v.y : v.x;
+        const double sq = __dmul_rn(x, x);
+        const int e = e0 + q + h;
+        if (sq == 0.0) continue;  // rn(A + 0) = A: no effect on the chain
+        const unsigned long long sb = (unsigned long long)__double_as_longlong(sq);
+        const float Pn = P + sq_est(sq);
+        // the estimated chain before and after the element, widened by 2^-10
+        const unsigned lob = __float_as_uint(P * (1.f - 0x1p-10f));
+        const unsigned hib = __float_as_uint(Pn * (1.f + 0x1p-10f));
+        const int elo = (int)((lob >> 23) & 0xff), ehi = (int)((hib >> 23) & 0xff);
+        int es = (int)((sb >> 52) & 0x7ff);
+        bool clean = elo == ehi && elo >= 28 && elo <= 253 && es < 0x7ff;
+        unsigned long long r = 0;
+        const int E = elo - 127;  // binade [2^E, 2^(E+1)) of the exact chain across this element
+        if (clean) {  // rnd_u(sq), u = 2^(E-52), from the bits of sq
+          unsigned long long M = sb & ((1ull << 52) - 1);
+          if (es) M |= 1ull << 52;
+          else es = 1;
+          const int sh = E + 1023 - es;  // sq / u = M * 2^-sh
+          if (sh <= 0) {
+            clean = false;
+          } else if (sh < 64) {
+            const unsigned long long rem = M & ((1ull << sh) - 1), half = 1ull << (sh - 1);
+            r = (M >> sh) + (rem > half ? 1ull : 0ull);
+            clean = rem != half;  // a tie rounds by the chain value's last bit
+          }
+        }
+        if (clean) {
+          if (runFirst >= 0 && E == runE) {
+            runD += r;
+            runLast = e;
+          } else {
+            flush();
+            runE = E;
+            runD = r;
+            runFirst = runLast = e;
+          }
+        } else {
+          flush();
+          if (nr < SN_R) lr[nr] = SnRec{sb, 0, (short)SN_SINGLE, (short)e, (short)e};
+          ++nr;
+        }
+        P = Pn;
+      }
+    }
+    flush();
+    if (nr > SN_R) {  // too many records: this thread's elements by the plain chain
+      nr = 1;
+      lr[0] = SnRec{0, 0, (short)SN_PLAIN, (short)e0, (short)(e0 + EPT - 1)};
+    }
+    // Level 1 (every warp): its lanes' records in element order, consecutive
+    // runs of one binade merged (warp-segmented sums) into segments
+    {
+      int ci = nr;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, ci, o);
+        if (lane >= o) ci += y;
+      }
+      const int off = ci - nr, M = __shfl_sync(0xffffffffu, ci, 31);
+      SnRec *wr = rec + warp * 32 * SN_R;  // this warp's records
+      SnRec *ws = seg + warp * 32 * SN_R;  // ... and segments
+#pragma unroll
+      for (int k = 0; k < SN_R; ++k)
+        if (k < nr) wr[off + k] = lr[k];
+      __syncwarp();
+      int nseg = 0;  // (warp-uniform)
+      for (int c0 = 0; c0 < M; c0 += 32) {
+        const int i = c0 + lane;
+        const bool valid = i < M;
+        const SnRec r = valid ? wr[i] : SnRec{0, 0, -1, 0, 0};
+        const int rkind = r.kind, rE = r.E;
+        const int pk = __shfl_up_sync(0xffffffffu, rkind, 1), pe = __shfl_up_sync(0xffffffffu, rE, 1);
+        const bool cont = lane > 0 && valid && rkind == SN_RUN && pk == SN_RUN && pe == rE;
+        const unsigned heads = __ballot_sync(0xffffffffu, valid && !cont);
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        const unsigned ends = vm & ((heads >> 1) | ~(vm >> 1) | 0x80000000u);
+        unsigned long long ps = rkind == SN_RUN ? r.D : 0ull;  // inclusive prefix of run D
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned long long y = __shfl_up_sync(0xffffffffu, ps, o);
+          if (lane >= o) ps += y;
+        }
+        const int hl = 31 - __clz((int)(heads & (0xffffffffu >> (31 - lane))));
+        const unsigned long long pre = __shfl_sync(0xffffffffu, ps, hl > 0 ? hl - 1 : 0);
+        const int first = __shfl_sync(0xffffffffu, (int)r.first, hl < 0 ? 0 : hl);
+        // segment end lanes write their segment; a run continuing the
+        // previous chunk's last segment is merged into it
+        const bool is_end = (ends >> lane) & 1u;
+        const bool merge0 = lane == hl && hl == 0 && c0 > 0 && rkind == SN_RUN && nseg > 0 &&
+                            ws[nseg - 1].kind == SN_RUN && ws[nseg - 1].E == rE;
+        const bool merge_first = __shfl_sync(0xffffffffu, merge0 ? 1 : 0, 0) != 0;
+        const int before = __popc(ends & ((1u << lane) - 1));  // segments ending before this lane
+        if (is_end) {
+          SnRec sg;
+          sg.kind = (short)rkind;
+          sg.E = (short)rE;
+          sg.first = (short)first;
+          sg.last = r.last;
+          sg.D = rkind == SN_RUN ? ps - (hl > 0 ? pre : 0ull) : r.D;
+          if (hl == 0 && merge_first) {  // (the first segment of this chunk)
+            ws[nseg - 1].D += sg.D;
+            ws[nseg - 1].last = sg.last;
+          } else {
+            ws[nseg + before - (merge_first ? 1 : 0)] = sg;
+          }
+        }
+        nseg += __popc(ends) - (merge_first ? 1 : 0);
+        __syncwarp();
+      }
+      if (lane == 0) s_wcnt[warp] = nseg;
+    }
+    __syncthreads();
+    if (tl_on) k1_tl[4 * lx + 1] = k1_gt();
+    // Level 2 (one warp): the segments in order, each one exact add, one
+    // rounded add or (rare) a plain chain
+    if (warp == 0) {
+      double acc = 0.0;
+      int pE = 0, pFirst = -1, pLast = -1;
+      unsigned long long pD = 0;
+      auto replay = [&](int f, int l) {  // the plain chain over elements [f, l]
+        for (int e0r = f; e0r <= l; e0r += 32) {  // squares in parallel, then the chain
+          const int e = e0r + lane;
+          const int et = e / EPT, eq = e - et * EPT;  // (element e of the staged layout)
+          const double x = e <= l ? stage[2 * ((eq >> 1) * SN_THREADS + et) + (eq & 1)] : 0.0;
+          const double sq = __dmul_rn(x, x);
+          const int n = l - e0r + 1 < 32 ? l - e0r + 1 : 32;
+          for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, sq, k));
+        }
+      };
+      auto flushp = [&]() {
+        if (pFirst < 0) return;
+        bool ok = false;
+        const unsigned long long ab = (unsigned long long)__double_as_longlong(acc);
+        if (pD < (1ull << 53) && (int)((ab >> 52) & 0x7ff) == pE + 1023) {
+          const double v = acc + (double)pD * pow2_exact(pE - 52);  // exact below 2^(E+1)
+          if (v < pow2_exact(pE + 1)) {
+            acc = v;
+            ok = true;
+          }
+        }
+        if (!ok) replay(pFirst, pLast);
+        pFirst = -1;
+      };
+      for (int w = 0; w < NW; ++w) {
+        const SnRec *ws = seg + w * 32 * SN_R;
+        const int n = s_wcnt[w];
+        for (int k = 0; k < n; ++k) {
+          const SnRec sg = ws[k];
+          if (sg.kind == SN_RUN) {
+            if (pFirst >= 0 && pE == sg.E) {
+              pD += sg.D;
+              pLast = sg.last;
+            } else {
+              flushp();
+              pE = sg.E;
+              pD = sg.D;
+              pFirst = sg.first;
+              pLast = sg.last;
+            }
+          } else if (sg.kind == SN_SINGLE) {
+            flushp();
+            acc = __dadd_rn(acc, __longlong_as_double((long long)sg.D));
+          } else {
+            flushp();
+            replay(sg.first, sg.last);
+          }
+        }
+      }
+      flushp();
+      if (lane == 0) s_acc = acc;
+    }
+    __syncthreads();
+    if (tl_on) k1_tl[4 * lx + 2] = k1_gt();
+    unsigned long long all = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) all |= s_bits[w];
+    const bool nz = (all << 1) != 0;
+    if (!nz && all) {  // all zero with some -0.0: canonicalise to +0.0
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) const_cast<double *>(src)[q] = 0.0;
+    }
+    if (tid == 0) {
+      const double acc = s_acc;
+      nsq_leaf[leaf] = acc;
+      occ_leaf[leaf] = (uint8_t)nz;
+      tail.nrm[level_offset(tail.depth) + leaf] = __dsqrt_rn(acc);
+      if (tail.grp_done) tail.grp_done[lx] = 0u;  // zero at rest for the next product
+    }
+    __syncthreads();  // (the record area and s_* are reused by the next leaf)
+  }
+  if (tail.ticket) {  // the last CTA builds the pyramid
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(tail.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      if (tail.trav_done && threadIdx.x == 0) spin_acquire_nonzero(tail.trav_done);
+      __threadfence();
+      pyramid_cta(tail, sn_smem, smem_bytes);
       if (threadIdx.x == 0) {
         *tail.ticket = 0u;
         if (tail.t_end) *tail.t_end = k1_gt();
@@ -881,6 +1242,30 @@ void k1_timeline_enable(cudaStream_t st) {
 void k1_timeline_dump(unsigned long long k3_end, unsigned long long k3_start) {
   std::vector<unsigned long long> tl(4 * 8192);
   cudaMemcpy(tl.data(), h_k1_tl_dev, tl.size() * 8, cudaMemcpyDeviceToHost);
+  {  // segmented-chain kernel: per leaf [flag seen, staged, norm done, warp reached it]
+    std::vector<std::pair<unsigned long long, int>> done;
+    for (int q = 0; q < 8192; ++q)
+      if (tl[4 * q + 2] && tl[4 * q + 3]) done.push_back({tl[4 * q + 2], q});
+    if (!done.empty()) {
+      std::sort(done.begin(), done.end());
+      double norm_sum = 0;
+      for (auto &d : done) norm_sum += (double)(tl[4 * d.second + 2] - tl[4 * d.second + 1]);
+      int before_end = 0;
+      double first_reach = 1e30;
+      for (auto &d : done) {
+        before_end += d.first < k3_end;
+        first_reach = std::min(first_reach, ((double)tl[4 * d.second + 3] - (double)k3_end) * 1e-3);
+      }
+      fprintf(stderr, "[k1 seg] leaves=%zu done during K3 %d, first reach %.1f us, mean norm %.2f us; last leaves (us after K3 end): ",
+              done.size(), before_end, first_reach, norm_sum / done.size() * 1e-3);
+      for (size_t k = done.size() > 4 ? done.size() - 4 : 0; k < done.size(); ++k) {
+        const int q = done[k].second;
+        auto rel = [&](int f) { return ((double)tl[4 * q + f] - (double)k3_end) * 1e-3; };
+        fprintf(stderr, " [reach %.1f flag %.1f staged %.1f done %.1f]", rel(3), rel(0), rel(1), rel(2));
+      }
+      fprintf(stderr, "\n");
+    }
+  }
   unsigned long long t0 = ~0ull;
   int n = 0;
   for (int q = 0; q < 8192; ++q)
@@ -926,7 +1311,54 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
   // segmented kernel is latency-short, but for 10^4-10^6 C blocks the staged
   // kernel's 32-leaf CTAs stream them faster: c3 C tree 0.13 vs 0.35 ms, c5
   // 0.30 vs 0.81 ms)
-  if (list && !no_seg && grp_done && (t->leaf == 32 || t->leaf == 64)) {
+  // (SPAMM_STREAM_NORMS: the CTA-per-leaf streaming kernel instead -- exact
+  // too, measured slower: DESIGN.md, K1)
+  static const bool stream_norms = getenv("SPAMM_STREAM_NORMS") != nullptr;
+  if (list && !no_seg && stream_norms && grp_done && t->dtype == SPAMM_DTYPE_F64 &&
+      (t->leaf == 32 || t->leaf == 64)) {
+    // the streaming exact-norm kernel: one small CTA per SM beside K3 (it is
+    // launched programmatically behind K3 and becomes resident at once)
+    PyrTail tail{};
+    tail.nsq = t->nsq;
+    tail.occ = t->occ;
+    tail.nrm = t->nrm;
+    tail.depth = t->depth;
+    tail.ticket = t->depth <= PYR_TAIL_MAX_DEPTH ? ticket : nullptr;
+    tail.grp_done = ov->grp_done;
+    tail.grp_target = ov->grp_target;
+    tail.overflow = ov->overflow;
+    tail.t_end = ov->t_end;
+    tail.pdl_wait = 0;
+    tail.ready = ov->ready;
+    tail.trav_done = ov->trav_done;
+    cudaLaunchConfig_t cfg{};
+    // CTAs (a leaf each at a time) fill the SMs as K3's CTAs retire: up to
+    // two per SM (256 threads, 57 KB of shared memory each at leaf 64)
+    static const int per_sm = getenv("SPAMM_SN_CTAS_PER_SM") ? atoi(getenv("SPAMM_SN_CTAS_PER_SM")) : 2;
+    const unsigned smem = t->leaf == 64 ? sn_smem_bytes<64>() : sn_smem_bytes<32>();
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(std::min<int64_t>(list_cap, t->nb * t->nb), (int64_t)ctx->num_sms * per_sm)));
+    cfg.blockDim = dim3(SN_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    auto go = [&](auto kern) -> int {
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      // (the library's kernels all ask for the maximum shared-memory carveout)
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      SPAMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, (double *)t->padded, t->N, t->nb,
+                                        t->nsq + level_offset(t->depth), t->occ + level_offset(t->depth),
+                                        list, list_count, tail, smem));
+      return SPAMM_OK;
+    };
+    if (t->leaf == 64) SPAMM_TRY(go(leaf_norm_stream_kernel<64>));
+    else SPAMM_TRY(go(leaf_norm_stream_kernel<32>));
+    fused = tail.ticket != nullptr;
+  } else if (list && !no_seg && grp_done && (t->leaf == 32 || t->leaf == 64)) {
     const bool f64 = t->dtype == SPAMM_DTYPE_F64;
     PyrTail tail{};
     tail.nsq = t->nsq;
