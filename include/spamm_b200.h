@@ -1,8 +1,9 @@
 /*
  * spamm_b200.h -- C ABI of the B200-native SpAMM hot path.
  *
- * Plain pointers, sizes and opaque handles only (no torch or CUDA types in
- * the signatures).  Every entry point returns SPAMM_OK (0) or an error code
+ * Plain pointers, sizes and opaque handles only (no torch types in the
+ * signatures; the one CUDA type is spamm_stream_t, the layout of a
+ * cudaStream_t, declared here without the CUDA headers).  Every entry point returns SPAMM_OK (0) or an error code
  * and records a message retrievable with spamm_last_error() (thread-local).
  * Calls are synchronous from the caller's point of view: results are ready
  * on return.  Trees are immutable after construction and safe to share
@@ -40,6 +41,8 @@
  *   spamm_tc2_update          <- the add/scale pair of tc2_step  purification.py:123-133
  *   spamm_tree_band_* , spamm_tree_pyramid_rebuild, spamm_tree_blocks_*_device,
  *   spamm_tree_diagonal_rows  <- (new) row bands of distributed matrices
+ *   spamm_stream_wait / _signal, *_on  <- (new) stream-ordered hand-off with the
+ *                                caller's CUDA streams (no device-wide synchronisation)
  */
 #ifndef SPAMM_B200_H
 #define SPAMM_B200_H
@@ -131,6 +134,20 @@ SPAMM_API int spamm_device_count(int *count);
 /* Library build identity, e.g. "spamm_b200 0.1 sm_100a". */
 SPAMM_API const char *spamm_version(void);
 
+/* -- stream ordering ------------------------------------------------------ */
+/* The library works on its own CUDA stream per device.  Device data that a
+ * caller's stream produces or consumes is handed over with events, never a
+ * device-wide synchronisation:
+ *   spamm_stream_wait(device, s)   the library's stream waits for the work
+ *                                  queued on s so far (s produced the input);
+ *   spamm_stream_signal(device, s) s waits for the work queued on the
+ *                                  library's stream so far (s reads a result,
+ *                                  or may now reuse / free an input).
+ * spamm_stream_t has the layout of cudaStream_t (0 = the legacy stream). */
+typedef struct CUstream_st *spamm_stream_t;
+SPAMM_API int spamm_stream_wait(int32_t device, spamm_stream_t producer);
+SPAMM_API int spamm_stream_signal(int32_t device, spamm_stream_t consumer);
+
 /* -- trees ---------------------------------------------------------------- */
 SPAMM_API int spamm_tree_from_host(const void *host, int64_t n, int64_t ld, int32_t leaf_size,
                          int32_t dtype, int32_t device, spamm_tree **out);
@@ -148,6 +165,14 @@ SPAMM_API int spamm_tree_wait(const spamm_tree *t);
 /* `dev` is a device pointer on `device`; n x n with leading dimension ld. */
 SPAMM_API int spamm_tree_from_device(const void *dev, int64_t n, int64_t ld, int32_t leaf_size,
                            int32_t dtype, int32_t device, spamm_tree **out);
+/* spamm_tree_from_device ordered on the caller's stream: the copy starts
+ * after the work queued on `stream` (which produced `dev`), and `stream`
+ * waits for the copy, so the caller may reuse or free `dev` in stream order
+ * (e.g. torch's caching allocator) -- the reference's from_dense boundary
+ * (quadtree.py:218) for device-resident producers, without a device-wide sync. */
+SPAMM_API int spamm_tree_from_device_on(const void *dev, int64_t n, int64_t ld, int32_t leaf_size,
+                                        int32_t dtype, int32_t device, spamm_stream_t stream,
+                                        spamm_tree **out);
 /* Adopt an already padded N x N device array (copied), rebuild its pyramid. */
 SPAMM_API int spamm_tree_from_padded_device(const void *dev_padded, int64_t n, int64_t padded_dim,
                                   int32_t leaf_size, int32_t dtype, int32_t device,
@@ -209,6 +234,13 @@ SPAMM_API void spamm_tree_free(spamm_tree *t);
 /* -- multiply --------------------------------------------------------------- */
 SPAMM_API int spamm_multiply(const spamm_tree *a, const spamm_tree *b, double tau, uint32_t flags,
                    spamm_tree **c, spamm_stats *stats, spamm_product **product);
+/* spamm_multiply ordered on the caller's stream: the library's stream waits
+ * for the work queued on `stream` (e.g. kernels that wrote into the operands'
+ * storage), and `stream` waits for the product (C is complete on return, as
+ * for spamm_multiply, so the caller's later work on `stream` may read it). */
+SPAMM_API int spamm_multiply_on(const spamm_tree *a, const spamm_tree *b, double tau, uint32_t flags,
+                                spamm_stream_t stream, spamm_tree **c, spamm_stats *stats,
+                                spamm_product **product);
 /* Shard of spamm_multiply restricted to C leaf block rows [row_lo, row_hi):
  * only triples whose leaf rows intersect the range are traversed; pruned and
  * skipped calls are counted by the shard owning the call's first row, so the

@@ -47,6 +47,7 @@ EXPORTED = (
     "spamm_tree_band_from_device", "spamm_tree_band_set", "spamm_tree_pyramid_rebuild",
     "spamm_tree_blocks_gather_device", "spamm_tree_blocks_scatter_device",
     "spamm_tree_diagonal_rows", "spamm_tc2_update",
+    "spamm_stream_wait", "spamm_stream_signal", "spamm_tree_from_device_on", "spamm_multiply_on",
 )
 
 
@@ -113,6 +114,11 @@ def load(path=LIB_PATH):
         L.spamm_tree_free.argtypes = [vp]
         L.spamm_tree_free.restype = None
         L.spamm_multiply.argtypes = [vp, vp, ctypes.c_double, u32, pp, ctypes.POINTER(Stats), pp]
+        L.spamm_multiply_on.argtypes = [vp, vp, ctypes.c_double, u32, vp, pp, ctypes.POINTER(Stats),
+                                        pp]
+        L.spamm_stream_wait.argtypes = [i32, vp]
+        L.spamm_stream_signal.argtypes = [i32, vp]
+        L.spamm_tree_from_device_on.argtypes = [vp, i64, i64, i32, i32, i32, vp, pp]
         L.spamm_multiply_rows.argtypes = [vp, vp, ctypes.c_double, u32, i64, i64, pp,
                                           ctypes.POINTER(Stats), pp]
         L.spamm_product_boxes.argtypes = [vp, vp, i64]

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "spamm_b200.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace spamm {
 
@@ -88,6 +89,7 @@ struct DeviceContext {
   cudaStream_t copy_out = nullptr;   // device->host result transfers (overlap the next call)
   cudaStream_t copy_in = nullptr;    // asynchronous builds: host->device copy + K1 (overlap compute)
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t handoff = nullptr;  // stream hand-off with the caller's streams
   cudaEvent_t ev[8] = {};
   std::mutex mu;
   Scratch cull_codes[2];  // ping-pong survivor lists (packed i,j,k)
@@ -122,6 +124,16 @@ struct DeviceContext {
 };
 
 int get_context(int device, DeviceContext **ctx);
+
+// NVTX range over a host-side launch sequence (K1 builds, K2 traversal, K3
+// leaf products, C's tree, the multiply): kernels a profiler traces nest
+// under the range that launched them; no cost without a profiler attached.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 int ensure_scratch(Scratch &s, size_t bytes, cudaStream_t stream, bool zeroed = false);
 // Zero `bytes` at `p` with a kernel (16-byte stores; any alignment).  Used on
 // the multiply path instead of cudaMemsetAsync, which is carried out by a

@@ -103,6 +103,7 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
   DeviceContext *ctx;
   SPAMM_TRY(get_context(a->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  NvtxRange nvtx_mul("spamm.multiply");
   cudaStream_t st = ctx->stream;
   SPAMM_TRY(tree_join(ctx, a));
   SPAMM_TRY(tree_join(ctx, b));
@@ -227,9 +228,12 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
       ta.c_nrm_leaf = c->nrm + level_offset(depth);
       ta.c_occ_leaf = c->occ + level_offset(depth);
     }
-    if ((rc = dense ? launch_traverse_dense(ta, ctx->num_sms, st)
-                    : launch_traverse(ta, ctx->num_sms, st)))
-      break;
+    {
+      NvtxRange r("spamm.K2.traverse");
+      if ((rc = dense ? launch_traverse_dense(ta, ctx->num_sms, st)
+                      : launch_traverse(ta, ctx->num_sms, st)))
+        break;
+    }
     ctx->counter_parity ^= 1;
     if (dense) ctx->dense_parity ^= 1;
     ctx->last_bitmask = ta.bitmask_groups != 0;
@@ -323,11 +327,15 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     static const bool k1tl = getenv("SPAMM_K1_TIMELINE") != nullptr;
     if (k1tl) k1_timeline_enable(st);
     bool overlapped = false;
-    if ((rc = launch_leaf(la, a->dtype, ctx->num_sms, st, &launches, &overlapped))) break;
+    {
+      NvtxRange r("spamm.K3.leaf_products");
+      if ((rc = launch_leaf(la, a->dtype, ctx->num_sms, st, &launches, &overlapped))) break;
+    }
     if (!overlapped) SPAMM_CUDA_BREAK(cudaEventRecord(ctx->ev[3], st));
 
     // ------------------------------------------- C's tree (multiply.py:220)
     {
+      NvtxRange r("spamm.K1.c_tree");
       const int tile = a->leaf < 64 ? a->leaf : 64;
       const unsigned subs = (unsigned)((a->leaf / tile) * (a->leaf / tile));
       const bool bm = ta.bitmask_groups != 0;
@@ -590,6 +598,19 @@ int spamm_multiply(const spamm_tree *a, const spamm_tree *b, double tau, uint32_
   if (product) *product = nullptr;
   const int64_t nb = a ? a->nb : 0;
   return multiply_impl(a, b, tau, flags, 0, nb, c, stats, product);
+}
+
+int spamm_multiply_on(const spamm_tree *a, const spamm_tree *b, double tau, uint32_t flags,
+                      spamm_stream_t stream, spamm_tree **c, spamm_stats *stats,
+                      spamm_product **product) {
+  if (product) *product = nullptr;
+  if (!a || !b) {
+    set_error("null operand");
+    return SPAMM_ERR_VALUE;
+  }
+  SPAMM_TRY(spamm_stream_wait(a->device, stream));
+  SPAMM_TRY(multiply_impl(a, b, tau, flags, 0, a->nb, c, stats, product));
+  return spamm_stream_signal(a->device, stream);
 }
 
 int spamm_multiply_rows(const spamm_tree *a, const spamm_tree *b, double tau, uint32_t flags,

@@ -434,6 +434,7 @@ SPAMM_API int spamm_tc2_update(const spamm_tree *x, const spamm_tree *x2, int32_
   DeviceContext *ctx;
   SPAMM_TRY(get_context(x->device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  NvtxRange nvtx_tc2("spamm.tc2_update");
   SPAMM_TRY(tree_join(ctx, x));
   SPAMM_TRY(tree_join(ctx, x2));
   cudaStream_t st = ctx->stream;

@@ -54,6 +54,7 @@ int get_context(int device, DeviceContext **out) {
     SPAMM_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
     SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
     SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming));
+    SPAMM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->handoff, cudaEventDisableTiming));
     for (auto &e : ctx->ev) SPAMM_CUDA_TRY(cudaEventCreate(&e));
     SPAMM_CUDA_TRY(cudaMallocHost(&ctx->host_pinned, 1 << 16));
     // keep freed pool memory cached between calls (stream-ordered allocator)
@@ -1556,6 +1557,7 @@ static int tree_from(const void *src, bool src_on_host, int64_t n, int64_t ld, i
   DeviceContext *ctx;
   SPAMM_TRY(get_context(device, &ctx));
   std::lock_guard<std::mutex> lk(ctx->mu);
+  NvtxRange nvtx_build(src_on_host ? "spamm.K1.tree_from_host" : "spamm.K1.tree_from_device");
   spamm_tree *t = nullptr;
   SPAMM_TRY(alloc_tree(ctx, n, leaf, dtype, &t));
   const int64_t esz = t->elem_size();
@@ -1702,6 +1704,31 @@ int spamm_tree_wait(const spamm_tree *tc) {
 int spamm_tree_from_device(const void *dev, int64_t n, int64_t ld, int32_t leaf, int32_t dtype,
                            int32_t device, spamm_tree **out) {
   return tree_from(dev, false, n, ld, leaf, dtype, device, out);
+}
+
+int spamm_stream_wait(int32_t device, spamm_stream_t producer) {
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_CUDA_TRY(cudaEventRecord(ctx->handoff, (cudaStream_t)producer));
+  SPAMM_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->handoff, 0));
+  return SPAMM_OK;
+}
+
+int spamm_stream_signal(int32_t device, spamm_stream_t consumer) {
+  DeviceContext *ctx;
+  SPAMM_TRY(get_context(device, &ctx));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  SPAMM_CUDA_TRY(cudaEventRecord(ctx->handoff, ctx->stream));
+  SPAMM_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)consumer, ctx->handoff, 0));
+  return SPAMM_OK;
+}
+
+int spamm_tree_from_device_on(const void *dev, int64_t n, int64_t ld, int32_t leaf, int32_t dtype,
+                              int32_t device, spamm_stream_t stream, spamm_tree **out) {
+  SPAMM_TRY(spamm_stream_wait(device, stream));
+  SPAMM_TRY(tree_from(dev, false, n, ld, leaf, dtype, device, out));
+  return spamm_stream_signal(device, stream);
 }
 
 int spamm_tree_from_padded_device(const void *dev_padded, int64_t n, int64_t padded_dim,

@@ -173,6 +173,30 @@ def merge_pruned(parts):
 
 
 # -------------------------------------------------------------- collectives
+class _nvtx:
+    """NVTX range (torch.cuda.nvtx) around a collective or a distributed
+    phase, so a profiler shows the exchanges beside the library's K1/K2/K3
+    ranges; a no-op without CUDA."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        import torch
+
+        self.on = torch.cuda.is_available()
+        if self.on:
+            torch.cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            import torch
+
+            torch.cuda.nvtx.range_pop()
+        return False
+
+
 class Comm:
     """The process group plus staging: NCCL works on device tensors, gloo on
     host tensors (the CPU tests)."""
@@ -192,6 +216,10 @@ class Comm:
     def all_gather_var(self, t):
         """All-gather tensors whose first dimension differs between ranks;
         returns the list in rank order (on t's device)."""
+        with _nvtx("spamm.allgather"):
+            return self._all_gather_var(t)
+
+    def _all_gather_var(self, t):
         import torch
 
         dev = t.device
@@ -211,6 +239,10 @@ class Comm:
     def all_to_all_var(self, send):
         """send[q] (first dims may differ) goes to rank q; returns recv[q]
         from rank q, in rank order.  Rows of uint8 / int64 / float tensors."""
+        with _nvtx("spamm.alltoall"):
+            return self._all_to_all_var(send)
+
+    def _all_to_all_var(self, send):
         import torch
 
         dev = send[0].device
@@ -290,11 +322,20 @@ def _leaf_level(tree):
             torch.as_tensor(DeviceArray(occ + off, (G,), np.uint8), device=dev))
 
 
-def _sync_torch():
-    import torch
+def _to_lib(device):
+    """torch's queued work (which produced data the library reads) before the
+    library's stream: an event hand-off, not a device-wide synchronisation."""
+    from .quadtree import torch_to_lib
 
-    if torch.cuda.is_available() and torch.cuda.is_initialized():
-        torch.cuda.synchronize()
+    torch_to_lib(device)
+
+
+def _to_torch(device):
+    """The library's queued work before torch's current stream (which reads
+    library output or reuses memory the library read)."""
+    from .quadtree import lib_to_torch
+
+    lib_to_torch(device)
 
 
 def tree_from_padded(padded, n, leaf, device=None):
@@ -304,13 +345,14 @@ def tree_from_padded(padded, n, leaf, device=None):
     from .quadtree import _wrap
 
     assert padded.is_cuda and padded.is_contiguous()
-    _sync_torch()  # torch's collectives/kernels that filled `padded` come first
     code = _lib.DTYPE_F64 if padded.dtype == torch.float64 else _lib.DTYPE_F32
     h = ctypes.c_void_p()
     dev = padded.device.index if device is None else device
+    _to_lib(dev)  # torch's collectives/kernels that filled `padded` come first
     _lib.check(_lib.load().spamm_tree_from_padded_device(
         ctypes.c_void_p(padded.data_ptr()), int(n), int(padded.shape[0]), int(leaf), code, dev,
         ctypes.byref(h)))
+    _to_torch(dev)  # (torch may free / reuse `padded` after the copy)
     return _wrap(h.value)
 
 
@@ -349,12 +391,13 @@ class ShardedTree:
         code = _lib.DTYPE_F64 if rows.dtype == torch.float64 else _lib.DTYPE_F32
         if rows.numel():
             assert rows.is_cuda and rows.stride(1) == 1
-        _sync_torch()
+        _to_lib(dev)
         h = ctypes.c_void_p()
         ld = int(rows.stride(0)) if rows.numel() else int(n)
         _lib.check(_lib.load().spamm_tree_band_from_device(
             ctypes.c_void_p(rows.data_ptr() if rows.numel() else 0), int(n), max(ld, int(n)),
             int(leaf), code, int(band[0]), int(band[1]), dev, ctypes.byref(h)))
+        _to_torch(dev)
         st = cls(_wrap(h.value), band, comm)
         st.gather_pyramid()
         return st
@@ -463,6 +506,7 @@ def gather_leaf_level(tree, band, comm):
     import torch
 
     nsq, occ = _leaf_level(tree)
+    _to_torch(tree.device)  # the library's leaf level before torch reads it
     nb = tree.block_grid
     lo, hi = band
     mine = torch.cat([nsq[lo * nb:hi * nb].view(torch.uint8).view(-1, 8),
@@ -470,10 +514,9 @@ def gather_leaf_level(tree, band, comm):
     parts = comm.all_gather_var(mine)
     full = torch.cat(parts).to(nsq.device)
     assert full.shape[0] == nb * nb, "bands must cover every block row"
-    _sync_torch()
     nsq.copy_(full[:, :8].contiguous().view(torch.float64).view(-1))
     occ.copy_(full[:, 8])
-    _sync_torch()
+    _to_lib(tree.device)  # torch's writes of the leaf level before the rebuild
     _lib.check(_lib.load().spamm_tree_pyramid_rebuild(tree._handle))
     tree._host_pyramid = None
     info = _lib.TreeInfo()
@@ -486,6 +529,11 @@ def halo_exchange(b, needed, comm):
     """Fetch into b's storage the listed blocks (ids k * nb + j, any order)
     that other ranks hold: ids to their owners (all-to-all), blocks back
     (all-to-all).  Returns the bytes this rank received."""
+    with _nvtx("spamm.halo_exchange"):
+        return _halo_exchange(b, needed, comm)
+
+
+def _halo_exchange(b, needed, comm):
     import torch
 
     nb, L = b.block_grid, b.leaf_size
@@ -507,17 +555,18 @@ def halo_exchange(b, needed, comm):
         ids = asked[q].to(f"cuda:{b.tree.device}")
         buf = torch.empty((ids.numel(), blk), dtype=torch.uint8, device=f"cuda:{b.tree.device}")
         if ids.numel():
-            _sync_torch()
+            _to_lib(b.tree.device)
             _lib.check(L_.spamm_tree_blocks_gather_device(b.tree._handle,
                                                           ctypes.c_void_p(ids.data_ptr()),
                                                           ids.numel(),
                                                           ctypes.c_void_p(buf.data_ptr())))
+            _to_torch(b.tree.device)
         send.append(buf if comm.nccl else buf.cpu())
     got = comm.all_to_all_var(send)                # the blocks I asked for
     ids = torch.cat([r.to(f"cuda:{b.tree.device}") for r in req])
     data = torch.cat([g.to(f"cuda:{b.tree.device}") for g in got])
     if ids.numel():
-        _sync_torch()
+        _to_lib(b.tree.device)
         _lib.check(L_.spamm_tree_blocks_scatter_device(b.tree._handle,
                                                        ctypes.c_void_p(ids.data_ptr()),
                                                        ids.numel(),

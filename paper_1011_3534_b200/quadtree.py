@@ -366,31 +366,48 @@ def from_dense(dense, leaf_size=4, dtype=None, device=None, wait=True):
     return _wrap(h.value)
 
 
-def _sync_torch():
-    """Order device data produced by torch (on its streams) before the
-    library's own stream reads it."""
+def torch_stream(device):
+    """The handle of torch's current CUDA stream on `device` (0 = the legacy
+    stream, also when torch is not in use): the stream a caller's device data
+    is produced / consumed on."""
     import sys
 
     torch = sys.modules.get("torch")
     if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
-        torch.cuda.synchronize()
+        return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    return ctypes.c_void_p(0)
 
 
-def from_device_pointer(ptr, n, leaf_size=4, dtype=np.float64, device=None, ld=None):
+def torch_to_lib(device):
+    """Stream hand-off: the library's stream waits for the work torch has
+    queued so far (torch produced data the library reads).  An event wait on
+    the device, not a device-wide synchronisation."""
+    _lib.check(_lib.load().spamm_stream_wait(int(device), torch_stream(device)))
+
+
+def lib_to_torch(device):
+    """Stream hand-off: torch's current stream waits for the library's queued
+    work (torch reads library results or reuses memory the library read)."""
+    _lib.check(_lib.load().spamm_stream_signal(int(device), torch_stream(device)))
+
+
+def from_device_pointer(ptr, n, leaf_size=4, dtype=np.float64, device=None, ld=None, stream=None):
     """Build a tree from an n x n array already resident in device memory
-    (e.g. a torch CUDA tensor's ``data_ptr()``); no host staging.  The
-    library works on its own CUDA stream, so work queued by torch that
-    produces the array is waited for first."""
-    _sync_torch()
+    (e.g. a torch CUDA tensor's ``data_ptr()``); no host staging.  Stream
+    ordered (spamm_tree_from_device_on): the copy starts after the work
+    queued on `stream` (default: torch's current stream) and that stream
+    waits for the copy, so the caller may free or reuse the array in stream
+    order -- no device-wide synchronisation."""
     target = np.dtype(dtype)
     if target not in _SUPPORTED_DTYPES:
         raise ValueError(f"unsupported element dtype {target}")
     h = ctypes.c_void_p()
     dev = get_device() if device is None else int(device)
     code = _lib.DTYPE_F64 if target == np.float64 else _lib.DTYPE_F32
-    _lib.check(_lib.load().spamm_tree_from_device(ctypes.c_void_p(ptr), int(n),
-                                                  int(n if ld is None else ld), int(leaf_size),
-                                                  code, dev, ctypes.byref(h)))
+    st = torch_stream(dev) if stream is None else ctypes.c_void_p(int(stream))
+    _lib.check(_lib.load().spamm_tree_from_device_on(ctypes.c_void_p(ptr), int(n),
+                                                     int(n if ld is None else ld), int(leaf_size),
+                                                     code, dev, st, ctypes.byref(h)))
     return _wrap(h.value)
 
 

@@ -514,3 +514,28 @@ def test_chained_launch_path_is_deterministic():
         assert got[0] == ref[0]
         assert np.array_equal(got[1], ref[1])
         assert np.array_equal(got[2], ref[2]) and np.array_equal(got[3], ref[3])
+
+
+@pytest.mark.gpu
+def test_from_device_pointer_is_stream_ordered():
+    """from_device_pointer hands off with the producer's stream by events
+    (spamm_tree_from_device_on), no device-wide synchronisation: the copy sees
+    the final values of work still queued on a side stream, and that stream
+    may overwrite the array right after the call without touching the tree."""
+    import torch
+
+    n, leaf = 1024, 32
+    s = torch.cuda.Stream()
+    a = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(s):
+        x = torch.rand((2048, 2048), dtype=torch.float64, device="cuda")
+        for _ in range(20):  # keep the side stream busy well past the call below
+            x = torch.tanh(x @ x / 2048.0)
+        a.copy_(x[:n, :n])
+        t = sp.from_device_pointer(a.data_ptr(), n, leaf_size=leaf, stream=s.cuda_stream)
+        a.fill_(7.0)  # queued after the copy (the stream waits for the library)
+    s.synchronize()
+    want = x[:n, :n].cpu().numpy()
+    assert np.array_equal(t.to_dense(), want)
+    # the pyramid is the one of the final values
+    assert np.array_equal(t._pyramid()[2], sp.from_dense(want, leaf_size=leaf)._pyramid()[2])
