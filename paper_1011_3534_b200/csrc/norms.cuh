@@ -234,14 +234,15 @@ __device__ __forceinline__ double seg_leaf_norm(const unsigned char *wsm, SegInf
     const int seg = lane + 32 * h;
     const double hi_est = h ? pre1 : pre0, lo_est = hi_est - est[h];
     const double za = lo_est * (1.0 - 0x1p-30), zz = hi_est * (1.0 + 0x1p-30);
-    int ea = 0, ez = 0;
-    frexp(za, &ea);
-    frexp(zz, &ez);
+    // binade exponents (frexp's) from the bits: the estimates are normal
+    // whenever they are used (za > 2^-900, zz < 2^1000)
+    const int ea = (int)((__double_as_longlong(za) >> 52) & 0x7ff) - 1022;
+    const int ez = (int)((__double_as_longlong(zz) >> 52) & 0x7ff) - 1022;
     bool simp = finite[h] && seg > 0 && za > 0x1p-900 && zz < 0x1p+1000 && ea == ez;
     long long d = 0;
     if (simp) {
       const T *sx = reinterpret_cast<const T *>(wsm + seg * SS);
-      const double inv_u = ldexp(1.0, 53 - ea);  // 2^-(E-52), E = ea - 1: exact power of two
+      const double inv_u = pow2_exact(53 - ea);  // 2^-(E-52), E = ea - 1: exact power of two
       bool tie = false;
 #pragma unroll 16
       for (int i = 0; i < L; ++i) {
@@ -264,8 +265,8 @@ __device__ __forceinline__ double seg_leaf_norm(const unsigned char *wsm, SegInf
     long long runD = 0;
     auto close_run = [&](int end) {
       if (run0 < 0) return;
-      const double lo = ldexp(1.0, runE);
-      const double v = acc + (double)runD * ldexp(1.0, runE - 52);  // exact when it applies
+      const double lo = pow2_exact(runE);
+      const double v = acc + (double)runD * pow2_exact(runE - 52);  // exact when it applies
       if (runD < (1ll << 52) && acc >= lo && v < 2.0 * lo) {
         acc = v;  // every partial sum of the run stayed in [2^E, 2^(E+1))
       } else {
