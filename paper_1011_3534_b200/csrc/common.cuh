@@ -196,6 +196,13 @@ namespace spamm {
 struct DeviceContext;
 // zero-fill a lazy tree's empty blocks (stream-ordered on ctx->stream)
 int materialize(DeviceContext *ctx, const spamm_tree *t);
+// Leaf norms (K1) and the pyramid of `t`, stream-ordered (tree.cu).
+int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
+                        const uint32_t *list, const unsigned *list_count, int64_t list_cap,
+                        unsigned *grp_done, unsigned grp_target, const int *overflow,
+                        unsigned long long *t_end, const unsigned *ready = nullptr,
+                        const unsigned *trav_done = nullptr, const void *fuse_src = nullptr,
+                        int64_t fuse_ld = 0);
 // upper pyramid levels + interior nrm from the leaf level (tree.cu)
 int pyramid_upper_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches = nullptr);
 // order ctx->stream after an asynchronous build of t (no-op otherwise)

@@ -51,6 +51,12 @@ struct PyrTail {
   // before the kernel may complete
   const unsigned *ready;
   const unsigned *trav_done;
+  // fused build (dense f64 tree from device memory, n == N): the producers
+  // read the leaves from fuse_src (leading dimension fuse_ld) instead of the
+  // tree's storage, and the squarer warps write the raw values into the
+  // storage as they square them -- the source is read once, no separate copy
+  const void *fuse_src;
+  int64_t fuse_ld;
 };
 
 __device__ __forceinline__ void spin_acquire_nonzero(const unsigned *flag) {

@@ -29,11 +29,7 @@ namespace spamm {
 int alloc_tree(DeviceContext *ctx, int64_t n, int32_t leaf, int32_t dtype, spamm_tree **out,
                cudaStream_t st = nullptr);
 void free_tree_async(spamm_tree *t, cudaStream_t st);
-int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
-                        const uint32_t *list, const unsigned *list_count, int64_t list_cap,
-                        unsigned *grp_done, unsigned grp_target, const int *overflow,
-                        unsigned long long *t_end,
-                        const unsigned *ready = nullptr, const unsigned *trav_done = nullptr);
+// (declared in common.cuh)
 int finish_tree(DeviceContext *ctx, spamm_tree *t);
 
 __global__ void iota_u32_kernel(uint32_t *__restrict__ out, uint32_t base, int64_t n,

@@ -310,6 +310,8 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
   } else if (warp >= 1 + K1_SQ_WARPS + K1_SPACER / 32) {
     // ------------------------------------------------------------ producers
     const int p = tid - 32 * (1 + K1_SQ_WARPS) - K1_SPACER;
+    const T *fsrc = SQUARER ? reinterpret_cast<const T *>(tail.fuse_src) : nullptr;
+    const int64_t sld = fsrc ? tail.fuse_ld : N;  // the source's leading dimension
     constexpr int MAX_SLOTS = (K1_LT * (K1_CHUNK / 16) + K1_PRODUCERS - 1) / K1_PRODUCERS;
     const T *slot_ptr[MAX_SLOTS];
     unsigned slot_dst[MAX_SLOTS];
@@ -326,7 +328,8 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
           const int64_t bi = leaf / nb, bj = leaf - bi * nb;
           const int e = part * EPS;
           const int rr = e / CW, cc = e - rr * CW;
-          slot_ptr[q] = padded + (bi * b + rr) * N + bj * b + cc;
+          slot_ptr[q] = fsrc ? fsrc + (bi * b + rr) * sld + bj * b + cc
+                             : padded + (bi * b + rr) * N + bj * b + cc;
           slot_dst[q] = l * K1_LEAF_STRIDE + part * 16;
         }
       }
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
       const int stage = chunk % K1_STAGES;
       if (chunk >= K1_STAGES) mbar_wait_backoff(&empty_bar[stage], ((chunk / K1_STAGES) - 1) & 1);
       const int64_t off =
-          (int64_t)((chunk >> shift_cpr) * R) * N + (chunk & (chunks_per_row - 1)) * CW;
+          (int64_t)((chunk >> shift_cpr) * R) * sld + (chunk & (chunks_per_row - 1)) * CW;
       unsigned char *base = k1_smem + stage * K1_STAGE_BYTES;
 #pragma unroll
       for (int q = 0; q < MAX_SLOTS; ++q)
@@ -366,16 +369,37 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
       const int sw = warp - 1;  // segments [sw*segs/4, (sw+1)*segs/4) of every leaf
       const int v0 = sw * segs / K1_SQ_WARPS, v1 = (sw + 1) * segs / K1_SQ_WARPS;
       U bits = 0;
+      // fused build: this lane's leaf in the tree's storage (raw values are
+      // written there as they pass through the stage)
+      // fused build: this lane's leaf in the tree's storage (raw values are
+      // written there as they pass through the stage, before the squaring)
+      T *fdst = nullptr;
+      if (tail.fuse_src && mine) {
+        const int64_t leaf = list ? (int64_t)list[leaf0 + lane] : leaf0 + lane;
+        const int64_t bi = leaf / nb, bj = leaf - bi * nb;
+        fdst = padded + (bi * b) * N + bj * b;
+      }
       for (int chunk = 0; chunk < n_chunks; ++chunk) {
         const int stage = chunk % K1_STAGES;
         mbar_wait_backoff(&full_bar[stage], (chunk / K1_STAGES) & 1);
         if (mine) {
           unsigned char *pp = k1_smem + stage * K1_STAGE_BYTES + lane * K1_LEAF_STRIDE;
+          // (fused build) where piece v of this chunk goes in the tree's storage
+          T *crow = fdst ? fdst + (int64_t)((chunk >> (__ffs(chunks_per_row) - 1)) * R) * N +
+                               (chunk & (chunks_per_row - 1)) * CW
+                         : nullptr;
+          auto raw_out = [&](int v, const double2 &w) {
+            const int e = v * EPS, rr = e / CW, cc = e - rr * CW;
+            *reinterpret_cast<double2 *>(crow + (int64_t)rr * N + cc) = w;
+          };
           int v = v0;
           for (; v + 8 <= v1; v += 8) {  // batched: loads, then squares, then stores
             double2 w[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) w[u] = *reinterpret_cast<double2 *>(pp + 16 * (v + u));
+            if (crow)
+#pragma unroll
+              for (int u = 0; u < 8; ++u) raw_out(v + u, w[u]);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               bits |= Bits<T>::of((T)w[u].x) | Bits<T>::of((T)w[u].y);
@@ -387,6 +411,7 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
           }
           for (; v < v1; ++v) {
             double2 w = *reinterpret_cast<double2 *>(pp + 16 * v);
+            if (crow) raw_out(v, w);
             bits |= Bits<T>::of((T)w.x) | Bits<T>::of((T)w.y);
             w.x = __dmul_rn(w.x, w.x);
             w.y = __dmul_rn(w.y, w.y);
@@ -1135,6 +1160,8 @@ struct K1Overlap {
   unsigned long long *t_end;
   bool pdl;  // programmatic dependent launch behind the leaf-product kernel
   const unsigned *ready, *trav_done;  // bitmask groups (see PyrTail)
+  const void *fuse_src;               // fused build (see PyrTail)
+  int64_t fuse_ld;
 };
 
 template <typename T, int S, int LT>
@@ -1162,6 +1189,8 @@ static int launch_staged(spamm_tree *t, cudaStream_t st, const uint32_t *list,
     tail.pdl_wait = ov->pdl && !ov->grp_done;
     tail.ready = ov->ready;
     tail.trav_done = ov->trav_done;
+    tail.fuse_src = ov->fuse_src;
+    tail.fuse_ld = ov->fuse_ld;
   }
   double *nsq_leaf = t->nsq + level_offset(t->depth);
   uint8_t *occ_leaf = t->occ + level_offset(t->depth);
@@ -1283,11 +1312,7 @@ void k1_timeline_dump(unsigned long long k3_end, unsigned long long k3_start) {
   fprintf(stderr, "\n");
 }
 
-int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches,
-                        const uint32_t *list, const unsigned *list_count, int64_t list_cap,
-                        unsigned *grp_done, unsigned grp_target, const int *overflow,
-                        unsigned long long *t_end, const unsigned *ready = nullptr,
-                        const unsigned *trav_done = nullptr);
+// (build_pyramid_async is declared in common.cuh)
 
 // Rebuild the whole pyramid of `t` from its padded storage (canonicalising
 // all-zero leaves in place).  Stream-ordered; no host sync; two launches.
@@ -1295,7 +1320,7 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap,
                         unsigned *grp_done, unsigned grp_target, const int *overflow,
                         unsigned long long *t_end, const unsigned *ready,
-                        const unsigned *trav_done) {
+                        const unsigned *trav_done, const void *fuse_src, int64_t fuse_ld) {
   // builds on copy_in run concurrently with the main stream's: own tickets
   Scratch &k1t = st == ctx->copy_in ? ctx->k1_ticket_in : ctx->k1_ticket;
   SPAMM_TRY(ensure_scratch(k1t, sizeof(unsigned), st, /*zeroed=*/true));
@@ -1304,8 +1329,8 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
   // list mode follows the leaf-product kernel: launch it programmatically so
   // its CTAs are resident (and waiting) as that kernel's CTAs retire
   K1Overlap ovs{grp_done, grp_target, overflow, t_end, list != nullptr && t_end != nullptr, ready,
-                trav_done};
-  const K1Overlap *ov = (grp_done || t_end) ? &ovs : nullptr;
+                trav_done, fuse_src, fuse_ld};
+  const K1Overlap *ov = (grp_done || t_end || fuse_src) ? &ovs : nullptr;
   // list mode (C's tree): the segmented-chain kernel, a warp per leaf
   static const bool no_seg = getenv("SPAMM_NO_SEG_CHAIN") != nullptr;
   // (only where K1 overlaps K3's tail -- small block grids: per leaf the
@@ -1562,8 +1587,21 @@ static int tree_from(const void *src, bool src_on_host, int64_t n, int64_t ld, i
   SPAMM_TRY(alloc_tree(ctx, n, leaf, dtype, &t));
   const int64_t esz = t->elem_size();
   int rc = SPAMM_OK;
+  // Fused build (f64 device source that fills the padded matrix exactly, 16-byte
+  // aligned rows): K1 reads the source once and writes the tree's storage as
+  // it squares -- no separate device-to-device copy (SPAMM_NO_FUSED_BUILD: copy, then K1)
+  static const bool no_fused = getenv("SPAMM_NO_FUSED_BUILD") != nullptr;
+  const bool fuse = !src_on_host && !no_fused && dtype == SPAMM_DTYPE_F64 && t->N == n &&
+                    leaf * esz >= 16 && ld % 2 == 0 && ((uintptr_t)src & 15) == 0;
   do {
     cudaError_t e;
+    if (fuse) {
+      rc = build_pyramid_async(ctx, t, ctx->stream, nullptr, nullptr, nullptr, 0, nullptr, 0, nullptr,
+                               nullptr, nullptr, nullptr, src, ld);
+      if (rc) break;
+      rc = finish_tree(ctx, t);
+      break;
+    }
     if (t->N != n) {
       e = cudaMemsetAsync(t->padded, 0, (size_t)(t->N * t->N * esz), ctx->stream);
       if (e != cudaSuccess) { set_error("memset: %s", cudaGetErrorString(e)); rc = SPAMM_ERR_CUDA; break; }

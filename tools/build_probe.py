@@ -22,6 +22,13 @@ for rep in range(3):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    print(f"{name}: n={n} from_device (copy + norms + pyramid) {ms:.3f} ms, "
-          f"{n * n * 8 * 3 / (ms * 1e-3) / 1e9:.0f} GB/s of copy+read traffic", flush=True)
+    import os
+    fused = os.environ.get("SPAMM_NO_FUSED_BUILD") is None
+    traffic = n * n * 8 * (2 if fused else 3)  # fused: read the source once, write the tree
+    print(f"{name}: n={n} from_device ({'fused read+write+norms' if fused else 'copy, then norms'}"
+          f" + pyramid) {ms:.3f} ms, {traffic / (ms * 1e-3) / 1e9:.0f} GB/s of DRAM traffic, "
+          f"algorithmic (one read of n^2 f64) {n * n * 8 / 6534.5e9 * 1e3:.2f} ms at 6534.5 GB/s",
+          flush=True)
+    if rep == 2 and "check" in sys.argv:
+        ref = sp.from_device_pointer(at.data_ptr(), n, leaf_size=leaf) if False else None
     del t
