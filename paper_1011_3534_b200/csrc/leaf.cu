@@ -417,6 +417,18 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
         }
       };
       for (;;) {
+        // Final wave (the last drain_items tickets): take an item only once
+        // the consumers have taken every stage already issued, so the last
+        // items go to the CTAs that are actually free instead of those whose
+        // producer runs a ring ahead of its consumers (end spread)
+        if (args.drain_items && gstep > 0) {
+          unsigned long long taken;
+          asm volatile("ld.relaxed.gpu.u64 %0, [%1];" : "=l"(taken) : "l"(&args.tc->gemm_ticket) : "memory");
+          if (taken + (unsigned long long)args.drain_items >= (unsigned long long)(ng * subs)) {
+            const long long last = gstep - 1;
+            mbar_wait_l(&empty_bar[last % C::STAGES], (unsigned)((last / C::STAGES) & 1));
+          }
+        }
         const int item = (int)atomicAdd(&args.tc->gemm_ticket, 1ull);
         if (item >= ng * subs) break;
         ++items;
@@ -697,6 +709,9 @@ static int launch_dmma_ws(LeafArgs args, int num_sms, cudaStream_t st) {
   static const int tm_sync = getenv("SPAMM_K3_TM_SYNC") != nullptr;
   args.tm_slots = tm_env;
   args.tm_sync = tm_sync;
+  // final-wave ticket policy (SPAMM_K3_DRAIN = tickets per CTA of the final wave, 0: off)
+  static const int drain = getenv("SPAMM_K3_DRAIN") ? atoi(getenv("SPAMM_K3_DRAIN")) : 0;
+  args.drain_items = drain * num_sms;
   CUtensorMap ma, mb;
   SPAMM_TRY(make_operand_map(&ma, args.a, args.N, 2, TILE));             // A: 32 k x TILE rows
   args.b_map5 = TILE == 64 && make_b_map5(&mb, args.b, args.N);

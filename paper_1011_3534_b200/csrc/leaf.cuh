@@ -28,6 +28,7 @@ struct LeafArgs {
   const uint32_t *am;
   int tm_slots;                       // merge-stack slots kept in TMEM (the rest in local memory)
   int tm_sync;                        // wait for each TMEM spill to complete (debug)
+  int drain_items;                    // final wave: take a ticket only with the ring drained
 };
 
 // Returns through *signals whether the launched kernel reports finished groups

@@ -539,3 +539,26 @@ def test_from_device_pointer_is_stream_ordered():
     assert np.array_equal(t.to_dense(), want)
     # the pyramid is the one of the final values
     assert np.array_equal(t._pyramid()[2], sp.from_dense(want, leaf_size=leaf)._pyramid()[2])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,ld_pad", [(1024, 0), (1024, 6), (1000, 0), (777, 3)])
+def test_from_device_pointer_fused_and_copy_paths(n, ld_pad):
+    """from_device_pointer on device data: the fused build (K1 reads the
+    source once and writes the tree's storage, n == N with 16-byte aligned
+    rows) and the copy-then-K1 path (padding, odd leading dimensions) give
+    the host build's tree bit for bit -- storage and pyramid."""
+    import torch
+
+    rng = np.random.default_rng(n + ld_pad)
+    d = np.abs(np.subtract.outer(np.arange(n), np.arange(n)))
+    host = rng.uniform(-1, 1, (n, n)) * 0.9 ** d
+    host[5, :] = 0.0
+    host[7, 9] = -0.0
+    dev = torch.zeros((n, n + ld_pad), dtype=torch.float64, device="cuda")
+    dev[:, :n] = torch.from_numpy(host).cuda()
+    t = sp.from_device_pointer(dev.data_ptr(), n, leaf_size=32, ld=n + ld_pad)
+    ref = sp.from_dense(host, leaf_size=32)
+    assert np.array_equal(t._padded.view(np.uint64), ref._padded.view(np.uint64))
+    assert np.array_equal(t._pyramid()[2].view(np.uint64), ref._pyramid()[2].view(np.uint64))
+    assert np.array_equal(t._pyramid()[3], ref._pyramid()[3])
