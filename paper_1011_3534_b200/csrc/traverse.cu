@@ -850,39 +850,7 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   const uint8_t *__restrict__ occ_a = a.occ_a;
   const uint8_t *__restrict__ occ_b = a.occ_b;
 
-  // the previous call's counters and work set were read back / consumed
-  // already: leave them zero for the call after this one
-  for (int x = blockIdx.x * DN_THREADS + threadIdx.x; x < (int)(sizeof(TraverseCounters) / 8);
-       x += nblocks * DN_THREADS)
-    reinterpret_cast<unsigned long long *>(a.tc_clear)[x] = 0ull;
-  for (uint64_t x = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x; x < a.dn_work_words;
-       x += (uint64_t)nblocks * DN_THREADS)
-    a.dn_masks_clear[x] = 0u;
-  for (int x = threadIdx.x; x < (D + 1) * 4; x += DN_THREADS) (&s_cnt[0][0])[x] = 0u;
-  // the operands' pyramid tops (levels 0..U: the warp-uniform tiers), staged
-  // once per CTA -- those tiers' verdicts then cost shared-memory reads
-  constexpr int U = D >= 2 ? D - 2 : -1;
-  constexpr int TOPN = U >= 0 ? (int)level_offset(U + 1) : 1;
-  static_assert(TOPN <= PREFIX_ENTRIES, "pyramid top exceeds the staging area");
-  double *s_top_na = sh.u.top.nrm_a, *s_top_nb = sh.u.top.nrm_b;  // (sh.u is free until the barrier)
-  uint8_t *s_top_oa = sh.u.top.occ_a, *s_top_ob = sh.u.top.occ_b;
-  if (U >= 0)
-    for (int e = threadIdx.x; e < TOPN; e += DN_THREADS) {
-      s_top_na[e] = __ldg(nrm_a + e);
-      s_top_nb[e] = __ldg(nrm_b + e);
-      s_top_oa[e] = __ldg(occ_a + e);
-      s_top_ob[e] = __ldg(occ_b + e);
-    }
-  __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) tc->phase_ns[2] = globaltimer() - t_entry;  // (durations)
-
-  // ---------------- phase 1: classify every leaf triple and its ancestors
-  // Tiers t <= U have one ancestor per 64 consecutive x, so a warp's 32
-  // lanes share it: those verdicts are warp-uniform and a warp whose tier-U
-  // ancestor is not active leaves after them.
-  unsigned wc[D + 1][4];
-#pragma unroll
-  for (int t = 0; t <= D; ++t) wc[t][0] = wc[t][1] = wc[t][2] = wc[t][3] = 0u;
+  constexpr int U = D >= 2 ? D - 2 : -1;  // tiers <= U are warp-uniform (see phase 1)
   // Per-lane tiers T0..D read the operands' lower pyramid levels from L2;
   // those loads do not depend on the verdicts, so the next x's are issued
   // before this x is classified (one memory round trip per thread, not one
@@ -909,7 +877,43 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   const uint64_t x_stride = (uint64_t)nblocks * DN_THREADS;
   LaneOps cur;
   uint64_t x = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x;
+  // the first x's operand loads go out before anything else: their DRAM
+  // latency (the L2 is cold after a flush) overlaps the clears and the
+  // staging of the pyramid tops below
   if (x < N_X32) load_lane(x, cur);
+
+  // the previous call's counters and work set were read back / consumed
+  // already: leave them zero for the call after this one
+  for (int x = blockIdx.x * DN_THREADS + threadIdx.x; x < (int)(sizeof(TraverseCounters) / 8);
+       x += nblocks * DN_THREADS)
+    reinterpret_cast<unsigned long long *>(a.tc_clear)[x] = 0ull;
+  for (uint64_t x = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x; x < a.dn_work_words;
+       x += (uint64_t)nblocks * DN_THREADS)
+    a.dn_masks_clear[x] = 0u;
+  for (int x = threadIdx.x; x < (D + 1) * 4; x += DN_THREADS) (&s_cnt[0][0])[x] = 0u;
+  // the operands' pyramid tops (levels 0..U: the warp-uniform tiers), staged
+  // once per CTA -- those tiers' verdicts then cost shared-memory reads
+  constexpr int TOPN = U >= 0 ? (int)level_offset(U + 1) : 1;
+  static_assert(TOPN <= PREFIX_ENTRIES, "pyramid top exceeds the staging area");
+  double *s_top_na = sh.u.top.nrm_a, *s_top_nb = sh.u.top.nrm_b;  // (sh.u is free until the barrier)
+  uint8_t *s_top_oa = sh.u.top.occ_a, *s_top_ob = sh.u.top.occ_b;
+  if (U >= 0)
+    for (int e = threadIdx.x; e < TOPN; e += DN_THREADS) {
+      s_top_na[e] = __ldg(nrm_a + e);
+      s_top_nb[e] = __ldg(nrm_b + e);
+      s_top_oa[e] = __ldg(occ_a + e);
+      s_top_ob[e] = __ldg(occ_b + e);
+    }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) tc->phase_ns[2] = globaltimer() - t_entry;  // (durations)
+
+  // ---------------- phase 1: classify every leaf triple and its ancestors
+  // Tiers t <= U have one ancestor per 64 consecutive x, so a warp's 32
+  // lanes share it: those verdicts are warp-uniform and a warp whose tier-U
+  // ancestor is not active leaves after them.
+  unsigned wc[D + 1][4];
+#pragma unroll
+  for (int t = 0; t <= D; ++t) wc[t][0] = wc[t][1] = wc[t][2] = wc[t][3] = 0u;
   for (; x < N_X32; x += x_stride) {
     LaneOps nxt;
     if (x + x_stride < N_X32) load_lane(x + x_stride, nxt);
