@@ -1008,17 +1008,21 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
     cur = nxt;
     if (blockIdx.x == 0 && threadIdx.x == 0 && x < 4 * x_stride) tc->phase_ns[3 + x / x_stride] = globaltimer() - t_entry;
   }
+  // per-warp counters (lane 0 holds them) -> shared memory, then one thread
+  // per counter sums the warps (no shared atomics in a chain)
+  __shared__ unsigned s_wc[DN_THREADS / 32][(D + 1) * 4];
   if (lane == 0) {
 #pragma unroll
     for (int t = 0; t <= D; ++t)
 #pragma unroll
-      for (int f = 0; f < 4; ++f)
-        if (wc[t][f]) atomicAdd(&s_cnt[t][f], wc[t][f]);
+      for (int f = 0; f < 4; ++f) s_wc[warp][t * 4 + f] = wc[t][f];
   }
   __syncthreads();
   // CTA totals into one of DN_PARTS copies (spreads the global atomics)
   for (int x = threadIdx.x; x < (D + 1) * 4; x += DN_THREADS) {
-    const unsigned v = (&s_cnt[0][0])[x];
+    unsigned v = 0;
+#pragma unroll
+    for (int w = 0; w < DN_THREADS / 32; ++w) v += s_wc[w][x];
     if (v) atomicAdd(&tc->dn_part[blockIdx.x % DN_PARTS][x / 4][x % 4], (unsigned long long)v);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
