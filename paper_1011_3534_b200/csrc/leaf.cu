@@ -834,7 +834,7 @@ constexpr size_t SG_SMEM = sizeof(float) * 2 * (SG_A_FLOATS + SG_B_FLOATS);
 
 // TM x TN outputs per thread (64 / TN threads across, 64 / TM down).
 template <int TM, int TN>
-__global__ void __launch_bounds__(4096 / (TM * TN)) leaf_sgemm_kernel(LeafArgs args) {
+__global__ void __launch_bounds__(4096 / (TM * TN), 512 / (4096 / (TM * TN)) < 3 ? 1 : 3) leaf_sgemm_kernel(LeafArgs args) {
   constexpr int THREADS = 4096 / (TM * TN), NX = 64 / TN;
   constexpr int PER = 1024 / THREADS;  // float4 pieces per thread per operand tile
   extern __shared__ __align__(16) float sg_smem[];
@@ -847,7 +847,6 @@ __global__ void __launch_bounds__(4096 / (TM * TN)) leaf_sgemm_kernel(LeafArgs a
   const float *__restrict__ B = (const float *)args.b;
   float *__restrict__ Cm = (float *)args.c;
   float stk[MAXD][TM * TN];
-  int ops[MAXD];
   WorkItem w;
   while (fetch_work(args, subs_side, &s_work, w)) {
     const int64_t nk = w.end - w.start;
@@ -892,7 +891,7 @@ __global__ void __launch_bounds__(4096 / (TM * TN)) leaf_sgemm_kernel(LeafArgs a
     float acc[TM * TN];
 #pragma unroll
     for (int e = 0; e < TM * TN; ++e) acc[e] = 0.f;
-    int sp = 0;
+    uint32_t pending = 0;
     load(0);
     store(0);
     __syncthreads();
@@ -928,22 +927,26 @@ __global__ void __launch_bounds__(4096 / (TM * TN)) leaf_sgemm_kernel(LeafArgs a
       __syncthreads();
       const int64_t s = step / kchunks;
       if (step - s * kchunks == kchunks - 1) {  // product P_k complete: merge in tree order
+        // the stack's merge levels as a bit set (they increase downwards, so
+        // the top is the lowest set bit and the depth is the popcount): no
+        // local-memory level array in the pop loop's condition
         const uint32_t k = args.ks[w.start + s];
-        int h = 99;
-        if (s + 1 < nk) h = merge_level(k, args.ks[w.start + s + 1]);
-        while (sp > 0 && ops[sp - 1] < h) {
-          --sp;
+        const bool has_next = s + 1 < nk;
+        const int h = has_next ? merge_level(k, args.ks[w.start + s + 1]) : 32;
+        while (pending && (__ffs(pending) - 1) < h) {
+          const int top = __popc(pending) - 1;
 #pragma unroll
-          for (int e = 0; e < TM * TN; ++e) acc[e] = stk[sp][e] + acc[e];
+          for (int e = 0; e < TM * TN; ++e) acc[e] = stk[top][e] + acc[e];
+          pending &= pending - 1;
         }
-        if (s + 1 < nk) {
+        if (has_next) {
+          const int slot = __popc(pending);
 #pragma unroll
           for (int e = 0; e < TM * TN; ++e) {
-            stk[sp][e] = acc[e];
+            stk[slot][e] = acc[e];
             acc[e] = 0.f;
           }
-          ops[sp] = h;
-          ++sp;
+          pending |= 1u << h;
         }
       }
     }
