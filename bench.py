@@ -308,7 +308,23 @@ def run_b200(args, cfg_name):
 
     dev_cfg = cfg_name in workloads.DEVICE_CONFIGS
     tdtype = torch.float32 if args.dtype == "f32" else torch.float64
-    if dev_cfg:  # generated on the GPU (c5: > 100 GB of host staging otherwise)
+    # c5 (one multiply per step) under torchrun: the distributed layout --
+    # rank 0 generates A, ShardedTree.scatter sends each rank its block rows
+    # (NCCL), every multiply is spamm_sharded (plan, halo exchange of the
+    # operand blocks other ranks hold, band products, merged statistics)
+    sharded = dev_cfg and use_dist
+    A_sh = None
+    if sharded:
+        cfgd = workloads.DEVICE_CONFIGS[cfg_name]
+        n, leaf, taus = cfgd["n"], cfgd["leaf"], list(cfgd["taus"])
+        at = (workloads.make_config_device(cfg_name, f"cuda:{local}", tdtype)[0]
+              if rank == 0 else None)
+        A_sh = spd.ShardedTree.scatter(at, n, leaf, spd.Comm(), dtype=tdtype)
+        del at
+        torch.cuda.empty_cache()
+        a = b = A_sh.tree
+        a_host = b_host = None
+    elif dev_cfg:  # generated on the GPU (c5: > 100 GB of host staging otherwise)
         at, _, leaf, taus = workloads.make_config_device(cfg_name, f"cuda:{local}", tdtype)
         n = at.shape[0]
         a_host = b_host = None
@@ -335,7 +351,7 @@ def run_b200(args, cfg_name):
     # collective in the data path)
     pieces = [(q, None) for q in range(len(taus))]
     plan_desc = None
-    if use_dist:
+    if use_dist and not sharded:
         row_counts = []
         for tau in taus:
             _, _, det = sp.spamm_detailed(a, b, sp.SpammConfig(tau=tau), keep_triples=True)
@@ -351,6 +367,26 @@ def run_b200(args, cfg_name):
             tau = taus[q]
             flush.zero_()
             torch.cuda.synchronize()
+            if sharded:  # the whole distributed multiply, timed on the device around the call
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                c, st, det = spd.spamm_sharded(A_sh, A_sh, sp.SpammConfig(tau=tau))
+                e1.record()
+                torch.cuda.synchronize()
+                # (st: the global statistics; count each rank's share once in the sum below)
+                f += leaf_flops(leaf, st.leaf_matmuls) / world
+                ms += e0.elapsed_time(e1)
+                gemm += det.ms_gemm if det is not None else 0.0
+                launches += det.kernel_launches if det is not None else 0
+                per_tau.append((tau, st.leaf_matmuls, e0.elapsed_time(e1),
+                                det.ms_gemm if det is not None else 0.0,
+                                det.ms_cull if det is not None else 0.0,
+                                det.ms_ctree if det is not None else 0.0,
+                                det.n_groups if det is not None else 0,
+                                int(det.tier_survivors[-1]) if det is not None and det.tier_survivors
+                                else 0))
+                del c
+                continue
             c, st, det = sp.spamm_detailed(a, b, sp.SpammConfig(tau=tau), rows=rows)
             f += leaf_flops(leaf, st.leaf_matmuls)
             ms += det.ms_total
@@ -395,12 +431,13 @@ def run_b200(args, cfg_name):
     table = [{"tau": t, "retained": r, "frac_of_nb3": r / (a.block_grid ** 3), "ms": m,
               "gemm_ms": g, "cull_ms": cu, "ctree_ms": ct, "c_blocks": ng,
               "tflops": leaf_flops(leaf, r) / (m * 1e-3) / 1e12}
-             for (t, r, m, g, cu, ct, ng) in per_tau_all[-1]]
+             for (t, r, m, g, cu, ct, ng, *_) in per_tau_all[-1]]
 
     f64_tensor = args.dtype == "f64" and leaf >= 32
     peak, peak_src = fp64_peak() if f64_tensor else fp32_peak()
     # K3 roofline from this rank's own flops and K3 event time
-    local_f = sum(leaf_flops(leaf, x[1]) for step in per_tau_all for x in step)
+    # (sharded: this rank's own retained triples, the last tier's survivors)
+    local_f = sum(leaf_flops(leaf, x[7] if len(x) > 7 else x[1]) for step in per_tau_all for x in step)
     local_gemm = sum(x[3] for step in per_tau_all for x in step)
     achieved = local_f / (local_gemm * 1e-3) / 1e12 if local_gemm > 0 else 0.0
     traffic = k3_traffic()
@@ -422,7 +459,11 @@ def run_b200(args, cfg_name):
                  if dev_cfg else "synthetic (seeded numpy PCG64, SURVEY §8(d))"),
         "config": {"workload": workload_string(cfg_name, n, leaf, taus),
                    "l2": "flushed (256 MiB write) before every multiply",
-                   "parallelism": (f"tau sweep partitioned over {world} ranks: each tau whole or "
+                   "parallelism": (f"row-distributed over {world} ranks (ShardedTree: rows scattered "
+                                   f"from rank 0 over NCCL, per multiply a halo exchange of the "
+                                   f"operand blocks other ranks hold, C kept as bands)"
+                                   if sharded else
+                                   f"tau sweep partitioned over {world} ranks: each tau whole or "
                                    f"split into C block-row shards (no data-path collective)"
                                    if use_dist else "single GPU"),
                    "plan": plan_desc,

@@ -141,14 +141,15 @@ def morton_keys(tier_ijk):
     """i-major interleave of (i, j, k) -- a candidate's position in its tier's
     breadth-first list (children (di, dj, dk) = 000..111, multiply.py:35-37)."""
     t = np.asarray(tier_ijk, dtype=np.int64).reshape(-1, 4)
-    key = np.zeros(len(t), np.uint64)
-    i, j, k = (t[:, q].astype(np.uint64) for q in (1, 2, 3))
-    for bit in range(21):
-        b = np.uint64(bit)
-        key |= ((i >> b) & np.uint64(1)) << np.uint64(3 * bit + 2)
-        key |= ((j >> b) & np.uint64(1)) << np.uint64(3 * bit + 1)
-        key |= ((k >> b) & np.uint64(1)) << np.uint64(3 * bit)
-    return key
+
+    def spread3(x):  # bit b of a 21-bit x -> bit 3b
+        x = x.astype(np.uint64) & np.uint64(0x1FFFFF)
+        for shift, mask in ((32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF), (8, 0x100F00F00F00F00F),
+                            (4, 0x10C30C30C30C30C3), (2, 0x1249249249249249)):
+            x = (x | (x << np.uint64(shift))) & np.uint64(mask)
+        return x
+
+    return (spread3(t[:, 1]) << np.uint64(2)) | (spread3(t[:, 2]) << np.uint64(1)) | spread3(t[:, 3])
 
 
 def merge_pruned(parts):
@@ -619,6 +620,14 @@ def spamm_sharded(a, b, config=None, keep_triples=False):
     assert b.band == a.band, "operands must share the row partition"
     nb = a.block_grid
     halo = 0
+    if comm.world == 1:
+        # one rank holds every row: no exchange, its statistics are the global ones
+        c_tree, st, det = spamm_detailed(a.tree, b.tree, config, keep_triples=keep_triples,
+                                         rows=(lo, hi))
+        c = ShardedTree.from_product(c_tree, (lo, hi), comm)
+        if det is not None:
+            det.halo_bytes = 0
+        return c, st, det
     if hi > lo:
         # plan: the B blocks this band's retained triples read
         _, _, plan = spamm_detailed(a.tree, b.tree, replace_cfg(config), keep_triples=True,

@@ -178,3 +178,22 @@ def test_sharded_budget_is_bit_identical(tmp_path, world):
     assert np.array_equal(np.load(tmp_path / "merged.npy"), want)
     bands = np.load(tmp_path / "bands.npy")
     assert bands[0][0] == 0 and bands[-1][1] == 64
+
+
+def test_morton_keys_match_bitwise_interleave():
+    """distributed.morton_keys (magic-number spreads) equals the i-major
+    bit-by-bit interleave of (i, j, k) -- the candidate order inside a tier
+    (multiply.py:35-37) the merged pruned list follows."""
+    from paper_1011_3534_b200 import distributed as spd
+
+    rng = np.random.default_rng(0)
+    t = np.c_[rng.integers(0, 12, 4000), rng.integers(0, 2 ** 21, (4000, 3))]
+    want = []
+    for _, i, j, k in t.tolist():
+        key = 0
+        for bit in range(21):
+            key |= ((i >> bit) & 1) << (3 * bit + 2)
+            key |= ((j >> bit) & 1) << (3 * bit + 1)
+            key |= ((k >> bit) & 1) << (3 * bit)
+        want.append(key)
+    assert np.array_equal(spd.morton_keys(t), np.array(want, dtype=np.uint64))
