@@ -88,6 +88,10 @@ extern "C" {
  * order (spamm_product_pruned): the multi-GPU budget merges the shards' lists
  * into the single-GPU order and sums them with the reference's pairwise sum. */
 #define SPAMM_KEEP_PRUNED 0x40u
+/* The B blocks (k, j) the retained triples read, as a bitmask over the block
+ * grid (bit k * nb + j), formed on the device (spamm_product_need_blocks):
+ * the multi-GPU plan without copying the retained triples off the device. */
+#define SPAMM_NEED_BLOCKS 0x80u
 
 typedef struct spamm_tree spamm_tree;
 typedef struct spamm_product spamm_product;
@@ -262,6 +266,9 @@ SPAMM_API int spamm_product_triples(const spamm_product *p, int32_t *out, int64_
 SPAMM_API int spamm_product_pruned(const spamm_product *p, int32_t *tier_ijk, double *np_out,
                                    int64_t capacity);
 SPAMM_API int64_t spamm_product_pruned_count(const spamm_product *p);
+/* SPAMM_NEED_BLOCKS: (nb*nb + 31) / 32 words, bit k * nb + j set when a
+ * retained triple (i, j, k) reads B block (k, j). */
+SPAMM_API int spamm_product_need_blocks(const spamm_product *p, uint32_t *out, int64_t nwords);
 SPAMM_API void spamm_product_free(spamm_product *p);
 
 /* -- row bands of distributed matrices (multi-GPU; csrc/shard.cu) ------------

@@ -30,6 +30,7 @@ KEEP_TRIPLES = 0x8
 TIERED_TRAVERSAL = 0x10
 TRAVERSE_ONLY = 0x20
 KEEP_PRUNED = 0x40
+NEED_BLOCKS = 0x80
 
 # every symbol include/spamm_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
@@ -48,6 +49,7 @@ EXPORTED = (
     "spamm_tree_blocks_gather_device", "spamm_tree_blocks_scatter_device",
     "spamm_tree_diagonal_rows", "spamm_tc2_update",
     "spamm_stream_wait", "spamm_stream_signal", "spamm_tree_from_device_on", "spamm_multiply_on",
+    "spamm_product_need_blocks",
 )
 
 
@@ -132,6 +134,7 @@ def load(path=LIB_PATH):
         L.spamm_product_pruned.argtypes = [vp, vp, vp, i64]
         L.spamm_product_pruned_count.argtypes = [vp]
         L.spamm_product_pruned_count.restype = i64
+        L.spamm_product_need_blocks.argtypes = [vp, vp, i64]
         L.spamm_tree_band_from_device.argtypes = [vp, i64, i64, i32, i32, i64, i64, i32, pp]
         L.spamm_tree_band_set.argtypes = [vp, i64, i64]
         L.spamm_tree_pyramid_rebuild.argtypes = [vp]

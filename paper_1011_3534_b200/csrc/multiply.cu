@@ -23,6 +23,7 @@ struct spamm_product {
   std::vector<int32_t> triples;  // 3 per retained leaf product: i, j, k
   std::vector<int32_t> pruned;   // 4 per tau-pruned call: tier, i, j, k (SPAMM_KEEP_PRUNED)
   std::vector<double> pruned_np; // its norm product rn(rn(sqrt a) rn(sqrt b))
+  std::vector<uint32_t> need;    // SPAMM_NEED_BLOCKS: bit k * nb + j per B block read
 };
 
 namespace spamm {
@@ -68,6 +69,39 @@ static int check_conformable(const spamm_tree *a, const spamm_tree *b) {
       break;                                                                            \
     }                                                                                   \
   }
+
+// The B blocks (k, j) read by the retained triples, as a bitmask (bit
+// k * nb + j) -- from the k lists (one warp per group) ...
+__global__ void need_blocks_ks_kernel(const uint32_t *__restrict__ group_ids,
+                                      const uint32_t *__restrict__ group_starts,
+                                      const uint32_t *__restrict__ ks, unsigned ng, uint64_t m,
+                                      int64_t nb, uint32_t *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (unsigned g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ng;
+       g += (gridDim.x * blockDim.x) >> 5) {
+    const int64_t j = group_ids[g] % nb;
+    const uint64_t s0 = group_starts[g], s1 = g + 1 < ng ? group_starts[g + 1] : m;
+    for (uint64_t s = s0 + lane; s < s1; s += 32) {
+      const uint64_t bit = (uint64_t)ks[s] * nb + j;
+      atomicOr(out + (bit >> 5), 1u << (bit & 31));
+    }
+  }
+}
+// ... or from the dense traversal's retained-triple bitmask (Morton order)
+__global__ void need_blocks_am_kernel(const uint32_t *__restrict__ am, int64_t words, int64_t nb,
+                                      uint32_t *__restrict__ out) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t bits = am[w];
+    while (bits) {
+      const uint32_t x = (uint32_t)(w * 32) + (uint32_t)(__ffs(bits) - 1);
+      bits &= bits - 1;
+      const uint64_t j = compact3(x >> 1), k = compact3(x);
+      const uint64_t bit = k * nb + j;
+      atomicOr(out + (bit >> 5), 1u << (bit & 31));
+    }
+  }
+}
 
 static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, uint32_t flags,
                          int64_t row_lo, int64_t row_hi, spamm_tree **c_out, spamm_stats *stats,
@@ -566,6 +600,33 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
                                                (int32_t)ks[x]});
       }
     }
+    if ((flags & SPAMM_NEED_BLOCKS) && e == cudaSuccess) {
+      // the B blocks the retained triples read, formed on the device from the
+      // traversal's lists (still in the context's scratch)
+      const size_t nwords = (size_t)((G + 31) / 32);
+      p->need.assign(nwords, 0u);
+      int zr = ensure_scratch(ctx->reduce_tmp, nwords * sizeof(uint32_t), st);
+      if (!zr && m) zr = zero_async(ctx->reduce_tmp.ptr, nwords * sizeof(uint32_t), st, ctx->num_sms);
+      if (zr) {
+        free_tree_async(c, st);
+        return zr;
+      }
+      uint32_t *need = (uint32_t *)ctx->reduce_tmp.ptr;
+      if (m && ctx->last_bitmask) {
+        const int64_t words = (int64_t)dense_retained_words(depth);
+        need_blocks_am_kernel<<<(unsigned)std::min<int64_t>((words + 255) / 256, 4 * ctx->num_sms),
+                                256, 0, st>>>((const uint32_t *)ctx->dn_retained.ptr, words, nb, need);
+      } else if (m) {
+        const size_t gcap = std::min<size_t>(ctx->cull_capacity, G);
+        need_blocks_ks_kernel<<<4 * ctx->num_sms, 256, 0, st>>>(
+            (const uint32_t *)ctx->group_starts.ptr, (const uint32_t *)ctx->group_starts.ptr + gcap,
+            (const uint32_t *)ctx->keys[1].ptr, (unsigned)s.n_groups, (uint64_t)m, nb, need);
+      }
+      e = cudaGetLastError();
+      if (m && e == cudaSuccess)
+        e = cudaMemcpyAsync(p->need.data(), need, nwords * sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    }
     if (e != cudaSuccess) {
       free_tree_async(c, st);
       set_error("copy of product records: %s", cudaGetErrorString(e));
@@ -643,6 +704,14 @@ int spamm_product_pruned(const spamm_product *p, int32_t *tier_ijk, double *np_o
 
 int64_t spamm_product_pruned_count(const spamm_product *p) {
   return p ? (int64_t)p->pruned_np.size() : 0;
+}
+
+int spamm_product_need_blocks(const spamm_product *p, uint32_t *out, int64_t nwords) {
+  if (!p) { set_error("null product"); return SPAMM_ERR_VALUE; }
+  if (p->need.empty()) { set_error("product kept no needed-block set (SPAMM_NEED_BLOCKS)"); return SPAMM_ERR_VALUE; }
+  if (nwords < (int64_t)p->need.size()) { set_error("need buffer too small"); return SPAMM_ERR_VALUE; }
+  std::copy(p->need.begin(), p->need.end(), out);
+  return SPAMM_OK;
 }
 
 void spamm_product_free(spamm_product *p) { delete p; }

@@ -630,10 +630,10 @@ def spamm_sharded(a, b, config=None, keep_triples=False):
         return c, st, det
     if hi > lo:
         # plan: the B blocks this band's retained triples read
-        _, _, plan = spamm_detailed(a.tree, b.tree, replace_cfg(config), keep_triples=True,
-                                    rows=(lo, hi), traverse_only=True)
-        tr = plan.triples
-        needed = tr[:, 2].astype(np.int64) * nb + tr[:, 1] if len(tr) else np.zeros(0, np.int64)
+        # (a bitmask over the block grid formed on the device: no triples copied)
+        _, _, plan = spamm_detailed(a.tree, b.tree, replace_cfg(config), rows=(lo, hi),
+                                    traverse_only=True, need_blocks=True)
+        needed = np.flatnonzero(plan.need_blocks).astype(np.int64)
     else:
         needed = np.zeros(0, np.int64)
     halo = halo_exchange(b, needed, comm)

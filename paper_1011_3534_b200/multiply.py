@@ -95,9 +95,11 @@ class MultiplyDetail:
     pruned: np.ndarray | None = None        # (p, 4) int32 (tier, i, j, k), keep_pruned
     pruned_np: np.ndarray | None = None     # (p,) their norm products, reference order
     halo_bytes: int = 0                     # operand bytes fetched (distributed multiply)
+    need_blocks: np.ndarray | None = None   # (nb*nb,) bool: B block (k, j) read at [k*nb+j]
 
 
-def _flags(config, keep_triples, traversal="auto", traverse_only=False, keep_pruned=False):
+def _flags(config, keep_triples, traversal="auto", traverse_only=False, keep_pruned=False,
+           need_blocks=False):
     if traversal not in ("auto", "tiered"):
         raise ValueError(f"traversal must be 'auto' or 'tiered', got {traversal!r}")
     f = _lib.TIERED_TRAVERSAL if traversal == "tiered" else 0
@@ -105,6 +107,8 @@ def _flags(config, keep_triples, traversal="auto", traverse_only=False, keep_pru
         f |= _lib.TRAVERSE_ONLY
     if keep_pruned:
         f |= _lib.KEEP_PRUNED
+    if need_blocks:
+        f |= _lib.NEED_BLOCKS
     if config.collect_boxes:
         f |= _lib.COLLECT_BOXES
     if config.count_stats:
@@ -117,7 +121,7 @@ def _flags(config, keep_triples, traversal="auto", traverse_only=False, keep_pru
 
 
 def spamm_detailed(a, b, config=None, keep_triples=False, rows=None, traversal="auto",
-                   traverse_only=False, keep_pruned=False):
+                   traverse_only=False, keep_pruned=False, need_blocks=False):
     """spamm() plus a MultiplyDetail (retained triples, per-tier counts,
     device timings).  ``rows=(lo, hi)`` restricts the product to C leaf block
     rows [lo, hi) -- the shard of one rank in the multi-GPU layout.
@@ -125,7 +129,9 @@ def spamm_detailed(a, b, config=None, keep_triples=False, rows=None, traversal="
     the dense single-pass kernel applies (depth <= 6); results are identical.
     ``traverse_only``: the traversal alone (no product; C is None) -- the
     multi-GPU plan.  ``keep_pruned``: the pruned calls and their norm
-    products in reference order (detail.pruned / pruned_np)."""
+    products in reference order (detail.pruned / pruned_np).  ``need_blocks``:
+    the B blocks the retained triples read (detail.need_blocks), formed on
+    the device -- the multi-GPU plan without the triples' device->host copy."""
     _require_conformable(a, b)
     if config is None:
         config = SpammConfig()
@@ -133,7 +139,7 @@ def spamm_detailed(a, b, config=None, keep_triples=False, rows=None, traversal="
     c = ctypes.c_void_p()
     prod = ctypes.c_void_p()
     st = _lib.Stats()
-    flags = _flags(config, keep_triples, traversal, traverse_only, keep_pruned)
+    flags = _flags(config, keep_triples, traversal, traverse_only, keep_pruned, need_blocks)
     if rows is None:
         _lib.check(L.spamm_multiply(a._handle, b._handle, float(config.tau), flags,
                                     ctypes.byref(c), ctypes.byref(st), ctypes.byref(prod)))
@@ -174,6 +180,12 @@ def spamm_detailed(a, b, config=None, keep_triples=False, rows=None, traversal="
             if m:
                 _lib.check(L.spamm_product_pruned(prod, detail.pruned.ctypes.data,
                                                   detail.pruned_np.ctypes.data, m))
+        if need_blocks:
+            nb = a.block_grid
+            words = np.empty((nb * nb + 31) // 32, np.uint32)
+            _lib.check(L.spamm_product_need_blocks(prod, words.ctypes.data, words.size))
+            detail.need_blocks = np.unpackbits(words.view(np.uint8), bitorder="little")[:nb * nb] \
+                .astype(bool)
     finally:
         if prod.value:
             L.spamm_product_free(prod)

@@ -562,3 +562,26 @@ def test_from_device_pointer_fused_and_copy_paths(n, ld_pad):
     assert np.array_equal(t._padded.view(np.uint64), ref._padded.view(np.uint64))
     assert np.array_equal(t._pyramid()[2].view(np.uint64), ref._pyramid()[2].view(np.uint64))
     assert np.array_equal(t._pyramid()[3], ref._pyramid()[3])
+
+
+@pytest.mark.parametrize("traversal", ["auto", "tiered"])
+@pytest.mark.parametrize("dtype,leaf", [(np.float64, 32), (np.float32, 32), (np.float64, 16)])
+def test_need_blocks_match_retained_triples(traversal, dtype, leaf):
+    """The device-formed plan (SPAMM_NEED_BLOCKS) is exactly the set of B
+    blocks (k, j) the retained triples read, whole product and row bands,
+    dense (bitmask groups) and tiered traversals."""
+    a, b = _exp_pair(1024, 0.05, 0.08)
+    ta = sp.from_dense(a.astype(dtype), leaf_size=leaf)
+    tb = sp.from_dense(b.astype(dtype), leaf_size=leaf)
+    nb = ta.block_grid
+    for rows in (None, (0, nb), (3, nb // 2 + 1), (nb - 1, nb)):
+        for tau in (1e-9, 1e-4, 10.0):
+            for trav_only in (True, False):
+                _, _, det = sp.spamm_detailed(ta, tb, sp.SpammConfig(tau=tau), keep_triples=True,
+                                              rows=rows, traversal=traversal,
+                                              traverse_only=trav_only, need_blocks=True)
+                want = np.zeros(nb * nb, bool)
+                tr = det.triples
+                want[tr[:, 2].astype(np.int64) * nb + tr[:, 1]] = True
+                assert det.need_blocks.shape == (nb * nb,)
+                assert np.array_equal(det.need_blocks, want), (rows, tau, trav_only)
