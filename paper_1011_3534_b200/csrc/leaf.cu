@@ -143,6 +143,18 @@ __device__ __forceinline__ void mbar_wait_l(uint64_t *bar, unsigned parity) {
       : "memory");
 }
 
+// try_wait with a suspend-time hint: the waiting thread is parked until the
+// phase completes (or the hint elapses) instead of re-issuing the test --
+// a spinning producer lane otherwise takes issue slots from the consumer
+// warps on its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+      "r"(parity), "r"(0x100000u)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx_l(uint64_t *bar, unsigned bytes) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared.b64 st, [%0], %1;\n}\n" ::"r"(
                    (unsigned)__cvta_generic_to_shared(bar)),
@@ -960,6 +972,298 @@ __global__ void __launch_bounds__(4096 / (TM * TN), 512 / (4096 / (TM * TN)) < 3
   }
 }
 
+// ------------------------------------- FP32 warp-specialised TMA path
+// The same per-element FMA chain as leaf_sgemm_kernel, restructured for the
+// shared-memory pipe, which bounds the register-staged kernel (ncu: L1 81 %,
+// eight wavefronts per inner step per warp, transposing stores 4-way
+// conflicted):
+//   * a producer warp streams each (product, 64-wide inner chunk) as two TMA
+//     boxes into a STAGES-deep ring (mbarrier completion) -- no register
+//     staging, no block-wide barrier, item boundaries without a bubble;
+//   * A stays row-major: its box is 68 floats wide (the 4 extra columns are
+//     never read, OOB columns zero-filled), so rows sit 272 B apart and a
+//     thread reads four inner steps of one row as one 16-byte load;
+//   * two consumer warps own the 64 x 64 C tile, 8 x 8 outputs per thread
+//     (rows 16 u + 4 ty + r', columns 32 v + 4 tx + c'): per four inner steps
+//     a thread issues 8 A loads and 8 B loads for 256 FMAs, and every
+//     half-warp load touches <= 128 distinct bytes in distinct banks (one
+//     wavefront).
+// KW = the inner-chunk width of one stage (64 or 32): A box KW + 4 floats
+// wide (rows 4 apart 16 banks apart), B box 64 x KW.
+template <int KW>
+struct SwCfg {
+  static constexpr int AW = KW + 4;
+  static constexpr int A_BYTES = 64 * AW * 4, B_BYTES = KW * 64 * 4;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // a multiple of 128
+};
+constexpr int SW_CWARPS = 2, SW_THREADS = 32 * (1 + SW_CWARPS);
+
+__device__ __forceinline__ void tma_load_2d(void *smem, const CUtensorMap *map, int x, int y,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+      "l"((uint64_t)map), "r"(x), "r"(y), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+// MINB = CTAs per SM the register budget is sized for: 4 (168 registers, no
+// spills, room for the scheduler to run the fragment loads ahead) measured
+// faster than 5 (128) or 6 (96, spilling) at c5-f32 -- 45.4 vs 39.0 vs 28.2
+// TFLOP/s.
+template <int STAGES, int KW, int MINB = 4>
+__global__ void __launch_bounds__(SW_THREADS, MINB)
+    leaf_sgemm_ws_kernel(LeafArgs args, const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmB) {
+  extern __shared__ __align__(128) unsigned char sw_raw[];
+  // (offset arithmetic on the shared array keeps the loads LDS)
+  unsigned char *dsm = sw_raw + ((128u - ((unsigned)__cvta_generic_to_shared(sw_raw) & 127u)) & 127u);
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  __shared__ StageInfo info[STAGES];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = args.leaf;
+  using C = SwCfg<KW>;
+  const int kchunks = b / KW, subs_side = b / 64;
+  const int64_t N = args.N;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init_l(&full_bar[s], 1);
+      mbar_init_l(&empty_bar[s], SW_CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // ============================================================ producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmB) : "memory");
+      if (args.am) {
+        const unsigned *rdy = &args.tc->groups_ready;
+        for (;;) {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(rdy) : "memory");
+          if (v) break;
+          __nanosleep(32);
+        }
+      } else {
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+      }
+      asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+      atomicMax(&args.tc->k3_t0n, ~gtimer());
+      unsigned long long m = *args.n_codes;
+      if (m > args.capacity) m = args.capacity;
+      const int ng = args.am ? (int)args.tc->num_groups
+                             : args.tc->overflow ? 0 : (int)args.tc->num_groups;
+      const int subs = subs_side * subs_side;
+      int stage = 0;
+      unsigned phase = 0;
+      long long gstep = 0;
+      for (;;) {
+        const int item = (int)atomicAdd(&args.tc->gemm_ticket, 1ull);
+        if (item >= ng * subs) break;
+        const int grp = item / subs, sub = item - grp * subs;
+        const int si = sub / subs_side, sj = sub - si * subs_side;
+        const uint32_t gid = args.group_ids[grp];
+        const int64_t ci = gid / (uint64_t)args.nb, cj = gid - ci * args.nb;
+        const int arow0 = (int)(ci * b + si * 64), bcol0 = (int)(cj * b + sj * 64);
+        const int64_t c_off = (int64_t)arow0 * N + bcol0;
+        int64_t s = 0, end = 0;
+        uint64_t kmask = 0;
+        uint32_t k;
+        if (args.am) {
+          kmask = retained_kmask(args.am, (uint32_t)ci, (uint32_t)cj, (int)args.nb);
+          k = (uint32_t)(__ffsll((long long)kmask) - 1);
+          kmask &= kmask - 1;
+        } else {
+          s = args.group_starts[grp];
+          end = grp + 1 < ng ? args.group_starts[grp + 1] : (int64_t)m;
+          k = args.ks[s];
+        }
+        for (;;) {
+          const bool has_next = args.am ? kmask != 0 : s + 1 < end;
+          const uint32_t knext = !has_next ? 0u
+                                 : args.am ? (uint32_t)(__ffsll((long long)kmask) - 1) : args.ks[s + 1];
+          for (int kc = 0; kc < kchunks; ++kc) {
+            if (gstep >= STAGES) mbar_wait_sleep(&empty_bar[stage], phase ^ 1);
+            unsigned char *stg = dsm + stage * C::STAGE_BYTES;
+            const int kcol = (int)(k * b + kc * KW);
+            int flags = 0, h = 31;
+            if (kc == kchunks - 1) {
+              flags = STG_MERGE;
+              if (has_next) h = merge_level(k, knext);
+              else flags |= STG_END;
+            }
+            info[stage].flags = flags;
+            info[stage].h = h;
+            info[stage].c_off = c_off;
+            info[stage].grp = grp;
+            mbar_arrive_expect_tx_l(&full_bar[stage], (unsigned)C::STAGE_BYTES);
+            tma_load_2d(stg, &tmA, kcol, arow0, &full_bar[stage]);
+            tma_load_2d(stg + C::A_BYTES, &tmB, bcol0, kcol, &full_bar[stage]);
+            ++gstep;
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          if (!has_next) break;
+          k = knext;
+          if (args.am) kmask &= kmask - 1;
+          else ++s;
+        }
+      }
+      if (gstep >= STAGES) mbar_wait_sleep(&empty_bar[stage], phase ^ 1);
+      info[stage].flags = STG_DONE;
+      mbar_arrive_l(&full_bar[stage]);
+    }
+    __syncwarp();
+  } else {
+    // ============================================================ consumers
+    const int cw = warp - 1, tx = lane & 7, ty = lane >> 3;
+    float *__restrict__ Cm = (float *)args.c;
+    // this thread's rows (relative to the tile) and the byte offsets of its
+    // A row starts / B column pairs within a stage
+    int a_off[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a_off[r] = (cw * 32 + (r >> 2) * 16 + ty * 4 + (r & 3)) * C::AW * 4;
+    const int b_off = C::A_BYTES + tx * 16;
+    float acc[64];
+#pragma unroll
+    for (int e = 0; e < 64; ++e) acc[e] = 0.f;
+    float stk[MAXD][64];
+    uint32_t pending = 0;
+    int stage = 0;
+    unsigned phase = 0;
+    for (;;) {
+      mbar_wait_sleep(&full_bar[stage], phase);
+      const StageInfo si = info[stage];
+      if (si.flags & STG_DONE) break;
+      const unsigned char *stg = dsm + stage * C::STAGE_BYTES;
+#pragma unroll 2
+      for (int q4 = 0; q4 < KW / 4; ++q4) {
+        float4 a[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) a[r] = *reinterpret_cast<const float4 *>(stg + a_off[r] + q4 * 16);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          const unsigned char *brow = stg + b_off + (q4 * 4 + qq) * 256;
+          const float4 b0 = *reinterpret_cast<const float4 *>(brow);
+          const float4 b1 = *reinterpret_cast<const float4 *>(brow + 128);
+          const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const float av = qq == 0 ? a[r].x : qq == 1 ? a[r].y : qq == 2 ? a[r].z : a[r].w;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[r * 8 + c] = fmaf(av, bv[c], acc[r * 8 + c]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_l(&empty_bar[stage]);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+      if (si.flags & STG_MERGE) {
+        const int h = si.h;
+        while (pending && (__ffs(pending) - 1) < h) {
+          const int top = __popc(pending) - 1;
+#pragma unroll
+          for (int e = 0; e < 64; ++e) acc[e] = stk[top][e] + acc[e];
+          pending &= pending - 1;
+        }
+        if (!(si.flags & STG_END)) {
+          const int slot = __popc(pending);
+#pragma unroll
+          for (int e = 0; e < 64; ++e) {
+            stk[slot][e] = acc[e];
+            acc[e] = 0.f;
+          }
+          pending |= 1u << h;
+        } else {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            float *crow = Cm + si.c_off + (int64_t)(cw * 32 + (r >> 2) * 16 + ty * 4 + (r & 3)) * N + tx * 4;
+            // (scalar stores: vector stores would pin the accumulators into
+            // aligned quads whose registers share banks with the B quads)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              crow[c] = acc[r * 8 + c];
+              crow[32 + c] = acc[r * 8 + 4 + c];
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 64; ++e) acc[e] = 0.f;
+          pending = 0;
+          if (args.grp_done) {
+            __syncwarp();
+            if (lane == 0)
+              asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(&args.grp_done[si.grp])
+                           : "memory");
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) atomicMax(&args.tc->k3_t1, gtimer());
+}
+
+// 2-D view {N, N} of a padded f32 operand: box {w, h}.
+static int make_f32_map(CUtensorMap *map, const void *base, int64_t N, int w, int h) {
+  auto enc = tensor_map_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return SPAMM_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)N};
+  cuuint64_t strides[1] = {(cuuint64_t)(N * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)w, (cuuint32_t)h};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (f32) failed (%d)", (int)r);
+    return SPAMM_ERR_CUDA;
+  }
+  return SPAMM_OK;
+}
+
+template <int STAGES, int KW, int MINB = 4>
+static int launch_sgemm_ws(LeafArgs args, int num_sms, cudaStream_t st) {
+  CUtensorMap ma, mb;
+  SPAMM_TRY(make_f32_map(&ma, args.a, args.N, SwCfg<KW>::AW, 64));
+  SPAMM_TRY(make_f32_map(&mb, args.b, args.N, 64, KW));
+  auto kern = leaf_sgemm_ws_kernel<STAGES, KW, MINB>;
+  const int smem = STAGES * SwCfg<KW>::STAGE_BYTES + 128;
+  SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int per_sm = 0;
+  SPAMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SW_THREADS, smem));
+  if (per_sm < 1) per_sm = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(num_sms * per_sm);
+  cfg.blockDim = dim3(SW_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (args.pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  SPAMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args, ma, mb));
+  return SPAMM_OK;
+}
+
+static int sgemm_ws_stages() {
+  static const int v = getenv("SPAMM_SGEMM_WS_STAGES") ? atoi(getenv("SPAMM_SGEMM_WS_STAGES")) : 2;
+  return v;
+}
+
 int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, int *launches,
                 bool *signals) {
   if (signals) *signals = false;
@@ -979,6 +1283,18 @@ int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, i
     static const bool no_sgemm = getenv("SPAMM_NO_SGEMM") != nullptr;
     if (dtype == SPAMM_DTYPE_F64) {
       leaf_simt_kernel<double><<<num_sms * 2, SIMT_THREADS, 0, st>>>(a2);
+    } else if (args.leaf >= 64 && !no_sgemm && sgemm_ws_stages() > 0) {
+      // FP32 warp-specialised TMA kernel (SPAMM_SGEMM_WS_STAGES: ring depth, 0: off)
+      // SPAMM_SGEMM_WS_STAGES: 2 (default) or 3 stages of 32-wide inner
+      // chunks; 64: 2 stages of 64 (3 CTAs per SM by shared memory); 5: two
+      // stages at the 128-register budget (5 CTAs per SM); 0: the
+      // register-staged kernel below
+      switch (sgemm_ws_stages()) {
+        case 3: SPAMM_TRY((launch_sgemm_ws<3, 32>(a2, num_sms, st))); break;
+        case 64: SPAMM_TRY((launch_sgemm_ws<2, 64>(a2, num_sms, st))); break;
+        case 5: SPAMM_TRY((launch_sgemm_ws<2, 32, 5>(a2, num_sms, st))); break;
+        default: SPAMM_TRY((launch_sgemm_ws<2, 32>(a2, num_sms, st))); break;
+      }
     } else if (args.leaf >= 64 && !no_sgemm) {
       // micro-tile shape (SPAMM_SGEMM_SHAPE): 84 = 8 x 4 per thread (128 threads,
       // default), 44 = 4 x 4 (256), 88 = 8 x 8 (64)

@@ -1,0 +1,30 @@
+"""FP32 leaf-product kernel probe (diagnostics): the c5 workload (or a
+smaller n of the same decay) in f32, K3 time and TFLOP/s per multiply.
+
+    python tools/sgemm_probe.py [n] [reps]     (env SPAMM_SGEMM_SHAPE etc. as usual)"""
+import sys
+
+sys.path.insert(0, ".")
+import numpy as np
+import torch
+
+import paper_1011_3534_b200 as sp
+from paper_1011_3534_b200 import workloads
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+cfg = workloads.DEVICE_CONFIGS["c5"]
+at = workloads.exponential_decay_device(n, cfg["lam"], cfg["seed"], "cuda", torch.float32)
+a = sp.from_device_pointer(at.data_ptr(), n, leaf_size=cfg["leaf"], dtype=np.float32)
+del at
+torch.cuda.empty_cache()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for rep in range(reps):
+    for tau in cfg["taus"]:
+        flush.zero_()
+        torch.cuda.synchronize()
+        c, st, det = sp.spamm_detailed(a, a, sp.SpammConfig(tau=tau))
+        del c
+        fl = 2 * cfg["leaf"] ** 3 * st.leaf_matmuls
+        print(f"n={n} tau={tau} retained={st.leaf_matmuls} total={det.ms_total:.3f} ms "
+              f"gemm={det.ms_gemm:.3f} ms K3={fl / det.ms_gemm / 1e9:.1f} TFLOP/s", flush=True)
