@@ -348,9 +348,11 @@ __global__ void __launch_bounds__(WsCfg<TILE, CW, WMv, ST>::THREADS, 1)
                         const __grid_constant__ CUtensorMap tmB) {
   using C = WsCfg<TILE, CW, WMv, ST>;
   extern __shared__ __align__(1024) unsigned char dsm_raw[];
-  // TMA 128-byte swizzle needs 1024-byte aligned tiles
+  // TMA 128-byte swizzle needs 1024-byte aligned tiles (offset arithmetic on
+  // the shared array: an integer round-trip of the pointer would lose its
+  // address space and turn every fragment load into a generic LD)
   double *dsm = reinterpret_cast<double *>(
-      (reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+      dsm_raw + ((1024u - ((unsigned)__cvta_generic_to_shared(dsm_raw) & 1023u)) & 1023u));
   __shared__ __align__(8) uint64_t full_bar[C::STAGES], empty_bar[C::STAGES];
   __shared__ StageInfo info[C::STAGES];
   __shared__ uint32_t s_tmem;

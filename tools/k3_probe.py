@@ -1,7 +1,7 @@
-"""FP32 leaf-product kernel probe (diagnostics): the c5 workload (or a
-smaller n of the same decay) in f32, K3 time and TFLOP/s per multiply.
+"""Leaf-product kernel probe (diagnostics): the c5 workload (or a smaller n
+of the same decay) in f32 (default) or f64, K3 time and TFLOP/s per multiply.
 
-    python tools/sgemm_probe.py [n] [reps]     (env SPAMM_SGEMM_SHAPE etc. as usual)"""
+    python tools/k3_probe.py [n] [reps] [f32|f64]   (env SPAMM_* switches as usual)"""
 import sys
 
 sys.path.insert(0, ".")
@@ -13,9 +13,12 @@ from paper_1011_3534_b200 import workloads
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+f64 = len(sys.argv) > 3 and sys.argv[3] == "f64"
 cfg = workloads.DEVICE_CONFIGS["c5"]
-at = workloads.exponential_decay_device(n, cfg["lam"], cfg["seed"], "cuda", torch.float32)
-a = sp.from_device_pointer(at.data_ptr(), n, leaf_size=cfg["leaf"], dtype=np.float32)
+at = workloads.exponential_decay_device(n, cfg["lam"], cfg["seed"], "cuda",
+                                       torch.float64 if f64 else torch.float32)
+a = sp.from_device_pointer(at.data_ptr(), n, leaf_size=cfg["leaf"],
+                           dtype=np.float64 if f64 else np.float32)
 del at
 torch.cuda.empty_cache()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
