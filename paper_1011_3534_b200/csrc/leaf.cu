@@ -820,16 +820,19 @@ __global__ void __launch_bounds__(SIMT_THREADS) leaf_simt_kernel(LeafArgs args) 
 }
 
 // consumer-warp layout of the FP64 kernel at leaf >= 64 (SPAMM_K3_WARPS):
-// 16 = 4 x 4 warp tiles of 16 x 16 (default), 8 = 2 x 4 of 32 x 16,
-// 9 = 4 x 2 of 16 x 32, 4 = 2 x 2 of 32 x 32
+// 8 = 2 x 4 warp tiles of 32 x 16 (eight independent DMMA chains per warp;
+// c5 K3 31.8 vs 29.8 TFLOP/s for 16) on a 6-stage ring, 84 = the same on 4
+// stages (default: as fast, and leaves shared memory for C's norm kernel to
+// run beside it), 87 = 7 stages, 16 = 4 x 4 of 16 x 16, 9 = 4 x 2 of 16 x 32,
+// 4 = 2 x 2 of 32 x 32
 int k3_warps() {
-  static const int w = getenv("SPAMM_K3_WARPS") ? atoi(getenv("SPAMM_K3_WARPS")) : 16;
+  static const int w = getenv("SPAMM_K3_WARPS") ? atoi(getenv("SPAMM_K3_WARPS")) : 84;
   return w;
 }
 unsigned leaf_signals_per_tile(int leaf) {
   if (leaf < 64) return 16;
   const int w = k3_warps();
-  return w == 8 || w == 9 ? 8 : w == 4 ? 4 : 16;
+  return w == 8 || w == 9 || w == 84 || w == 87 ? 8 : w == 4 ? 4 : 16;
 }
 
 // ----------------------------------------------------- FP32 tiled path
@@ -1272,6 +1275,8 @@ int launch_leaf(const LeafArgs &args, int dtype, int num_sms, cudaStream_t st, i
   if (dtype == SPAMM_DTYPE_F64 && args.leaf >= 32) {
     if (args.leaf == 32) SPAMM_TRY((launch_dmma_ws<32>(args, num_sms, st)));
     else if (k3_warps() == 8) SPAMM_TRY((launch_dmma_ws<64, 8, 2>(args, num_sms, st)));
+    else if (k3_warps() == 84) SPAMM_TRY((launch_dmma_ws<64, 8, 2, 4>(args, num_sms, st)));
+    else if (k3_warps() == 87) SPAMM_TRY((launch_dmma_ws<64, 8, 2, 7>(args, num_sms, st)));
     else if (k3_warps() == 9) SPAMM_TRY((launch_dmma_ws<64, 8, 4>(args, num_sms, st)));
     else if (k3_warps() == 4) SPAMM_TRY((launch_dmma_ws<64, 4, 2>(args, num_sms, st)));
     else if (k3_warps() == 5) SPAMM_TRY((launch_dmma_ws<64, 16, 4, 5>(args, num_sms, st)));

@@ -57,6 +57,10 @@ struct PyrTail {
   // storage as they square them -- the source is read once, no separate copy
   const void *fuse_src;
   int64_t fuse_ld;
+  // dynamic leaf assignment (segmented-chain kernel beside K3): warps take
+  // list slots from this counter in completion order instead of a fixed
+  // stride; zero at rest, reset by the last CTA with `ticket`
+  unsigned *leaf_ticket;
 };
 
 __device__ __forceinline__ void spin_acquire_nonzero(const unsigned *flag) {

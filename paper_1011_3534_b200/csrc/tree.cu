@@ -564,8 +564,11 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
 // exact add and running the plain chain over the other segments.
 constexpr int SEG_WARPS = 6;
 
-template <typename T, int LEAF>
-__global__ void __launch_bounds__(32 * SEG_WARPS) leaf_norm_seg_kernel(
+// W warps stage and norm leaves; H more warps only join the pyramid tail (the
+// last CTA builds C's pyramid with all W + H warps; beside K3 a CTA has
+// shared memory for two staging warps, but registers for six)
+template <typename T, int LEAF, int W = SEG_WARPS, int H = 0>
+__global__ void __launch_bounds__(32 * (W + H)) leaf_norm_seg_kernel(
     T *__restrict__ padded, int64_t N, int64_t nb, double *__restrict__ nsq_leaf,
     uint8_t *__restrict__ occ_leaf, const uint32_t *__restrict__ list, const unsigned *list_count,
     PyrTail tail, unsigned smem_bytes) {
@@ -574,7 +577,7 @@ __global__ void __launch_bounds__(32 * SEG_WARPS) leaf_norm_seg_kernel(
   constexpr int EPV = 16 / (int)sizeof(T);
   constexpr int SS = seg_stride<T, LEAF>();
   extern __shared__ __align__(16) unsigned char seg_smem[];
-  __shared__ SegInfo tbl[SEG_WARPS][64];
+  __shared__ SegInfo tbl[W][64];
   if (tail.pdl_wait) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (tail.ready) {
     if (threadIdx.x == 0) spin_acquire_nonzero(tail.ready);
@@ -583,11 +586,17 @@ __global__ void __launch_bounds__(32 * SEG_WARPS) leaf_norm_seg_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned char *wsm = seg_smem + (size_t)warp * seg_warp_bytes<T, LEAF>();
   const int64_t n_leaves = list ? (int64_t)*list_count : nb * nb;
-  const int64_t gw = (int64_t)blockIdx.x * SEG_WARPS + warp;
-  const int64_t nw = (int64_t)gridDim.x * SEG_WARPS;
+  const int64_t gw = (int64_t)blockIdx.x * W + warp;
+  const int64_t nw = (int64_t)gridDim.x * W;
   const bool check_flags = tail.grp_done && (!tail.overflow || !*(volatile const int *)tail.overflow);
   unsigned long long *const k1_tl = g_k1_tl;  // optional per-leaf timeline (SPAMM_K1_TIMELINE)
-  for (int64_t lx = gw; lx < n_leaves; lx += nw) {
+  auto next_slot = [&](int64_t cur) -> int64_t {
+    if (!tail.leaf_ticket) return cur < 0 ? gw : cur + nw;
+    unsigned v = 0;
+    if (lane == 0) v = atomicAdd(tail.leaf_ticket, 1u);
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  for (int64_t lx = warp < W ? next_slot(-1) : n_leaves; lx < n_leaves; lx = next_slot(lx)) {
     const int64_t leaf = list ? (int64_t)list[lx] : lx;
     const int64_t bi = leaf / nb, bj = leaf - bi * nb;
     const bool tl_on = k1_tl && lane == 0 && lx < 8192;
@@ -646,6 +655,7 @@ __global__ void __launch_bounds__(32 * SEG_WARPS) leaf_norm_seg_kernel(
       pyramid_cta(tail, seg_smem, smem_bytes);
       if (threadIdx.x == 0) {
         *tail.ticket = 0u;
+        if (tail.leaf_ticket) *tail.leaf_ticket = 0u;
         if (tail.t_end) *tail.t_end = k1_gt();
       }
     }
@@ -1323,7 +1333,7 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
                         const unsigned *trav_done, const void *fuse_src, int64_t fuse_ld) {
   // builds on copy_in run concurrently with the main stream's: own tickets
   Scratch &k1t = st == ctx->copy_in ? ctx->k1_ticket_in : ctx->k1_ticket;
-  SPAMM_TRY(ensure_scratch(k1t, sizeof(unsigned), st, /*zeroed=*/true));
+  SPAMM_TRY(ensure_scratch(k1t, 2 * sizeof(unsigned), st, /*zeroed=*/true));  // + leaf ticket
   unsigned *ticket = (unsigned *)k1t.ptr;
   bool fused = false;
   // list mode follows the leaf-product kernel: launch it programmatically so
@@ -1401,16 +1411,30 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
       tail.ready = ov->ready;
       tail.trav_done = ov->trav_done;
     }
-    // shared memory: a staged leaf per warp (one CTA per SM)
-    const unsigned smem = (unsigned)(SEG_WARPS * (t->leaf == 64
+    // shared memory: a staged leaf per warp (one CTA per SM).  Behind a
+    // leaf-product kernel that signals finished groups, CTAs of 2 warps: one
+    // fits beside K3's CTA on every SM (K3 on its 4-stage ring leaves ~95 KB
+    // of shared memory), so C's leaves are normed while K3 still runs and
+    // only the last groups' leaves remain after it (SPAMM_SEG_OVL_WARPS: 2 or
+    // 6 = one 6-warp CTA per SM that starts as K3's CTAs retire)
+    static const int ovl_w = getenv("SPAMM_SEG_OVL_WARPS") ? atoi(getenv("SPAMM_SEG_OVL_WARPS")) : 2;
+    const int W = (ov && ov->grp_done && ovl_w == 2) ? 2 : SEG_WARPS;
+    const unsigned smem = (unsigned)(W * (t->leaf == 64
         ? (f64 ? seg_warp_bytes<double, 64>() : seg_warp_bytes<float, 64>())
         : (f64 ? seg_warp_bytes<double, 32>() : seg_warp_bytes<float, 32>())));
     const int64_t cap = std::min<int64_t>(list_cap, t->nb * t->nb);
+    // beside K3: warps take leaves from a ticket (the CTA per SM that joins
+    // K3 works through the groups as they complete, the CTAs that start as
+    // K3 retires share what is left); three 2-warp CTAs per SM in all
+    const bool dyn = W == 2 && tail.ticket != nullptr;
+    if (dyn) tail.leaf_ticket = ticket + 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(
-        1, std::min<int64_t>((cap + SEG_WARPS - 1) / SEG_WARPS,
-                             (int64_t)ctx->num_sms)));
-    cfg.blockDim = dim3(32 * SEG_WARPS);
+        1, std::min<int64_t>((cap + W - 1) / W, (int64_t)ctx->num_sms * (dyn ? 3 : 1))));
+    // (W == 2: + SPAMM_SEG_HELPERS pyramid-only warps)
+    static const int seg_helpers_env = getenv("SPAMM_SEG_HELPERS") ? atoi(getenv("SPAMM_SEG_HELPERS")) : 0;
+    const int seg_helpers = seg_helpers_env == 1 || seg_helpers_env == 2 ? seg_helpers_env : 0;
+    cfg.blockDim = dim3(32 * (W == 2 ? 2 + seg_helpers : W));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1422,14 +1446,31 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
     }
     auto launch = [&](auto kern, auto *data) -> int {
       SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      // (the same shared-memory carveout as K3: a CTA can only join an SM
+      // whose L1 / shared split it accepts)
+      SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       SPAMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, data, t->N, t->nb, t->nsq + level_offset(t->depth),
                                         t->occ + level_offset(t->depth), list, list_count, tail, smem));
       return SPAMM_OK;
     };
     double *pd = (double *)t->padded;
     float *pf = (float *)t->padded;
-    if (t->leaf == 64) SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 64>, pd) : launch(leaf_norm_seg_kernel<float, 64>, pf));
-    else SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 32>, pd) : launch(leaf_norm_seg_kernel<float, 32>, pf));
+    if (W == 2) {
+      if (seg_helpers == 2) {
+        if (t->leaf == 64) SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 64, 2, 2>, pd) : launch(leaf_norm_seg_kernel<float, 64, 2, 2>, pf));
+        else SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 32, 2, 2>, pd) : launch(leaf_norm_seg_kernel<float, 32, 2, 2>, pf));
+      } else if (seg_helpers == 1) {
+        if (t->leaf == 64) SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 64, 2, 1>, pd) : launch(leaf_norm_seg_kernel<float, 64, 2, 1>, pf));
+        else SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 32, 2, 1>, pd) : launch(leaf_norm_seg_kernel<float, 32, 2, 1>, pf));
+      } else {
+        if (t->leaf == 64) SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 64, 2>, pd) : launch(leaf_norm_seg_kernel<float, 64, 2>, pf));
+        else SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 32, 2>, pd) : launch(leaf_norm_seg_kernel<float, 32, 2>, pf));
+      }
+    } else if (t->leaf == 64) {
+      SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 64>, pd) : launch(leaf_norm_seg_kernel<float, 64>, pf));
+    } else {
+      SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 32>, pd) : launch(leaf_norm_seg_kernel<float, 32>, pf));
+    }
     fused = tail.ticket != nullptr;
   } else if (t->dtype == SPAMM_DTYPE_F64)
     SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap, ticket, ov, &fused));
