@@ -102,6 +102,7 @@ struct DeviceContext {
   Scratch reduce_tmp;     // misc reduction scratch
   Scratch pyr_tickets;    // pyramid hand-off counters (self-resetting, zero at rest)
   Scratch k1_ticket;      // K1's last-CTA ticket for the fused pyramid (zero at rest)
+  Scratch k1_pcnt;        // K1 beside K3: finished children per leaf parent (zero at rest)
   Scratch pyr_tickets_in, k1_ticket_in;  // the same, for builds on copy_in
   Scratch dn_masks;       // dense traversal: two work sets (zero at rest)
   size_t dn_set_words = 0;  // words per dense work set
@@ -202,7 +203,7 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
                         unsigned *grp_done, unsigned grp_target, const int *overflow,
                         unsigned long long *t_end, const unsigned *ready = nullptr,
                         const unsigned *trav_done = nullptr, const void *fuse_src = nullptr,
-                        int64_t fuse_ld = 0);
+                        int64_t fuse_ld = 0, const uint32_t *ne = nullptr);
 // upper pyramid levels + interior nrm from the leaf level (tree.cu)
 int pyramid_upper_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int *launches = nullptr);
 // order ctx->stream after an asynchronous build of t (no-op otherwise)

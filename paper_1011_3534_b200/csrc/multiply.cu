@@ -374,7 +374,8 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
                                     leaf_signals_per_tile(a->leaf) * subs,
                                     bm ? nullptr : &dtc->overflow, &dtc->k1_t1,
                                     bm ? &dtc->groups_ready : nullptr,
-                                    bm ? &dtc->trav_done : nullptr)))
+                                    bm ? &dtc->trav_done : nullptr, nullptr, 0,
+                                    bm && overlapped ? ta.dn_masks + dense_ne_offset(depth) : nullptr)))
         break;
     }
     ctx->last_overlapped = overlapped;

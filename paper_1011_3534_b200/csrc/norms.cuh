@@ -61,6 +61,12 @@ struct PyrTail {
   // list slots from this counter in completion order instead of a fixed
   // stride; zero at rest, reset by the last CTA with `ticket`
   unsigned *leaf_ticket;
+  // ... and the leaves' parents built as their last listed child completes:
+  // ne = the product's non-empty leaf blocks (bit i * nb + j), pcnt = finished
+  // children per parent (zero at rest); the last CTA's pyramid then starts
+  // one level up (the parent level is zeroed by the traversal)
+  const uint32_t *ne;
+  unsigned *pcnt;
 };
 
 __device__ __forceinline__ void spin_acquire_nonzero(const unsigned *flag) {
@@ -116,7 +122,15 @@ __device__ __forceinline__ void pyr_nodes_from_global(const PyrTail &pt, int k, 
   }
 }
 
-__device__ inline void pyramid_cta(const PyrTail &pt, unsigned char *smem, size_t smem_bytes) {
+__device__ inline void pyramid_cta(const PyrTail &pt, unsigned char *smem, size_t smem_bytes,
+                                   unsigned long long *dbg = nullptr) {
+  auto stamp = [&](int q) {
+    if (dbg && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      dbg[q] = t;
+    }
+  };
   int k = pt.depth - 1;
   if (k < 0) return;
   // global-memory levels until one fits (with the next) in shared memory
@@ -132,8 +146,10 @@ __device__ inline void pyramid_cta(const PyrTail &pt, unsigned char *smem, size_
   double *bufB = bufA + n0;
   uint8_t *oA = reinterpret_cast<uint8_t *>(bufB + (n0 >> 2) + 1);
   uint8_t *oB = oA + n0;
+  stamp(0);
   for (int e0 = threadIdx.x; e0 < n0; e0 += 4 * blockDim.x) pyr_nodes_from_global(pt, k, e0, n0, bufA, oA);
   __syncthreads();
+  stamp(1);
   int side = 1 << k;
   for (--k; k >= 0; --k) {
     const int ps = side >> 1;
@@ -154,6 +170,7 @@ __device__ inline void pyramid_cta(const PyrTail &pt, unsigned char *smem, size_
     uint8_t *to = oA; oA = oB; oB = to;
     side = ps;
   }
+  stamp(2);
 }
 
 // whole-pyramid tails are used up to this depth (one CTA: 4^depth leaves)

@@ -830,12 +830,13 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
   // the leaf-product kernel may launch now: its CTAs take SMs as this grid's
   // CTAs retire and wait (griddepcontrol.wait) for this grid's results
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  if (a.c_nsq_leaf) {  // the product's leaf-level norms start at zero
-    for (uint64_t e = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x; e < G;
+  if (a.c_nsq_leaf) {  // the product's leaf-level norms (and their parents') start at zero
+    const uint64_t P = D >= 1 ? G / 4 : 0;  // the parent level precedes the leaf level
+    for (uint64_t e = (uint64_t)blockIdx.x * DN_THREADS + threadIdx.x; e < G + P;
          e += (uint64_t)nblocks * DN_THREADS) {
-      a.c_nsq_leaf[e] = 0.0;
-      a.c_nrm_leaf[e] = 0.0;
-      a.c_occ_leaf[e] = 0;
+      a.c_nsq_leaf[(int64_t)e - (int64_t)P] = 0.0;
+      a.c_nrm_leaf[(int64_t)e - (int64_t)P] = 0.0;
+      a.c_occ_leaf[(int64_t)e - (int64_t)P] = 0;
     }
   }
   uint32_t *ws = a.dn_masks;                     // this call's work set
@@ -1388,6 +1389,21 @@ __global__ void __launch_bounds__(DN_THREADS) traverse_dense_kernel(TraverseArgs
 
 template <int D>
 static size_t dense_work_words_d() { return (size_t)DnLayout<D>::WORDS; }
+template <int D>
+static size_t dense_ne_offset_d() { return (size_t)DnLayout<D>::NE; }
+// word offset of the non-empty C-block bitmask within a work set
+size_t dense_ne_offset(int depth) {
+  switch (depth) {
+    case 0: return dense_ne_offset_d<0>();
+    case 1: return dense_ne_offset_d<1>();
+    case 2: return dense_ne_offset_d<2>();
+    case 3: return dense_ne_offset_d<3>();
+    case 4: return dense_ne_offset_d<4>();
+    case 5: return dense_ne_offset_d<5>();
+    case 6: return dense_ne_offset_d<6>();
+    default: return dense_ne_offset_d<7>();
+  }
+}
 size_t dense_work_words(int depth) {
   switch (depth) {
     case 0: return dense_work_words_d<0>();

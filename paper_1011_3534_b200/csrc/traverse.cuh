@@ -115,6 +115,7 @@ int launch_traverse(const TraverseArgs &args, int num_sms, cudaStream_t st);
 bool dense_traversal_ok(int depth);
 size_t dense_mask_words(int depth);
 size_t dense_work_words(int depth);
+size_t dense_ne_offset(int depth);  // (words, within a work set)
 size_t dense_retained_words(int depth);
 size_t dense_pruned_tiles(int depth);
 size_t dense_np_entries(int depth);

@@ -639,6 +639,27 @@ __global__ void __launch_bounds__(32 * (W + H)) leaf_norm_seg_kernel(
       occ_leaf[leaf] = (uint8_t)nz;
       tail.nrm[level_offset(tail.depth) + leaf] = __dsqrt_rn(acc);
       if (tail.grp_done) tail.grp_done[lx] = 0u;  // zero at rest for the next product
+      if (tail.pcnt) {
+        // the parent once its last non-empty child is final: ((c11 + c12) + c21) + c22
+        // (quadtree.py:90-92); empty children read as the zeros the traversal wrote
+        const int64_t pi = bi >> 1, pj = bj >> 1, c0 = 2 * pi * nb + 2 * pj, c1 = c0 + nb;
+        auto bit = [&](int64_t g) { return (int)((__ldcg(tail.ne + (g >> 5)) >> (g & 31)) & 1u); };
+        const unsigned expect = (unsigned)(bit(c0) + bit(c0 + 1) + bit(c1) + bit(c1 + 1));
+        const int64_t p = pi * (nb >> 1) + pj;
+        __threadfence();
+        if (atomicAdd(tail.pcnt + p, 1u) + 1u == expect) {
+          __threadfence();
+          const double v = __dadd_rn(__dadd_rn(__dadd_rn(__ldcg(nsq_leaf + c0), __ldcg(nsq_leaf + c0 + 1)),
+                                               __ldcg(nsq_leaf + c1)), __ldcg(nsq_leaf + c1 + 1));
+          const uint8_t o = __ldcg(occ_leaf + c0) | __ldcg(occ_leaf + c0 + 1) | __ldcg(occ_leaf + c1) |
+                            __ldcg(occ_leaf + c1 + 1);
+          const int64_t lo = level_offset(tail.depth - 1);
+          tail.nsq[lo + p] = v;
+          tail.occ[lo + p] = o;
+          tail.nrm[lo + p] = __dsqrt_rn(v);
+          tail.pcnt[p] = 0u;
+        }
+      }
     }
   }
   if (tail.ticket) {  // the last CTA builds the pyramid
@@ -650,13 +671,23 @@ __global__ void __launch_bounds__(32 * (W + H)) leaf_norm_seg_kernel(
     }
     __syncthreads();
     if (s_last) {
+      // (timeline: [8191] = last CTA decided, trav_done seen, pyramid done)
+      if (k1_tl && threadIdx.x == 0) k1_tl[4 * 8191] = k1_gt();
       if (tail.trav_done && threadIdx.x == 0) spin_acquire_nonzero(tail.trav_done);
       __threadfence();
-      pyramid_cta(tail, seg_smem, smem_bytes);
+      if (k1_tl && threadIdx.x == 0) k1_tl[4 * 8191 + 1] = k1_gt();
+      if (tail.pcnt) {  // the leaves' parents are built: the pyramid from their level
+        PyrTail up = tail;
+        up.depth = tail.depth - 1;
+        pyramid_cta(up, seg_smem, smem_bytes, k1_tl ? k1_tl + 4 * 8190 : nullptr);
+      } else {
+        pyramid_cta(tail, seg_smem, smem_bytes, k1_tl ? k1_tl + 4 * 8190 : nullptr);
+      }
       if (threadIdx.x == 0) {
         *tail.ticket = 0u;
         if (tail.leaf_ticket) *tail.leaf_ticket = 0u;
         if (tail.t_end) *tail.t_end = k1_gt();
+        if (k1_tl) k1_tl[4 * 8191 + 2] = k1_gt();
       }
     }
   }
@@ -1172,6 +1203,7 @@ struct K1Overlap {
   const unsigned *ready, *trav_done;  // bitmask groups (see PyrTail)
   const void *fuse_src;               // fused build (see PyrTail)
   int64_t fuse_ld;
+  const uint32_t *ne;                 // non-empty leaf blocks (see PyrTail)
 };
 
 template <typename T, int S, int LT>
@@ -1303,6 +1335,13 @@ void k1_timeline_dump(unsigned long long k3_end, unsigned long long k3_start) {
         auto rel = [&](int f) { return ((double)tl[4 * q + f] - (double)k3_end) * 1e-3; };
         fprintf(stderr, " [reach %.1f flag %.1f staged %.1f done %.1f]", rel(3), rel(0), rel(1), rel(2));
       }
+      if (tl[4 * 8190])
+        fprintf(stderr, " | pyr start %.1f global level %.1f smem levels %.1f", ((double)tl[4 * 8190] - (double)k3_end) * 1e-3,
+                ((double)tl[4 * 8190 + 1] - (double)k3_end) * 1e-3, ((double)tl[4 * 8190 + 2] - (double)k3_end) * 1e-3);
+      if (tl[4 * 8191])
+        fprintf(stderr, " | last CTA %.1f trav %.1f pyramid done %.1f",
+                ((double)tl[4 * 8191] - (double)k3_end) * 1e-3, ((double)tl[4 * 8191 + 1] - (double)k3_end) * 1e-3,
+                ((double)tl[4 * 8191 + 2] - (double)k3_end) * 1e-3);
       fprintf(stderr, "\n");
     }
   }
@@ -1330,7 +1369,8 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
                         const uint32_t *list, const unsigned *list_count, int64_t list_cap,
                         unsigned *grp_done, unsigned grp_target, const int *overflow,
                         unsigned long long *t_end, const unsigned *ready,
-                        const unsigned *trav_done, const void *fuse_src, int64_t fuse_ld) {
+                        const unsigned *trav_done, const void *fuse_src, int64_t fuse_ld,
+                        const uint32_t *ne) {
   // builds on copy_in run concurrently with the main stream's: own tickets
   Scratch &k1t = st == ctx->copy_in ? ctx->k1_ticket_in : ctx->k1_ticket;
   SPAMM_TRY(ensure_scratch(k1t, 2 * sizeof(unsigned), st, /*zeroed=*/true));  // + leaf ticket
@@ -1339,7 +1379,7 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
   // list mode follows the leaf-product kernel: launch it programmatically so
   // its CTAs are resident (and waiting) as that kernel's CTAs retire
   K1Overlap ovs{grp_done, grp_target, overflow, t_end, list != nullptr && t_end != nullptr, ready,
-                trav_done, fuse_src, fuse_ld};
+                trav_done, fuse_src, fuse_ld, ne};
   const K1Overlap *ov = (grp_done || t_end || fuse_src) ? &ovs : nullptr;
   // list mode (C's tree): the segmented-chain kernel, a warp per leaf
   static const bool no_seg = getenv("SPAMM_NO_SEG_CHAIN") != nullptr;
@@ -1428,6 +1468,13 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
     // K3 retires share what is left); three 2-warp CTAs per SM in all
     const bool dyn = W == 2 && tail.ticket != nullptr;
     if (dyn) tail.leaf_ticket = ticket + 1;
+    static const bool no_par = getenv("SPAMM_NO_K1_PARENTS") != nullptr;
+    if (dyn && ov->ne && t->depth >= 1 && !no_par) {
+      SPAMM_TRY(ensure_scratch(ctx->k1_pcnt, sizeof(unsigned) * ((size_t)1 << (2 * (t->depth - 1))), st,
+                               /*zeroed=*/true));
+      tail.ne = ov->ne;
+      tail.pcnt = (unsigned *)ctx->k1_pcnt.ptr;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(
         1, std::min<int64_t>((cap + W - 1) / W, (int64_t)ctx->num_sms * (dyn ? 3 : 1))));
