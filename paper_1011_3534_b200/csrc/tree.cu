@@ -5,6 +5,7 @@
 // Reference: quadtree.py:116-151 (QuadTreeMatrix.__init__), :74-87
 // (_leaf_norm_sq), :90-92 (_aggregate_norm_sq), :218-251 (from_dense).
 #include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -248,6 +249,38 @@ __device__ void canonicalise_leaf(T *padded, int64_t N, int32_t b, int64_t bi, i
   for (int r = 0; r < b; ++r) {
     T *row = padded + (bi * b + r) * N + bj * b;
     for (int c = 0; c < b; ++c) row[c] = T(0);
+  }
+}
+
+// Warp-cooperative form (all 32 lanes call it): every flagged lane's leaf is
+// zeroed by the whole warp with coalesced stores.  (One lane storing its own
+// 4096 elements made a c5 build, where the 19 % of the leaves that hold only
+// underflowed +-0.0 are rewritten, spend most of its time here.)
+template <typename T>
+__device__ void canonicalise_leaves_warp(T *padded, int64_t N, int32_t b, int64_t nb, bool flag,
+                                         int64_t leaf) {
+  unsigned m = __ballot_sync(0xffffffffu, flag);
+  const int lane = threadIdx.x & 31;
+  const bool vec = ((int64_t)b * sizeof(T)) % 16 == 0 && (N * sizeof(T)) % 16 == 0 &&
+                   ((uintptr_t)padded & 15) == 0;
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    const int64_t lf = __shfl_sync(0xffffffffu, leaf, src);
+    const int64_t bi = lf / nb, bj = lf - bi * nb;
+    T *base = padded + (bi * b) * N + bj * b;
+    if (vec) {
+      const int spr = b * (int)sizeof(T) / 16;  // 16-byte segments per leaf row
+      for (int idx = lane; idx < b * spr; idx += 32) {
+        const int r = idx / spr, c = idx - r * spr;
+        reinterpret_cast<uint4 *>(base + (int64_t)r * N)[c] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    } else {
+      for (int idx = lane; idx < b * b; idx += 32) {
+        const int r = idx / b, c = idx - r * b;
+        base[(int64_t)r * N + c] = T(0);
+      }
+    }
   }
 }
 
@@ -495,6 +528,8 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
     for (int q = 0; q < K1_SQ_WARPS; ++q) bits |= lane < K1_LT ? s_bits[q][lane] : 0;
   }
   if (k1_tl && lane == 0) k1_tl[4 * blockIdx.x + 3] = k1_gt();
+  bool canon = false;
+  int64_t canon_leaf = 0;
   if (mine) {
     const int64_t lx = leaf0 + lane;
     const int64_t leaf = list ? (int64_t)list[lx] : lx;
@@ -503,11 +538,11 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
     occ_leaf[leaf] = (uint8_t)nz;
     tail.nrm[level_offset(tail.depth) + leaf] = __dsqrt_rn(acc);
     if (tail.grp_done) tail.grp_done[lx] = 0u;  // zero at rest for the next product
-    if (!nz && bits) {
-      const int64_t bi = leaf / nb;
-      canonicalise_leaf<T>(padded, N, b, bi, leaf - bi * nb);
-    }
+    canon = !nz && bits;  // only -0.0 entries: stored as +0.0 (quadtree.py:127-129)
+    canon_leaf = leaf;
   }
+  __syncwarp();
+  canonicalise_leaves_warp<T>(padded, N, b, nb, canon, canon_leaf);
   }  // warp 0
   }  // leaf0 < n_leaves
   if (tail.ticket) {  // the last CTA builds the pyramid
@@ -527,6 +562,166 @@ __global__ void __launch_bounds__(K1_THREADS) leaf_norm_staged_kernel(T *__restr
         if (tail.t_end) *tail.t_end = k1_gt();
       }
     }
+  }
+}
+
+// ------------------------------------------------ K1, dense rows (TMA-fed)
+// Dense builds of large trees (leaf 64, every leaf, block rows of a multiple
+// of 32 leaves) are HBM-bound: 32 KB read per leaf against one 4096-long add
+// chain.  Persistent kernel, one 4-warp CTA per SM, every warp on its own
+// SMSP and self-contained:
+//   * a warp owns 32 adjacent leaves of a block row at a time (lane = leaf);
+//     one matrix row of the group is 32 x (64 elements) contiguous in memory
+//     and arrives with ONE TMA tensor load per stage into the warp's own
+//     ROWS_R-stage ring (mbarrier completion).  The 4-D box {128 bytes,
+//     32 leaves, 128-byte pieces of the leaf row, 1 matrix row} puts piece j
+//     of leaf l in shared line j * 32 + l, and the 128-byte swizzle rotates
+//     the line's 16-byte chunks by l & 7: the per-lane LDS.128 reads (lane =
+//     leaf, a stride that would otherwise hit one bank group) are conflict
+//     free with no padding;
+//   * the lane squares and accumulates in the reference's order,
+//     acc = rn(acc + rn(x * x)) (quadtree.py:80-87), ORs the raw bits
+//     (occupancy, -0.0), and lane 0 re-issues the stage's next load itself --
+//     no producer warp, no empty barriers, the ring carries on across groups;
+//   * fused build (the source is not the tree's storage): lane 0 stores the
+//     raw stage into the tree with one TMA tensor store (shared -> global,
+//     the same box) while the warp runs the chains, and waits for the store's
+//     read of the stage before the stage is refilled.
+// Groups are dealt round-robin to the grid's warps.  (Per-lane 512-byte bulk
+// copies instead of the tensor box measured 4.0 TB/s: the 32-way serialised
+// UBLKCP issue, ~70 cycles each, was the limiter.)
+constexpr int ROWS_WARPS = 4;
+constexpr int ROWS_LEAF = 64;
+// SPAMM_K1_ROWS_DEBUG: per-warp {cycles waiting for data, cycles in all, chunks}
+__device__ unsigned long long *g_rows_dbg = nullptr;
+
+__device__ __forceinline__ void tma_load_4d(unsigned smem, const CUtensorMap *map, int c0, int c1, int c2,
+                                            int c3, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4, %5}], [%6];\n" ::"r"(smem),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                             unsigned smem) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n" ::"l"(
+                   (uint64_t)map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem)
+               : "memory");
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(32 * ROWS_WARPS, 1)
+    leaf_norm_rows_kernel(const __grid_constant__ CUtensorMap tm_src,
+                          const __grid_constant__ CUtensorMap tm_dst, int fuse, T *padded, int64_t N,
+                          int64_t nb, int gpr_shift, double *__restrict__ nsq_leaf,
+                          uint8_t *__restrict__ occ_leaf, double *__restrict__ nrm_leaf) {
+  using U = typename Bits<T>::U;
+  constexpr int ROWB = ROWS_LEAF * (int)sizeof(T);  // bytes of one leaf row
+  constexpr int PIECES = ROWB / 128;                // 128-byte pieces per leaf row
+  constexpr int STAGE = 32 * ROWB;
+  constexpr int EPS = 16 / (int)sizeof(T);
+  extern __shared__ unsigned char rows_smem_raw[];
+  __shared__ __align__(8) uint64_t rows_bar[ROWS_WARPS][R];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t G = nb << gpr_shift;    // groups in all (2^gpr_shift = nb / 32 per block row)
+  const int64_t W = (int64_t)gridDim.x * ROWS_WARPS;
+  const int64_t w0 = (int64_t)blockIdx.x + (int64_t)warp * gridDim.x;  // CTA-major deal
+  // 1024-byte aligned stages (the swizzle pattern is a function of the address)
+  const unsigned base = ((unsigned)__cvta_generic_to_shared(rows_smem_raw) + 1023u) & ~1023u;
+  const unsigned ring = base + warp * R * STAGE;
+  const unsigned bar0 = (unsigned)__cvta_generic_to_shared(&rows_bar[warp][0]);
+  if (lane == 0) {
+    for (int s = 0; s < R; ++s) mbar_init(&rows_bar[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  __syncwarp();
+  if (w0 >= G) return;
+  const int64_t my_groups = (G - w0 + W - 1) / W;
+  const int64_t Q = my_groups * ROWS_LEAF;  // chunks (matrix rows of a group) this warp streams
+  const int64_t gmask = ((int64_t)1 << gpr_shift) - 1;
+
+  // (lane 0) chunk q = row q & 63 of this warp's group q >> 6, into stage q % R
+  auto issue = [&](int64_t q) {
+    const int64_t g = w0 + (q >> 6) * W;
+    const int s = (int)(q % R);
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared.b64 st, [%0], %1;\n}\n" ::"r"(
+                     bar0 + 8 * s),
+                 "r"((unsigned)STAGE)
+                 : "memory");
+    tma_load_4d(ring + s * STAGE, &tm_src, 0, (int)((g & gmask) << 5), 0,
+                (int)((g >> gpr_shift) * ROWS_LEAF + (q & 63)), bar0 + 8 * s);
+  };
+  if (lane == 0)
+    for (int64_t q = 0; q < R && q < Q; ++q) issue(q);
+
+  // this lane's chunk c of piece j sits at line j * 32 + lane, chunk c ^ (lane & 7)
+  const unsigned lane_off = (unsigned)lane * 128u;
+  const unsigned sw = (unsigned)(lane & 7);
+  double acc = 0.0;
+  U bits = 0;
+  unsigned long long *const dbg = g_rows_dbg;
+  long long t_wait = 0, t_begin = dbg ? clock64() : 0;
+  for (int64_t q = 0; q < Q; ++q) {
+    const int s = (int)(q % R);
+    const long long tw = dbg ? clock64() : 0;
+    mbar_wait(&rows_bar[warp][s], (unsigned)((q / R) & 1));
+    if (dbg) t_wait += clock64() - tw;
+    const int64_t g = w0 + (q >> 6) * W;
+    const int64_t bi = g >> gpr_shift;
+    const int bj0 = (int)((g & gmask) << 5);
+    const int r = (int)(q & 63);
+    if (fuse && lane == 0) {
+      tma_store_4d(&tm_dst, 0, bj0, 0, (int)(bi * ROWS_LEAF + r), ring + s * STAGE);
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+    const unsigned st = ring + s * STAGE + lane_off;
+    uint4 w[PIECES * 8];
+#pragma unroll
+    for (int j = 0; j < PIECES; ++j)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const unsigned a = st + j * 4096 + (((unsigned)c ^ sw) << 4);
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                     : "=r"(w[j * 8 + c].x), "=r"(w[j * 8 + c].y), "=r"(w[j * 8 + c].z), "=r"(w[j * 8 + c].w)
+                     : "r"(a));
+      }
+#pragma unroll
+    for (int u = 0; u < PIECES * 8; ++u) {
+      const T *x = reinterpret_cast<const T *>(&w[u]);
+#pragma unroll
+      for (int e = 0; e < EPS; ++e) accum<T>(acc, bits, x[e]);
+    }
+    if (fuse && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0 && q + R < Q) issue(q + R);
+    if (r == 63) {  // the group's last row: publish the leaf
+      const int64_t bj = bj0 + lane;
+      const int64_t leaf = bi * nb + bj;
+      const bool nz = (U)(bits << 1) != 0;
+      nsq_leaf[leaf] = acc;
+      occ_leaf[leaf] = (uint8_t)nz;
+      nrm_leaf[leaf] = __dsqrt_rn(acc);
+      const bool canon = !nz && bits;  // only -0.0 entries: stored as +0.0 (quadtree.py:127-129)
+      if (__any_sync(0xffffffffu, canon)) {
+        if (fuse) {  // the tree's copy of the leaf must have landed first
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+          __syncwarp();
+          asm volatile("fence.proxy.async;\n" ::: "memory");
+        }
+        canonicalise_leaves_warp<T>(padded, N, ROWS_LEAF, nb, canon, leaf);
+      }
+      acc = 0.0;
+      bits = 0;
+    }
+  }
+  if (fuse && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  if (dbg && lane == 0) {
+    unsigned long long *d = dbg + 3 * (blockIdx.x * ROWS_WARPS + warp);
+    d[0] = (unsigned long long)t_wait;
+    d[1] = (unsigned long long)(clock64() - t_begin);
+    d[2] = (unsigned long long)Q;
   }
 }
 
@@ -1194,6 +1389,37 @@ __global__ void __launch_bounds__(PYR_THREADS) pyramid_fused_kernel(double *__re
 // kernel) makes it a programmatic dependent launch that overlaps that kernel
 // and waits per C block; its ring is then only 4 stages deep so one K1 CTA
 // fits beside the leaf kernel on every SM.
+// 4-D view of an N-row f64/f32 matrix for the rows kernel: {128 bytes of a
+// leaf row, leaf index along the matrix row, 128-byte piece of the leaf row,
+// matrix row}; box {128 B, 32 leaves, all pieces, 1 row}, 128-byte swizzle.
+// (The strides are not monotonic; a driver that rejects the encoding leaves
+// the staged kernel in charge.)
+static PFN_cuTensorMapEncodeTiled_v12000 rows_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+template <typename T>
+static bool rows_map(CUtensorMap *map, const void *base, int64_t nb, int64_t rows, int64_t ld) {
+  auto enc = rows_map_encoder();
+  if (!enc || ((uintptr_t)base & 15) || (ld * sizeof(T)) % 16) return false;
+  constexpr cuuint32_t E = 128 / sizeof(T), PIECES = ROWS_LEAF * sizeof(T) / 128;
+  cuuint64_t dims[4] = {E, (cuuint64_t)nb, PIECES, (cuuint64_t)rows};
+  cuuint64_t strides[3] = {ROWS_LEAF * sizeof(T), 128, (cuuint64_t)(ld * sizeof(T))};
+  cuuint32_t box[4] = {E, 32, PIECES, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+             const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct K1Overlap {
   unsigned *grp_done;
   unsigned grp_target;
@@ -1284,7 +1510,48 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
     // leaves per CTA, two CTAs per SM.
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
-    if (ov && ov->grp_done)
+    // dense builds of large leaf-64 trees: the TMA-fed persistent rows kernel
+    // (SPAMM_K1_ROWS=0: the staged kernel; =2/4: ring depth, 3 by default)
+    static const int rows_r = getenv("SPAMM_K1_ROWS") ? atoi(getenv("SPAMM_K1_ROWS")) : 3;
+    const bool rows_ok = rows_r > 0 && !list && t->leaf == ROWS_LEAF && t->nb % 32 == 0 &&
+                         n_leaves >= (int64_t)64 * sms && !(ov && (ov->grp_done || ov->t_end)) &&
+                         (!(ov && ov->fuse_src) || (ov->fuse_ld * sizeof(T)) % 16 == 0);
+    CUtensorMap tm_src, tm_dst;
+    const T *rows_src = ov && ov->fuse_src ? (const T *)ov->fuse_src : (const T *)t->padded;
+    const int64_t rows_sld = ov && ov->fuse_src ? ov->fuse_ld : t->N;
+    if (rows_ok && rows_map<T>(&tm_src, rows_src, t->nb, t->N, rows_sld) &&
+        rows_map<T>(&tm_dst, t->padded, t->nb, t->N, t->N)) {
+      int gpr_shift = 0;
+      while (((int64_t)32 << gpr_shift) < t->nb) ++gpr_shift;
+      const int64_t groups = t->nb << gpr_shift;
+      const unsigned grid = (unsigned)std::min<int64_t>(sms, (groups + ROWS_WARPS - 1) / ROWS_WARPS);
+      auto go = [&](auto kern, int R) -> int {
+        const size_t smem = (size_t)ROWS_WARPS * R * 32 * ROWS_LEAF * sizeof(T) + 1024;
+        SPAMM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, 32 * ROWS_WARPS, smem, st>>>(tm_src, tm_dst, rows_src != (const T *)t->padded ? 1 : 0,
+                                                  (T *)t->padded, t->N, t->nb, gpr_shift, nsq_leaf, occ_leaf,
+                                                  t->nrm + level_offset(t->depth));
+        return SPAMM_OK;
+      };
+      static const bool rows_debug = getenv("SPAMM_K1_ROWS_DEBUG") != nullptr;
+      static unsigned long long *dbg_dev = nullptr;
+      if (rows_debug && !dbg_dev) {
+        cudaMalloc(&dbg_dev, sizeof(unsigned long long) * 3 * ROWS_WARPS * 1024);
+        cudaMemcpyToSymbol(g_rows_dbg, &dbg_dev, sizeof(void *));
+      }
+      if (rows_r == 2) SPAMM_TRY(go(leaf_norm_rows_kernel<T, 2>, 2));
+      else if (rows_r == 4 && sizeof(T) == 4) SPAMM_TRY(go(leaf_norm_rows_kernel<T, 4>, 4));
+      else SPAMM_TRY(go(leaf_norm_rows_kernel<T, 3>, 3));
+      if (rows_debug) {
+        cudaStreamSynchronize(st);
+        std::vector<unsigned long long> h(3 * ROWS_WARPS * grid);
+        cudaMemcpy(h.data(), dbg_dev, h.size() * 8, cudaMemcpyDeviceToHost);
+        double wt = 0, tot = 0, ch = 0;
+        for (size_t i = 0; i < h.size(); i += 3) { wt += h[i]; tot += h[i + 1]; ch += h[i + 2]; }
+        fprintf(stderr, "[k1 rows] warps=%zu chunks/warp %.0f: cycles per chunk %.0f, of which waiting for data %.0f\n",
+                h.size() / 3, ch / (h.size() / 3), tot / ch, wt / ch);
+      }
+    } else if (ov && ov->grp_done)
       SPAMM_TRY((launch_staged<T, 12, 8>(t, st, list, list_count, n_leaves, ticket, ov, fused)));
     else if (n_leaves >= (int64_t)64 * sms && k1_big_stages() == 4)
       SPAMM_TRY((launch_staged<T, 4, 32>(t, st, list, list_count, n_leaves, ticket, ov, fused)));

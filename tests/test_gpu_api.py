@@ -564,6 +564,40 @@ def test_from_device_pointer_fused_and_copy_paths(n, ld_pad):
     assert np.array_equal(t._pyramid()[3], ref._pyramid()[3])
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,mode", [(np.float64, "host"), (np.float64, "device"),
+                                        (np.float64, "device_ld"), (np.float32, "host")])
+def test_dense_rows_build_matches_oracle(dtype, mode):
+    """Large dense builds (leaf 64, >= 64 leaves per SM: the TMA-fed rows
+    kernel, in place after a host copy or fused with the copy from a device
+    source) give the oracle's pyramid bit for bit and the source's storage,
+    with empty leaves, a leaf holding only -0.0 (canonicalised) and NaN."""
+    import torch
+    from oracle import oracle
+
+    n, leaf = 8192, 64
+    rng = np.random.default_rng(17)
+    host = (rng.uniform(-1, 1, (n, n)) * np.exp(-rng.uniform(0, 30, (n, n)))).astype(dtype)
+    host[128:192, :] = 0                      # a whole empty block row
+    host[640:704, 64:128] = 0
+    host[650, 70] = -0.0                      # only -0.0 in this leaf
+    host[1000, 3000] = np.nan
+    host[4097, 4095] = 1e-200                 # square underflows to a subnormal
+    if mode == "host":
+        t = sp.from_dense(host, leaf_size=leaf, dtype=dtype)
+    else:
+        pad = 2 if mode == "device_ld" else 0
+        dev = torch.zeros((n, n + pad), dtype=torch.float64, device="cuda")
+        dev[:, :n] = torch.from_numpy(host).cuda()
+        t = sp.from_device_pointer(dev.data_ptr(), n, leaf_size=leaf, ld=n + pad)
+    want = host.copy()
+    nsq, occ = oracle.build_pyramid(want, leaf)   # canonicalises `want` in place
+    u = np.uint64 if dtype == np.float64 else np.uint32
+    assert np.array_equal(t._pyramid()[2].view(np.uint64), nsq.view(np.uint64))
+    assert np.array_equal(t._pyramid()[3], occ)
+    assert np.array_equal(t._padded.view(u), want.view(u))
+
+
 @pytest.mark.parametrize("traversal", ["auto", "tiered"])
 @pytest.mark.parametrize("dtype,leaf", [(np.float64, 32), (np.float32, 32), (np.float64, 16)])
 def test_need_blocks_match_retained_triples(traversal, dtype, leaf):

@@ -8,7 +8,10 @@ import paper_1011_3534_b200 as sp
 from paper_1011_3534_b200 import workloads
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-if name in workloads.DEVICE_CONFIGS:
+if name.startswith("rand"):  # uniform(0.5, 1.5) entries, n = name[4:]: no tiny values anywhere
+    at = torch.rand((int(name[4:]), int(name[4:])), dtype=torch.float64, device="cuda") + 0.5
+    leaf = 64
+elif name in workloads.DEVICE_CONFIGS:
     at, _, leaf, _ = workloads.make_config_device(name, "cuda:0")
 else:
     a_h, _, leaf, _ = workloads.make_config(name)

@@ -24,7 +24,11 @@ __global__ void ldg_sum(const double2 *__restrict__ p, size_t n2, double *out) {
 __device__ __forceinline__ unsigned sa(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 template <int STAGES, int CHUNK>
-__global__ void __launch_bounds__(64) bulk_sum(const char *__restrict__ p, size_t bytes, double *out) {
+__global__ void __launch_bounds__(64) bulk_sum(const char *__restrict__ p, size_t bytes, double *out, int rows = 0) {
+  // rows != 0: K1's dense-build pattern on an N = 65536 f64 matrix (512 KB per
+  // row): chunk c = (group, r) reads the 16 KB of row r of a 32-leaf group;
+  // rows == 1: a CTA streams whole groups (64 rows, 512 KB apart);
+  // rows == 2: the same with four adjacent CTAs sharing a block row's pages
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const size_t nchunks = bytes / CHUNK;
@@ -48,8 +52,15 @@ __global__ void __launch_bounds__(64) bulk_sum(const char *__restrict__ p, size_
                        ::"r"(sa(&empty[s])), "r"(par));
         }
         asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(sa(&full[s])), "r"(CHUNK));
+        size_t off = c * CHUNK;
+        if (rows) {
+          // the CTA's it-th chunk: group blockIdx.x + (it / 64) * gridDim.x, row it % 64
+          const size_t g = blockIdx.x + (size_t)(it / 64) * gridDim.x, r = it % 64;
+          off = ((g / 32) * 64 + r) * (size_t)(65536 * 8) + (g % 32) * (size_t)16384;
+          if (off + CHUNK > bytes) off = 0;
+        }
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(sa(smem + s * CHUNK)), "l"(p + c * CHUNK), "r"(CHUNK), "r"(sa(&full[s])) : "memory");
+                     ::"r"(sa(smem + s * CHUNK)), "l"(p + off), "r"(CHUNK), "r"(sa(&full[s])) : "memory");
       }
     }
   } else {
@@ -70,7 +81,7 @@ __global__ void __launch_bounds__(64) bulk_sum(const char *__restrict__ p, size_
 }
 
 template <int STAGES, int CHUNK>
-static void run_bulk(const char *p, size_t bytes, double *out, int ctas_per_sm, int sms) {
+static void run_bulk(const char *p, size_t bytes, double *out, int ctas_per_sm, int sms, int rows = 0) {
   auto k = bulk_sum<STAGES, CHUNK>;
   const int sm = STAGES * CHUNK;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -79,14 +90,14 @@ static void run_bulk(const char *p, size_t bytes, double *out, int ctas_per_sm, 
   float best = 1e30f;
   for (int r = 0; r < 5; ++r) {
     cudaEventRecord(a);
-    k<<<sms * ctas_per_sm, 64, sm>>>(p, bytes, out);
+    k<<<sms * ctas_per_sm, 64, sm>>>(p, bytes, out, rows);
     cudaEventRecord(b);
     CK(cudaEventSynchronize(b));
     float ms; cudaEventElapsedTime(&ms, a, b);
     if (ms < best) best = ms;
   }
   CK(cudaGetLastError());
-  printf("bulk stages=%d chunk=%d ctas/sm=%d: %.3f ms %.0f GB/s\n", STAGES, CHUNK, ctas_per_sm, best,
+  printf("bulk%s stages=%d chunk=%d ctas/sm=%d: %.3f ms %.0f GB/s\n", rows ? " (K1 row pattern)" : "", STAGES, CHUNK, ctas_per_sm, best,
          bytes / (best * 1e-3) / 1e9);
 }
 
@@ -118,5 +129,9 @@ int main(int argc, char **argv) {
   run_bulk<3, 32768>(p, bytes, out, 2, sms);
   run_bulk<8, 8192>(p, bytes, out, 3, sms);
   run_bulk<4, 32768>(p, bytes, out, 1, sms);
+  run_bulk<3, 16384>(p, bytes, out, 4, sms);
+  run_bulk<3, 16384>(p, bytes, out, 4, sms, 1);
+  run_bulk<4, 16384>(p, bytes, out, 3, sms, 1);
+  run_bulk<6, 16384>(p, bytes, out, 2, sms, 1);
   return 0;
 }
