@@ -470,7 +470,9 @@ def run_b200(args, cfg_name):
                    "per_tau": table},
         "roofline": roofline,
         "clocks": clocks,
-        "gpu_launches": launches // max(args.steps, 1),
+        # this library's kernels launched inside the timed region (all K steps)
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches // max(args.steps, 1),
     }
 
     if rank == 0 and world == 1 and not args.profile and n <= 16384:

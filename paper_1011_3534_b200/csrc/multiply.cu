@@ -352,8 +352,13 @@ static int multiply_impl(const spamm_tree *a, const spamm_tree *b, double tau, u
     // Only for small block grids: the overlapped K1 runs one 8-leaf CTA per
     // SM, which suits ~1k C blocks (c2) but not 10^4-10^6 (c3, c5), where the
     // regular K1 (32 leaves per CTA, two per SM) finishes in fewer waves.
+    // (SPAMM_CTREE_OVERLAP_MAX: the largest block grid whose C tree runs
+    // beside K3 -- the segmented-chain kernel's 2-warp CTAs next to K3's CTA,
+    // leaves taken from a ticket in completion order)
     static const bool no_overlap = getenv("SPAMM_NO_CTREE_OVERLAP") != nullptr;
-    if (no_overlap || G > 4096) la.grp_done = nullptr;
+    static const int64_t overlap_max =
+        getenv("SPAMM_CTREE_OVERLAP_MAX") ? atoll(getenv("SPAMM_CTREE_OVERLAP_MAX")) : 4096;
+    if (no_overlap || G > overlap_max) la.grp_done = nullptr;
     static const bool k1tl = getenv("SPAMM_K1_TIMELINE") != nullptr;
     if (k1tl) k1_timeline_enable(st);
     bool overlapped = false;

@@ -67,6 +67,9 @@ struct PyrTail {
   // one level up (the parent level is zeroed by the traversal)
   const uint32_t *ne;
   unsigned *pcnt;
+  // trees deeper than PYR_TAIL_MAX_DEPTH beside K3: the last CTA only resets
+  // the tickets; the pyramid above the leaves is a launch of its own
+  int skip_pyramid;
 };
 
 __device__ __forceinline__ void spin_acquire_nonzero(const unsigned *flag) {

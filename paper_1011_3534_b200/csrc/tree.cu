@@ -871,7 +871,9 @@ __global__ void __launch_bounds__(32 * (W + H)) leaf_norm_seg_kernel(
       if (tail.trav_done && threadIdx.x == 0) spin_acquire_nonzero(tail.trav_done);
       __threadfence();
       if (k1_tl && threadIdx.x == 0) k1_tl[4 * 8191 + 1] = k1_gt();
-      if (tail.pcnt) {  // the leaves' parents are built: the pyramid from their level
+      if (tail.skip_pyramid) {
+        // (deep tree: pyramid_upper_async follows)
+      } else if (tail.pcnt) {  // the leaves' parents are built: the pyramid from their level
         PyrTail up = tail;
         up.depth = tail.depth - 1;
         pyramid_cta(up, seg_smem, smem_bytes, k1_tl ? k1_tl + 4 * 8190 : nullptr);
@@ -881,7 +883,7 @@ __global__ void __launch_bounds__(32 * (W + H)) leaf_norm_seg_kernel(
       if (threadIdx.x == 0) {
         *tail.ticket = 0u;
         if (tail.leaf_ticket) *tail.leaf_ticket = 0u;
-        if (tail.t_end) *tail.t_end = k1_gt();
+        if (tail.t_end && !tail.skip_pyramid) *tail.t_end = k1_gt();
         if (k1_tl) k1_tl[4 * 8191 + 2] = k1_gt();
       }
     }
@@ -1511,8 +1513,10 @@ static int launch_leaf_norms(spamm_tree *t, cudaStream_t st, const uint32_t *lis
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
     // dense builds of large leaf-64 trees: the TMA-fed persistent rows kernel
-    // (SPAMM_K1_ROWS=0: the staged kernel; =2/4: ring depth, 3 by default)
-    static const int rows_r = getenv("SPAMM_K1_ROWS") ? atoi(getenv("SPAMM_K1_ROWS")) : 3;
+    // (SPAMM_K1_ROWS=0: the staged kernel; =2/3/4: ring depth -- by default 3
+    // stages of 16 KB for f64 and 4 of 8 KB for f32)
+    static const int rows_env = getenv("SPAMM_K1_ROWS") ? atoi(getenv("SPAMM_K1_ROWS")) : -1;
+    const int rows_r = rows_env >= 0 ? rows_env : (sizeof(T) == 4 ? 4 : 3);
     const bool rows_ok = rows_r > 0 && !list && t->leaf == ROWS_LEAF && t->nb % 32 == 0 &&
                          n_leaves >= (int64_t)64 * sms && !(ov && (ov->grp_done || ov->t_end)) &&
                          (!(ov && ov->fuse_src) || (ov->fuse_ld * sizeof(T)) % 16 == 0);
@@ -1708,7 +1712,10 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
     tail.occ = t->occ;
     tail.nrm = t->nrm;
     tail.depth = t->depth;
-    tail.ticket = t->depth <= PYR_TAIL_MAX_DEPTH ? ticket : nullptr;
+    // (deeper trees: the ticket still elects the CTA that resets the leaf
+    // ticket; the levels above the leaves are pyramid_upper_async's)
+    tail.ticket = ticket;
+    tail.skip_pyramid = t->depth > PYR_TAIL_MAX_DEPTH;
     if (ov) {
       tail.grp_done = ov->grp_done;
       tail.grp_target = ov->grp_target;
@@ -1785,7 +1792,7 @@ int build_pyramid_async(DeviceContext *ctx, spamm_tree *t, cudaStream_t st, int 
     } else {
       SPAMM_TRY(f64 ? launch(leaf_norm_seg_kernel<double, 32>, pd) : launch(leaf_norm_seg_kernel<float, 32>, pf));
     }
-    fused = tail.ticket != nullptr;
+    fused = !tail.skip_pyramid;
   } else if (t->dtype == SPAMM_DTYPE_F64)
     SPAMM_TRY(launch_leaf_norms<double>(t, st, list, list_count, list_cap, ticket, ov, &fused));
   else
