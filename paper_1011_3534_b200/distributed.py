@@ -790,7 +790,7 @@ def tc2_step_sharded(x, n_occ, mode):
         x2, stats, _ = spamm_sharded(x, x, SpammConfig(tau=0.0))
     else:
         raise TypeError(f"sharded purification supports SpammMode (and DroppingMode(0)), got {mode!r}")
-    y, d_nsq, e_nsq = _tc2_pass(x, x2, make_y=tr < n_occ)
+    y, d_nsq, e_nsq = _tc2_pass(x, x2, make_y=not tr >= n_occ)  # NaN trace: 2X - X^2
     gap = float(np.sqrt(d_nsq))
     if gap <= _FIXED_POINT_FACTOR * np.finfo(x.dtype).eps * x.logical_dim:
         return x, stats, 0.0
