@@ -502,18 +502,21 @@ def test_chained_launch_path_is_deterministic():
     d = np.abs(np.subtract.outer(np.arange(n), np.arange(n)))
     u = rng.uniform(-1, 1, (n, n)) * 0.95 ** d
     a = sp.from_dense(0.5 * (u + u.T), leaf_size=leaf)
-    ref = None
-    for _ in range(12):
-        c, st = sp.spamm(a, a, sp.SpammConfig(tau=1e-6))
+    # tau alternates call after call, so each call's group list differs from
+    # the one the previous call left in the scratch buffers: a dependent that
+    # read them too early could not pass by seeing an identical stale list
+    refs = {}
+    for it in range(16):
+        tau = (1e-6, 1e-9)[it & 1]
+        c, st = sp.spamm(a, a, sp.SpammConfig(tau=tau))
         pyr = np.concatenate([lv.reshape(-1) for lv in c._norm_sq]).view(np.uint64)
         ids, blocks = c.nonzero_blocks()
         got = (st.leaf_matmuls, pyr.copy(), ids.copy(), blocks.view(np.uint64).copy())
-        if ref is None:
-            ref = got
-            continue
+        ref = refs.setdefault(tau, got)
         assert got[0] == ref[0]
         assert np.array_equal(got[1], ref[1])
         assert np.array_equal(got[2], ref[2]) and np.array_equal(got[3], ref[3])
+    assert refs[1e-6][0] < refs[1e-9][0]
 
 
 @pytest.mark.gpu
